@@ -1,0 +1,127 @@
+"""ORACLE (test infrastructure only) — pipeline instantiation and batch distribution,
+PAPER.md §4.2.  Plain definitions written out; exponential where the
+definition is (small inputs only).
+
+* `enumerate_sets`: Eq.5 (`eq:instantiation_dp`) literally —
+  X(p', N') = X(p'-1, N') ++ theta(X(p', N' - n_{p'}), p'), then the Requirement-2 filter
+  sum x >= f+1.
+* `enumerate_sets_brute`: nested loops over every x_i <= N'/n_i (pin for Eq.5).
+* `distribute_batch_brute`: Eq.6 (`eq:nonlinear_optimization`) by enumerating
+  every integer assignment N_{b,i} >= 1 with sum N_{b,i} b = B (reading R18); T_i is the
+  pipeline's per-microbatch steady cost t* (reading R19).
+* `recommend_batch`: smallest distributable B' >= B.
+* `iteration_ms`: T1 + (N_b - S + k* - 1) t* + T3 (Eq.2 with the real N_b).
+* `select_plan_brute`: max-throughput plan over all feasible sets.
+"""
+from __future__ import annotations
+
+from .brute import compositions
+
+
+def enumerate_sets(sizes, Nprime: int, f: int):
+    """Eq.5 with list concatenation; returns the feasible X (tuples), filtered by f."""
+    p = len(sizes)
+    memo = {}
+
+    def X(pp: int, n: int):
+        # pp = index of the last template allowed (-1: none)
+        if n < 0:
+            return []
+        if pp < 0:
+            return [tuple([0] * p)] if n == 0 else []
+        key = (pp, n)
+        if key in memo:
+            return memo[key]
+        keep = X(pp - 1, n)                          # X(p'-1, N')
+        add = []
+        for x in X(pp, n - sizes[pp]):               # theta(X(p', N' - n_p'), p')
+            y = list(x)
+            y[pp] += 1
+            add.append(tuple(y))
+        memo[key] = keep + add                       # concatenation
+        return memo[key]
+
+    return [x for x in X(p - 1, Nprime) if sum(x) >= f + 1]
+
+
+def enumerate_sets_brute(sizes, Nprime: int, f: int):
+    out = []
+
+    def rec(i, rem, cur):
+        if i == len(sizes):
+            if rem == 0 and sum(cur) >= f + 1:
+                out.append(tuple(cur))
+            return
+        for x in range(rem // sizes[i] + 1):
+            rec(i + 1, rem - x * sizes[i], cur + [x])
+    rec(0, Nprime, [])
+    return out
+
+
+def variance_objective(nb, T):
+    """sum_i (N_{b,i} T_i - mean)^2 (Eq.6 objective)."""
+    y = [n * t for n, t in zip(nb, T)]
+    mean = sum(y) / len(y)
+    return sum((v - mean) ** 2 for v in y)
+
+
+def distribute_batch_brute(T, B: int, b: int):
+    """Exact Eq.6 by enumeration; returns (nb tuple, objective) or raises ValueError."""
+    x = len(T)
+    if B % b != 0 or B // b < x:
+        raise ValueError("infeasible distribution")
+    K = B // b
+    best = None
+    for nb in compositions(K, x):
+        obj = variance_objective(nb, T)
+        if best is None or obj < best[1]:
+            best = (nb, obj)
+    return best
+
+
+def recommend_batch(x: int, b: int, B: int) -> int:
+    Bp = max(B, x * b)
+    if Bp % b:
+        Bp += b - Bp % b
+    return Bp
+
+
+def iteration_ms(tpl, Nb: int) -> float:
+    S = tpl["S"]
+    return (tpl["T1"] + float(Nb - S + tpl["kstar"] - 1) * tpl["tstar"]) + tpl["T3"]
+
+
+def select_plan_brute(templates, Nprime: int, f: int, B: int, b: int):
+    """Best plan over every Eq.5 set: (throughput, counts, nb) — highest throughput, then
+    fewer pipelines, then lexicographically smallest counts."""
+    sizes = [t["nodes"] for t in templates]
+    best = None
+    for X in enumerate_sets_brute(sizes, Nprime, f):
+        pipes = []
+        for i, cnt in enumerate(X):
+            pipes += [templates[i]] * cnt
+        try:
+            nb, _ = distribute_batch_brute([t["tstar"] for t in pipes], B, b)
+        except ValueError:
+            continue
+        it = max(iteration_ms(t, n) for t, n in zip(pipes, nb))
+        thr = B / it
+        key = (-thr, sum(X), X)
+        if best is None or key < best[0]:
+            best = (key, thr, X, nb)
+    if best is None:
+        return None
+    return best[1], best[2], best[3]
+
+
+def coverage_ok(sizes, lo: int, hi: int, f: int) -> bool:
+    """Every N' in [lo, hi] is a combination of sizes with >= f+1 pipelines (App. A),
+    by exhaustive reachability: most[n] = max number of pipelines summing to n."""
+    NEG = -1
+    most = [NEG] * (hi + 1)
+    most[0] = 0
+    for n in range(1, hi + 1):
+        for s in sizes:
+            if s <= n and most[n - s] != NEG:
+                most[n] = max(most[n], most[n - s] + 1)
+    return all(most[Np] >= f + 1 for Np in range(lo, hi + 1))
