@@ -1,0 +1,209 @@
+/*
+ * oobleck_plan.h — C ABI of the B200-native Oobleck pipeline-template planner.
+ *
+ * The library (paper_2309_08125_b200/liboobleck_plan.so) implements the planning path of
+ * Oobleck (arXiv 2309.08125, §4): pipeline-template generation — the memoized
+ * divide-and-conquer GPU-stage mapping of §4.1.2 (Eqs.1-4) run for every
+ * template node count of the node specification (§4.1.1) — as sm_100a CUDA
+ * kernels, plus the host-side instantiation (Eq.5, §4.2.1) and batch
+ * distribution (Eq.6, §4.2.2) that consume the template set.
+ *
+ * Conventions
+ *  - Every function returns an oob_status (OOB_OK = 0) unless stated; on failure a
+ *    human-readable message is available from oob_last_error() (thread-local, valid until
+ *    the next call on the same thread).  No C++ exception crosses this boundary.
+ *  - "host" pointers are ordinary CPU memory; "device" pointers are CUDA global memory on
+ *    the current device (e.g. torch tensors' data_ptr()).  Streams are cudaStream_t passed
+ *    as void* (NULL = legacy default stream).
+ *  - Opaque handles (oob_profile, oob_template_set, oob_dp_plan) are created and freed by
+ *    the library.  Profiles and template sets are immutable after creation and may be
+ *    shared read-only across threads.  An oob_dp_plan must not be used concurrently.
+ *  - Per-layer costs are milliseconds, binary64, row-major [L][M]: element [l*M + d-1] is
+ *    the cost of layer l on d GPUs of one node (F_{l,d} and B_{l,d}).
+ *  - Arithmetic contract: all DP arithmetic is IEEE binary64, round-to-nearest, without
+ *    FMA contraction, in the operation order stated in DESIGN.md; results are bit-identical
+ *    to oracle/ (tests/).
+ */
+#ifndef OOBLECK_PLAN_H
+#define OOBLECK_PLAN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    OOB_OK = 0,
+    OOB_E_PARSE = 1,       /* malformed profile JSON */
+    OOB_E_INVALID = 2,     /* bad argument: empty model, non-positive time, missing d, L>1023 */
+    OOB_E_INFEASIBLE = 3,  /* N < (f+1) n0; n0 > L */
+    OOB_E_BATCH = 4,       /* B % b != 0 or B/b < pipelines; see recommended */
+    OOB_E_TOO_MANY = 5,    /* Eq.5 enumeration exceeded max_enumerated (plan is best-so-far) */
+    OOB_E_CUDA = 6,        /* CUDA runtime/launch failure */
+    OOB_E_NCCL = 7,        /* reserved: collective failure */
+    OOB_E_NOMEM = 8        /* host allocation or workspace too small */
+} oob_status;
+
+typedef struct oob_profile oob_profile;
+typedef struct oob_template_set oob_template_set;
+typedef struct oob_dp_plan oob_dp_plan;
+
+/* One pipeline stage of a template: layers [layer_begin, layer_end) on
+ * `gpus` GPUs of node `node` (0..n-1, template-local), starting at GPU `gpu_offset`. */
+typedef struct {
+    int32_t layer_begin, layer_end, gpus, node, gpu_offset;
+} oob_stage;
+
+/* A pipeline template.  T1/T2/T3 per Eqs.1-3 at N_b = 4S,
+ * kstar = 0-based index of the slowest stage, tstar_ms its F+B, iter_ms = (T1+T2)+T3.
+ * `stages` borrows from the owning oob_template_set. */
+typedef struct {
+    int32_t nodes, num_stages, kstar, reserved;
+    double t1_ms, t2_ms, t3_ms, tstar_ms, iter_ms;
+    const oob_stage *stages;
+} oob_template;
+
+/* Options of oob_generate_templates. */
+typedef struct {
+    int32_t nodes;              /* N: initial node count */
+    int32_t gpus_per_node;      /* M; must equal every profile's M */
+    int32_t f;                  /* fault-tolerance threshold */
+    int32_t n0;                 /* smallest template; <= 0: derive with oob_min_nodes */
+    int64_t gpu_mem_bytes;      /* used only when n0 <= 0 */
+    double util;                /* usable memory fraction when n0 <= 0 (0: default 0.8) */
+    int32_t samples_per_gpu;    /* activation multiplier when n0 <= 0 (0: default 1) */
+    int32_t device;             /* CUDA device ordinal (< 0: current device) */
+    void *stream;               /* cudaStream_t for all device work (NULL: default) */
+    void *workspace;            /* optional caller-owned device memory (NULL: library
+                                   allocates and frees it inside the call) */
+    size_t workspace_bytes;     /* size of `workspace` (>= oob_dp_plan_info.workspace_bytes) */
+} oob_plan_opts;
+
+/* ------------------------------------------------------------------ errors */
+const char *oob_last_error(void);
+const char *oob_status_string(oob_status s);
+
+/* ------------------------------------------------------------------ profiles */
+/* Parse the profile JSON of SPEC S:99:
+ *  {"gpus_per_node": M, "microbatch_reference": b, "layers": [{"name": s, "state_bytes": i,
+ *   "activation_bytes_per_sample": i, "fwd_ms": {"1": f, ..., "M": f}, "bwd_ms": {...}}]}
+ * Errors: OOB_E_PARSE (syntax), OOB_E_INVALID (no layers, missing d entry, time <= 0). */
+oob_status oob_load_profile(const char *json_path, oob_profile **out);
+
+/* Profile from host arrays fwd_ms/bwd_ms [L][M] (copied); state_bytes [L] may be NULL.
+ * Errors: OOB_E_INVALID (L < 1, L > 1023, M < 1, M > 64, non-finite or non-positive time). */
+oob_status oob_profile_from_arrays(int32_t L, int32_t M, const double *fwd_ms,
+                                   const double *bwd_ms, const int64_t *state_bytes,
+                                   oob_profile **out);
+void oob_profile_free(oob_profile *p);
+int32_t oob_profile_layers(const oob_profile *p);
+int32_t oob_profile_gpus_per_node(const oob_profile *p);
+
+/* SPEC min_nodes (P:335 gives no formula; DESIGN reading R5):
+ * n0 = ceil((sum state_bytes + samples_per_gpu * sum act_bytes) / (M * gpu_mem * util)).
+ * Errors: OOB_E_INFEASIBLE when the model does not fit on `nodes` nodes. */
+oob_status oob_min_nodes(const oob_profile *p, int32_t nodes, int64_t gpu_mem_bytes,
+                         double util, int32_t samples_per_gpu, int32_t *n0_out);
+
+/* Node specification: sizes n0 .. min(N - f n0, L) (reading R4).
+ * Writes n_lo/n_hi.  Errors: OOB_E_INFEASIBLE if N < (f+1) n0 or n0 > L. */
+oob_status oob_node_sizes(int32_t nodes, int32_t f, int32_t n0, int32_t layers,
+                          int32_t *n_lo, int32_t *n_hi);
+
+/* ------------------------------------------------------------------ template generation
+ * For every profile and every size n in the node specification, one template: the
+ * argmin over S in n..min(L, nM) of the memoized recursion T(S, 0, L, W(n))
+ * (Eqs.1-4).  Runs on the GPU (sm_100a): host arrays are copied to the device, the DP
+ * wavefronts run, the packed templates are copied back.  `profiles` are num_profiles
+ * handles with identical L and M (batched sweep).  Errors: OOB_E_INVALID, OOB_E_INFEASIBLE,
+ * OOB_E_CUDA, OOB_E_NOMEM. */
+oob_status oob_generate_templates(const oob_profile *const *profiles, int32_t num_profiles,
+                                  const oob_plan_opts *opts, oob_template_set **out);
+int32_t oob_template_set_profiles(const oob_template_set *s);
+int32_t oob_template_count(const oob_template_set *s, int32_t profile);
+/* Fills *view for template i (size n = n_lo + i) of `profile`; view->stages borrows. */
+oob_status oob_template_get(const oob_template_set *s, int32_t profile, int32_t i,
+                            oob_template *view);
+void oob_template_set_free(oob_template_set *s);
+
+/* ------------------------------------------------------------------ device-resident DP
+ * The same computation on inputs already in device memory (the hot path timed by
+ * bench.py).  A plan holds the index geometry for (L, M, n_lo, n_hi, num_profiles).
+ *   d_fwd, d_bwd: device float64 [num_profiles][L][M]
+ *   d_workspace : device memory of >= info.workspace_bytes (caller-owned, e.g. torch)
+ *   d_packed    : device memory of >= info.packed_bytes receiving the packed templates:
+ *     per profile p, template i: a 64-byte header
+ *       {int32 nodes, S, kstar, status; double T1, T2, T3, tstar, iter}
+ *     followed by L records {int32 layer_begin, layer_end, gpus, node, gpu_offset};
+ *     stride info.packed_template_bytes, profile stride info.packed_profile_bytes.
+ * Kernels are enqueued on `stream`; the call returns without synchronizing. */
+typedef struct {
+    int32_t L, M, n_lo, n_hi, num_profiles, wavefronts;
+    int64_t cells_per_profile;      /* DP cells in the table universe */
+    int64_t splits_per_profile;     /* feasible split evaluations (the roofline unit) */
+    int64_t kernel_launches;        /* device kernels launched per oob_dp_run */
+    size_t workspace_bytes;
+    size_t packed_template_bytes, packed_profile_bytes, packed_bytes;
+} oob_dp_info;
+
+oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int32_t n_hi,
+                              int32_t num_profiles, oob_dp_plan **out);
+void oob_dp_plan_free(oob_dp_plan *plan);
+oob_status oob_dp_plan_info(const oob_dp_plan *plan, oob_dp_info *out);
+oob_status oob_dp_run(oob_dp_plan *plan, const double *d_fwd, const double *d_bwd,
+                      void *d_workspace, size_t workspace_bytes, void *d_packed, void *stream);
+/* Optional CUDA-event timing of the wavefront kernel (the dominant kernel): when enabled,
+ * oob_dp_run records events around each wavefront launch on `stream`; oob_dp_kernel_time
+ * returns the summed elapsed ms and number of launches since the last reset (it
+ * synchronizes on the recorded events). */
+oob_status oob_dp_set_timing(oob_dp_plan *plan, int32_t enable);
+oob_status oob_dp_kernel_time(oob_dp_plan *plan, double *ms_out, int64_t *launches_out,
+                              int32_t reset);
+/* Build a template set from a HOST copy of the packed output (d_packed copied back). */
+oob_status oob_template_set_from_packed(const void *h_packed, const oob_dp_info *info,
+                                        oob_template_set **out);
+
+/* ------------------------------------------------------------------ instantiation (Eq.5)
+ * Best plan for `nodes` available nodes: enumerate every X with
+ * sum x_i n_i = N' and sum x_i >= f+1 (Eq.5), distribute the batch for each (Eq.6), and
+ * keep the highest throughput B / max_i iteration_ms(N_b,i) (iteration_ms = T1 +
+ * (N_b - S + k* - 1) t* + T3); ties: fewer pipelines, then lexicographically
+ * smallest counts.
+ *  counts_out   : caller-owned int32 [oob_template_count] — x_i per template
+ *  nb_out       : caller-owned int64 [max_pipelines] — N_b per pipeline, pipelines ordered
+ *                 by template index; *num_pipelines_out receives sum x_i
+ *  throughput_out, iter_ms_out: of the chosen plan (samples per ms, ms)
+ *  num_feasible_out: number of feasible X (saturates at INT64_MAX)
+ * max_enumerated <= 0 means 1e6.  Errors: OOB_E_INFEASIBLE (N' < (f+1) n0 or no X),
+ * OOB_E_BATCH (no X can be distributed; *recommended_batch_out is set), OOB_E_TOO_MANY
+ * (more than max_enumerated X: outputs hold the best of the first max_enumerated),
+ * OOB_E_NOMEM (max_pipelines too small). */
+oob_status oob_instantiate(const oob_template_set *set, int32_t profile, int32_t nodes,
+                           int32_t f, int64_t global_batch, int32_t microbatch,
+                           int64_t max_enumerated, int32_t *counts_out, int64_t *nb_out,
+                           int32_t max_pipelines, int32_t *num_pipelines_out,
+                           double *throughput_out, double *iter_ms_out,
+                           int64_t *num_feasible_out, int64_t *recommended_batch_out);
+
+/* Number of X satisfying Eq.5's Requirements 1-2 for sizes n_lo..n_hi (saturating). */
+oob_status oob_count_sets(int32_t n_lo, int32_t n_hi, int32_t nodes, int32_t f,
+                          int64_t *count_out);
+
+/* ------------------------------------------------------------------ batch distribution (Eq.6)
+ * Exact integer minimiser of sum_i (N_b,i T_i - mean)^2 s.t. sum_i N_b,i b = B,
+ * N_b,i >= 1 (reading R18), T_i = per-microbatch time of pipeline i (reading
+ * R19: the slowest stage's F+B).  per_microbatch_ms: host [x]; nb_out: caller-owned
+ * int64 [x]; objective_out may be NULL.  Errors: OOB_E_INVALID (x < 1, b < 1, T_i <= 0),
+ * OOB_E_BATCH (B % b != 0 or B/b < x; *recommended_batch_out = smallest distributable
+ * B' >= B, P:549-551 / SPEC S:247-255). */
+oob_status oob_distribute_batch(const double *per_microbatch_ms, int32_t x,
+                                int64_t global_batch, int32_t microbatch, int64_t *nb_out,
+                                double *objective_out, int64_t *recommended_batch_out);
+int64_t oob_recommend_batch(int32_t x, int32_t microbatch, int64_t global_batch);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OOBLECK_PLAN_H */

@@ -1,0 +1,72 @@
+"""Builds paper_2309_08125_b200/liboobleck_plan.so in-tree (sm_100a, no GPU needed).
+
+nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo --fmad=false for the CUDA DP engine;
+g++ -ffp-contract=off for the host planner; cudart linked statically.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INC = os.path.join(ROOT, "include")
+BUILD = os.path.join(ROOT, "build")
+LIB = os.path.join(PKG, "liboobleck_plan.so")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA, "bin", "nvcc")
+
+CU_SOURCES = ["oob_dp.cu"]
+CPP_SOURCES = ["oob_host.cpp", "oob_geometry.cpp", "oob_instantiate.cpp"]
+HEADERS = [os.path.join(CSRC, "oob_internal.h"), os.path.join(INC, "oobleck_plan.h")]
+
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false",
+              "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-I", INC, "-I", CSRC]
+CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall",
+             "-I", INC, "-I", CSRC, "-I", os.path.join(CUDA, "include")]
+
+
+def _stale(obj: str, src: str) -> bool:
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    return any(os.path.getmtime(p) > t for p in [src] + HEADERS)
+
+
+def _run(cmd, log):
+    r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+    if log is not None:
+        log.append(r.stdout)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout)
+        raise RuntimeError("build failed: " + " ".join(cmd))
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    objs = []
+    log: list[str] = []
+    for src in CU_SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(BUILD, src + ".o")
+        if force or _stale(o, s):
+            _run([NVCC] + NVCC_FLAGS + ["-c", s, "-o", o], log)
+        objs.append(o)
+    for src in CPP_SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(BUILD, src + ".o")
+        if force or _stale(o, s):
+            _run(["g++"] + CXX_FLAGS + ["-c", s, "-o", o], log)
+        objs.append(o)
+    if force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
+        _run([NVCC, "-shared", "-o", LIB] + objs + ["-cudart", "static", "-gencode",
+                                                     "arch=compute_100a,code=sm_100a"], log)
+    if verbose:
+        print("\n".join(x for x in log if x.strip()))
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

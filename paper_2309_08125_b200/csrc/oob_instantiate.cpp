@@ -1,0 +1,269 @@
+// Pipeline instantiation (Eq.5, PAPER §4.2.1) and batch distribution (Eq.6,
+// §4.2.2) on the host, over a template set produced by the CUDA DP.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <limits>
+#include <vector>
+
+#include "oob_internal.h"
+
+using namespace oob;
+
+namespace {
+
+// ---------------------------------------------------------------- Eq.6 exact solver
+// Minimise sum_i (N_i T_i - mean)^2 with sum N_i = K, N_i >= 1 (DESIGN.md "Batch
+// distribution").  Pipelines with equal T form a group g (value tau_g, c_g members); at an
+// optimum their counts differ by at most 1, so a group is described by its total M_g.
+// For a fixed mean mu the problem is separable convex in M_g and solved by greedy
+// marginals delta_g(M) = tau_g^2 (2 floor(M / c_g) + 1) - 2 mu tau_g; sweeping mu from
+// -inf to +inf moves single units from smaller-tau to larger-tau groups at the crossing
+// points, visiting every allocation that is optimal for some mu.  The global optimum is
+// optimal for mu = its own mean, so the best true objective among visited allocations is
+// exact.
+struct Group {
+    double tau;
+    int64_t c;
+    int64_t Mg;
+    std::vector<int> members;
+};
+
+double group_objective(const std::vector<Group> &gs, int64_t x) {
+    double sum = 0.0;
+    for (auto &g : gs) sum += (double)g.Mg * g.tau;
+    const double mean = sum / (double)x;
+    double obj = 0.0;
+    for (auto &g : gs) {
+        const int64_t q = g.Mg / g.c, r = g.Mg % g.c;
+        const double hi = (double)(q + 1) * g.tau - mean, lo = (double)q * g.tau - mean;
+        obj += (double)r * hi * hi + (double)(g.c - r) * lo * lo;
+    }
+    return obj;
+}
+
+inline double marginal(const Group &g, int64_t M) {   // phi(M+1) - phi(M), without tau^2
+    return (double)(2 * (M / g.c) + 1);
+}
+
+void distribute_exact(const double *T, int x, int64_t K, int64_t *nb, double *obj_out) {
+    std::vector<Group> gs;
+    {
+        std::vector<int> idx(x);
+        for (int i = 0; i < x; ++i) idx[i] = i;
+        std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return T[a] < T[b]; });
+        for (int i : idx) {
+            if (gs.empty() || gs.back().tau != T[i]) gs.push_back({T[i], 0, 0, {}});
+            gs.back().c++;
+            gs.back().members.push_back(i);
+        }
+    }
+    for (auto &g : gs) std::sort(g.members.begin(), g.members.end());
+    for (auto &g : gs) g.Mg = g.c;
+    gs[0].Mg += K - x;
+    std::vector<int64_t> best_M(gs.size());
+    double best = group_objective(gs, x);
+    for (size_t i = 0; i < gs.size(); ++i) best_M[i] = gs[i].Mg;
+    double mu_cur = -std::numeric_limits<double>::infinity();
+    for (;;) {
+        double best_mu = std::numeric_limits<double>::infinity();
+        int bs = -1, bt = -1;
+        for (size_t s = 0; s < gs.size(); ++s) {
+            if (gs[s].Mg <= gs[s].c) continue;
+            const double ds = gs[s].tau * gs[s].tau * marginal(gs[s], gs[s].Mg - 1);
+            for (size_t t = s + 1; t < gs.size(); ++t) {
+                const double dt = gs[t].tau * gs[t].tau * marginal(gs[t], gs[t].Mg);
+                double mu = (dt - ds) / (2.0 * (gs[t].tau - gs[s].tau));
+                if (mu < mu_cur) mu = mu_cur;     // rounding guard: never move backwards
+                if (mu < best_mu) { best_mu = mu; bs = (int)s; bt = (int)t; }
+            }
+        }
+        if (bs < 0) break;
+        mu_cur = best_mu;
+        gs[bs].Mg--;
+        gs[bt].Mg++;
+        const double o = group_objective(gs, x);
+        if (o < best) {
+            best = o;
+            for (size_t i = 0; i < gs.size(); ++i) best_M[i] = gs[i].Mg;
+        }
+    }
+    for (size_t gi = 0; gi < gs.size(); ++gi) {
+        const Group &g = gs[gi];
+        const int64_t q = best_M[gi] / g.c, r = best_M[gi] % g.c;
+        for (size_t k = 0; k < g.members.size(); ++k) nb[g.members[k]] = q + ((int64_t)k < r ? 1 : 0);
+    }
+    if (obj_out) {
+        // objective of the final assignment, per pipeline (Eq.6 as written)
+        double sum = 0.0;
+        for (int i = 0; i < x; ++i) sum += (double)nb[i] * T[i];
+        const double mean = sum / x;
+        double o = 0.0;
+        for (int i = 0; i < x; ++i) {
+            const double d = (double)nb[i] * T[i] - mean;
+            o += d * d;
+        }
+        *obj_out = o;
+    }
+}
+
+}  // namespace
+
+extern "C" int64_t oob_recommend_batch(int32_t x, int32_t b, int64_t B) {
+    if (x < 1) x = 1;
+    if (b < 1) b = 1;
+    int64_t Bp = std::max<int64_t>(B, (int64_t)x * b);
+    if (Bp % b) Bp += b - Bp % b;
+    return Bp;
+}
+
+extern "C" oob_status oob_distribute_batch(const double *T, int32_t x, int64_t B, int32_t b,
+                                           int64_t *nb_out, double *objective_out,
+                                           int64_t *recommended_out) {
+    if (!T || !nb_out) return fail(OOB_E_INVALID, "oob_distribute_batch: NULL argument");
+    if (x < 1 || b < 1 || B < 1) return fail(OOB_E_INVALID, "need x >= 1, microbatch >= 1, B >= 1");
+    for (int i = 0; i < x; ++i)
+        if (!(std::isfinite(T[i]) && T[i] > 0.0)) return fail(OOB_E_INVALID, "per-microbatch time must be positive");
+    if (B % b != 0 || B / b < x) {
+        if (recommended_out) *recommended_out = oob_recommend_batch(x, b, B);
+        return fail(OOB_E_BATCH, "global batch cannot be distributed: B % b != 0 or B/b < pipelines");
+    }
+    distribute_exact(T, x, B / b, nb_out, objective_out);
+    if (recommended_out) *recommended_out = B;
+    return OOB_OK;
+}
+
+// ---------------------------------------------------------------- Eq.5
+namespace {
+
+// Count of X (sizes n_lo..n_hi, sum x_i n_i = N, sum x_i >= f+1), saturating at INT64_MAX.
+int64_t count_sets(int n_lo, int n_hi, int N, int f) {
+    const int C = f + 2;   // pipeline count buckets 0..f+1 (f+1 = "at least f+1")
+    std::vector<double> cnt((size_t)(N + 1) * C, 0.0);   // double: counts can exceed 2^64
+    cnt[0] = 1.0;
+    for (int n = n_lo; n <= n_hi; ++n)
+        for (int t = n; t <= N; ++t)
+            for (int c = 0; c < C; ++c) {
+                const double v = cnt[(size_t)(t - n) * C + c];
+                if (v == 0.0) continue;
+                cnt[(size_t)t * C + std::min(c + 1, C - 1)] += v;
+            }
+    const double r = cnt[(size_t)N * C + (C - 1)];
+    return r >= 9.2e18 ? INT64_MAX : (int64_t)r;
+}
+
+struct InstCtx {
+    const oob_template *tpl;   // [p]
+    int p, n_lo, N, f;
+    int64_t B;
+    int b;
+    int64_t max_enum, evaluated = 0, distributable = 0;
+    int min_pipes_fail = INT32_MAX;
+    bool capped = false;
+    std::vector<int32_t> x, best_x;
+    std::vector<int64_t> best_nb, nb;
+    std::vector<double> T;
+    double best_thr = -1.0, best_iter = 0.0;
+    int64_t best_pipes = 0;
+};
+
+void evaluate(InstCtx &c) {
+    int64_t pipes = 0;
+    for (int i = 0; i < c.p; ++i) pipes += c.x[i];
+    if (pipes < c.f + 1) return;
+    c.evaluated++;
+    const int64_t K = c.B / c.b;
+    if (c.B % c.b != 0 || K < pipes) {
+        c.min_pipes_fail = std::min<int64_t>(c.min_pipes_fail, pipes);
+        return;
+    }
+    c.T.clear();
+    for (int i = 0; i < c.p; ++i)
+        for (int k = 0; k < c.x[i]; ++k) c.T.push_back(c.tpl[i].tstar_ms);
+    c.nb.assign(pipes, 0);
+    distribute_exact(c.T.data(), (int)pipes, K, c.nb.data(), nullptr);
+    c.distributable++;
+    double iter = 0.0;
+    int64_t pi = 0;
+    for (int i = 0; i < c.p; ++i)
+        for (int k = 0; k < c.x[i]; ++k, ++pi) {
+            const oob_template &t = c.tpl[i];
+            // iteration_ms(N_b) = T1 + (N_b - S + k* - 1) t* + T3 (Eq.2 with the real N_b)
+            const double it = (t.t1_ms + (double)(c.nb[pi] - t.num_stages + t.kstar - 1) * t.tstar_ms) + t.t3_ms;
+            iter = std::max(iter, it);
+        }
+    const double thr = (double)c.B / iter;
+    bool better = false;
+    if (thr > c.best_thr) better = true;
+    else if (thr == c.best_thr) {
+        if (pipes < c.best_pipes) better = true;
+        else if (pipes == c.best_pipes && c.x < c.best_x) better = true;
+    }
+    if (better) {
+        c.best_thr = thr; c.best_iter = iter; c.best_pipes = pipes;
+        c.best_x = c.x; c.best_nb = c.nb;
+    }
+}
+
+// DFS over x_{p-1} .. x_0 (the recursion of Eq.5: either no more of template p', or one
+// more of it), stopping after max_enum feasible sets.
+void dfs(InstCtx &c, int i, int rem) {
+    if (c.capped) return;
+    if (i < 0) {
+        if (rem == 0) {
+            if (c.evaluated >= c.max_enum) { c.capped = true; return; }
+            evaluate(c);
+        }
+        return;
+    }
+    const int n = c.n_lo + i;
+    for (int k = 0; k * n <= rem; ++k) {
+        c.x[i] = k;
+        dfs(c, i - 1, rem - k * n);
+        if (c.capped) break;
+    }
+    c.x[i] = 0;
+}
+
+}  // namespace
+
+extern "C" oob_status oob_count_sets(int32_t n_lo, int32_t n_hi, int32_t N, int32_t f, int64_t *out) {
+    if (!out || n_lo < 1 || n_hi < n_lo || N < 0 || f < 0) return fail(OOB_E_INVALID, "oob_count_sets: bad argument");
+    *out = count_sets(n_lo, n_hi, N, f);
+    return OOB_OK;
+}
+
+extern "C" oob_status oob_instantiate(const oob_template_set *set, int32_t profile, int32_t N, int32_t f,
+                                      int64_t B, int32_t b, int64_t max_enum, int32_t *counts_out,
+                                      int64_t *nb_out, int32_t max_pipelines, int32_t *num_pipelines_out,
+                                      double *thr_out, double *iter_out, int64_t *num_feasible_out,
+                                      int64_t *rec_out) {
+    if (!set || !counts_out || !nb_out || !num_pipelines_out)
+        return fail(OOB_E_INVALID, "oob_instantiate: NULL argument");
+    if (profile < 0 || profile >= set->num_profiles) return fail(OOB_E_INVALID, "oob_instantiate: bad profile");
+    if (f < 0 || b < 1 || B < 1) return fail(OOB_E_INVALID, "oob_instantiate: need f >= 0, b >= 1, B >= 1");
+    const int p = set->n_hi - set->n_lo + 1;
+    if ((int64_t)N < (int64_t)(f + 1) * set->n_lo) return fail(OOB_E_INFEASIBLE, "insufficient nodes for f+1 replicas");
+    InstCtx c;
+    c.tpl = &set->templates[(size_t)profile * p];
+    c.p = p; c.n_lo = set->n_lo; c.N = N; c.f = f; c.B = B; c.b = b;
+    c.max_enum = max_enum > 0 ? max_enum : 1000000;
+    c.x.assign(p, 0);
+    const int64_t total = count_sets(set->n_lo, set->n_hi, N, f);
+    if (num_feasible_out) *num_feasible_out = total;
+    if (total == 0) return fail(OOB_E_INFEASIBLE, "no feasible pipeline set for this node count");
+    dfs(c, p - 1, N);
+    if (c.best_thr < 0) {
+        if (rec_out) *rec_out = oob_recommend_batch(c.min_pipes_fail == INT32_MAX ? f + 1 : c.min_pipes_fail, b, B);
+        return fail(OOB_E_BATCH, "no feasible set can distribute the global batch");
+    }
+    if (c.best_pipes > max_pipelines) return fail(OOB_E_NOMEM, "max_pipelines too small for the chosen plan");
+    for (int i = 0; i < p; ++i) counts_out[i] = c.best_x[i];
+    for (int64_t i = 0; i < c.best_pipes; ++i) nb_out[i] = c.best_nb[i];
+    *num_pipelines_out = (int32_t)c.best_pipes;
+    if (thr_out) *thr_out = c.best_thr;
+    if (iter_out) *iter_out = c.best_iter;
+    if (rec_out) *rec_out = B;
+    if (c.capped) return fail(OOB_E_TOO_MANY, "more than max_enumerated feasible sets; plan is the best of the first max_enumerated");
+    return OOB_OK;
+}

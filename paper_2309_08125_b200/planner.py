@@ -1,0 +1,207 @@
+"""Python API over the C ABI (same names as include/oobleck_plan.h, marshalling only).
+
+    from paper_2309_08125_b200 import planner
+    prof = planner.Profile.from_arrays(fwd_ms, bwd_ms)          # host arrays [L][M]
+    sets = planner.generate_templates([prof], nodes=N, gpus_per_node=M, f=f, n0=n0)
+    plan = planner.instantiate(sets, 0, nodes=N', f=f, global_batch=B, microbatch=b)
+    nb, obj = planner.distribute_batch(T, B, b)
+
+The device-resident path used by bench.py is `DPPlan` (inputs already in HBM).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import (OOB_E_BATCH, OOB_E_TOO_MANY, OOB_OK, OobDpInfo, OobError, OobPlanOpts,
+                   OobTemplate, check, lib)
+
+
+class Profile:
+    """Owning wrapper of an oob_profile handle."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @classmethod
+    def from_arrays(cls, fwd_ms, bwd_ms, state_bytes=None) -> "Profile":
+        fwd = np.ascontiguousarray(fwd_ms, dtype=np.float64)
+        bwd = np.ascontiguousarray(bwd_ms, dtype=np.float64)
+        if fwd.ndim != 2 or fwd.shape != bwd.shape:
+            raise ValueError("fwd_ms/bwd_ms must be [L][M] arrays of the same shape")
+        L, M = fwd.shape
+        st = None
+        if state_bytes is not None:
+            st = np.ascontiguousarray(state_bytes, dtype=np.int64)
+        h = ctypes.c_void_p()
+        check(lib.oob_profile_from_arrays(L, M, fwd.ctypes.data, bwd.ctypes.data,
+                                          None if st is None else st.ctypes.data, ctypes.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def load(cls, path: str) -> "Profile":
+        h = ctypes.c_void_p()
+        check(lib.oob_load_profile(path.encode(), ctypes.byref(h)))
+        return cls(h)
+
+    @property
+    def L(self) -> int:
+        return lib.oob_profile_layers(self._h)
+
+    @property
+    def M(self) -> int:
+        return lib.oob_profile_gpus_per_node(self._h)
+
+    def min_nodes(self, nodes: int, gpu_mem_bytes: int, util: float = 0.8, samples_per_gpu: int = 1) -> int:
+        out = ctypes.c_int32()
+        check(lib.oob_min_nodes(self._h, nodes, gpu_mem_bytes, util, samples_per_gpu, ctypes.byref(out)))
+        return out.value
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.oob_profile_free(self._h)
+            self._h = None
+
+
+def load_profile(path: str) -> Profile:
+    return Profile.load(path)
+
+
+def node_sizes(nodes: int, f: int, n0: int, layers: int) -> list[int]:
+    lo, hi = ctypes.c_int32(), ctypes.c_int32()
+    check(lib.oob_node_sizes(nodes, f, n0, layers, ctypes.byref(lo), ctypes.byref(hi)))
+    return list(range(lo.value, hi.value + 1))
+
+
+def _template_dict(t: OobTemplate) -> dict:
+    st = [(t.stages[j].layer_begin, t.stages[j].layer_end, t.stages[j].gpus, t.stages[j].node,
+           t.stages[j].gpu_offset) for j in range(t.num_stages)]
+    return {"nodes": t.nodes, "S": t.num_stages, "stages": st, "T1": t.t1_ms, "T2": t.t2_ms,
+            "T3": t.t3_ms, "kstar": t.kstar, "tstar": t.tstar_ms, "total": t.iter_ms}
+
+
+class TemplateSet:
+    """Owning wrapper of an oob_template_set handle."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @property
+    def num_profiles(self) -> int:
+        return lib.oob_template_set_profiles(self._h)
+
+    def count(self, profile: int = 0) -> int:
+        return lib.oob_template_count(self._h, profile)
+
+    def get(self, profile: int, i: int) -> dict:
+        t = OobTemplate()
+        check(lib.oob_template_get(self._h, profile, i, ctypes.byref(t)))
+        return _template_dict(t)
+
+    def templates(self, profile: int = 0) -> list[dict]:
+        return [self.get(profile, i) for i in range(self.count(profile))]
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.oob_template_set_free(self._h)
+            self._h = None
+
+
+def generate_templates(profiles, nodes: int, gpus_per_node: int, f: int, n0: int = 0,
+                       gpu_mem_bytes: int = 0, util: float = 0.8, samples_per_gpu: int = 1,
+                       device: int = -1, stream: int = 0, workspace: int = 0,
+                       workspace_bytes: int = 0) -> TemplateSet:
+    """oob_generate_templates: host profiles in, template set out (H2D + GPU DP + D2H)."""
+    profs = [p if isinstance(p, Profile) else Profile.from_arrays(*p) for p in profiles]
+    arr = (ctypes.c_void_p * len(profs))(*[p._h for p in profs])
+    opts = OobPlanOpts(nodes=nodes, gpus_per_node=gpus_per_node, f=f, n0=n0,
+                       gpu_mem_bytes=gpu_mem_bytes, util=util, samples_per_gpu=samples_per_gpu,
+                       device=device, stream=stream or None, workspace=workspace or None,
+                       workspace_bytes=workspace_bytes)
+    h = ctypes.c_void_p()
+    check(lib.oob_generate_templates(arr, len(profs), ctypes.byref(opts), ctypes.byref(h)))
+    ts = TemplateSet(h)
+    ts._keep = profs
+    return ts
+
+
+class DPPlan:
+    """oob_dp_plan: the device-resident DP (inputs already in HBM)."""
+
+    def __init__(self, L: int, M: int, n_lo: int, n_hi: int, num_profiles: int = 1):
+        h = ctypes.c_void_p()
+        check(lib.oob_dp_plan_create(L, M, n_lo, n_hi, num_profiles, ctypes.byref(h)))
+        self._h = h
+        self.info = OobDpInfo()
+        check(lib.oob_dp_plan_info(self._h, ctypes.byref(self.info)))
+
+    def run(self, d_fwd: int, d_bwd: int, d_workspace: int, workspace_bytes: int, d_packed: int,
+            stream: int = 0) -> None:
+        check(lib.oob_dp_run(self._h, d_fwd, d_bwd, d_workspace, workspace_bytes, d_packed, stream or None))
+
+    def set_timing(self, enable: bool) -> None:
+        check(lib.oob_dp_set_timing(self._h, 1 if enable else 0))
+
+    def kernel_time(self, reset: bool = True):
+        ms, n = ctypes.c_double(), ctypes.c_int64()
+        check(lib.oob_dp_kernel_time(self._h, ctypes.byref(ms), ctypes.byref(n), 1 if reset else 0))
+        return ms.value, n.value
+
+    def template_set(self, host_packed: np.ndarray) -> TemplateSet:
+        buf = np.ascontiguousarray(host_packed)
+        if buf.nbytes < self.info.packed_bytes:
+            raise ValueError("packed buffer too small")
+        h = ctypes.c_void_p()
+        check(lib.oob_template_set_from_packed(buf.ctypes.data, ctypes.byref(self.info), ctypes.byref(h)))
+        return TemplateSet(h)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.oob_dp_plan_free(self._h)
+            self._h = None
+
+
+def dp_info(L: int, M: int, n_lo: int, n_hi: int, num_profiles: int = 1) -> OobDpInfo:
+    return DPPlan(L, M, n_lo, n_hi, num_profiles).info
+
+
+def count_sets(n_lo: int, n_hi: int, nodes: int, f: int) -> int:
+    out = ctypes.c_int64()
+    check(lib.oob_count_sets(n_lo, n_hi, nodes, f, ctypes.byref(out)))
+    return out.value
+
+
+def instantiate(tset: TemplateSet, profile: int, nodes: int, f: int, global_batch: int,
+                microbatch: int, max_enumerated: int = 0) -> dict:
+    """oob_instantiate: best plan for `nodes` nodes (Eq.5 + Eq.6 + throughput)."""
+    p = tset.count(profile)
+    counts = np.zeros(p, np.int32)
+    maxp = max(1, nodes)
+    nb = np.zeros(maxp, np.int64)
+    npipes, thr, it = ctypes.c_int32(), ctypes.c_double(), ctypes.c_double()
+    nfeas, rec = ctypes.c_int64(), ctypes.c_int64()
+    st = lib.oob_instantiate(tset._h, profile, nodes, f, global_batch, microbatch, max_enumerated,
+                             counts.ctypes.data, nb.ctypes.data, maxp, ctypes.byref(npipes),
+                             ctypes.byref(thr), ctypes.byref(it), ctypes.byref(nfeas), ctypes.byref(rec))
+    if st not in (OOB_OK, OOB_E_TOO_MANY):
+        check(st, {"recommended_global_batch": rec.value})
+    return {"counts": tuple(int(c) for c in counts), "nb": tuple(int(x) for x in nb[:npipes.value]),
+            "throughput": thr.value, "iteration_ms": it.value, "num_feasible": nfeas.value,
+            "capped": st == OOB_E_TOO_MANY}
+
+
+def distribute_batch(per_microbatch_ms, global_batch: int, microbatch: int):
+    """oob_distribute_batch: exact Eq.6; returns (nb tuple, objective)."""
+    T = np.ascontiguousarray(per_microbatch_ms, dtype=np.float64)
+    nb = np.zeros(T.shape[0], np.int64)
+    obj, rec = ctypes.c_double(), ctypes.c_int64()
+    st = lib.oob_distribute_batch(T.ctypes.data, T.shape[0], global_batch, microbatch, nb.ctypes.data,
+                                  ctypes.byref(obj), ctypes.byref(rec))
+    check(st, {"recommended_global_batch": rec.value})
+    return tuple(int(x) for x in nb), obj.value
+
+
+def recommend_batch(x: int, microbatch: int, global_batch: int) -> int:
+    return int(lib.oob_recommend_batch(x, microbatch, global_batch))

@@ -1,0 +1,145 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, element by element.
+
+Bar (north star): stage boundaries, GPU counts, nodes, S and k* bit-exact; costs equal
+under the shared operation order — asserted bit-exact here (stricter than the north
+star's rel 1e-12, which `_close` would allow), on seeded synthetic inputs.
+"""
+import random
+
+import numpy as np
+import pytest
+
+from oracle import coracle
+from tests.helpers import load_golden
+from workloads import CONFIGS, config_profiles, random_profile
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def planner():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2309_08125_b200 import planner as p
+    return p
+
+
+def _gpu_set(planner, profs, cfg_like):
+    L, M, N, f, n0 = cfg_like
+    return planner.generate_templates([(p.fwd_ms, p.bwd_ms) for p in profs], nodes=N,
+                                      gpus_per_node=M, f=f, n0=n0, device=0)
+
+
+def _assert_same(got, want, ctx=""):
+    assert len(got) == len(want), ctx
+    for g, w in zip(got, want):
+        assert g["nodes"] == w["nodes"], ctx
+        assert (g["S"], g["kstar"], g["stages"]) == (w["S"], w["kstar"], w["stages"]), (ctx, g["nodes"])
+        for k in ("T1", "T2", "T3", "tstar", "total"):
+            assert g[k] == w[k], (ctx, g["nodes"], k, g[k], w[k])
+
+
+@pytest.mark.parametrize("key", ["cfg1", "cfg2", "cfg3"])
+@pytest.mark.parametrize("mode", ["real", "dyadic"])
+def test_configs_vs_oracle(planner, key, mode):
+    cfg = CONFIGS[key]
+    prof = config_profiles(cfg, mode)[0]
+    ts = _gpu_set(planner, [prof], (cfg.L, cfg.M, cfg.N, cfg.f, cfg.n0))
+    want, _ = coracle.template_set(prof.fwd_ms, prof.bwd_ms, cfg.M, cfg.n0, cfg.n_max)
+    _assert_same(ts.templates(0), want, key)
+
+
+def test_random_small_vs_oracle(planner):
+    """Many shapes (several tiles, ragged tails, ties): L 1..40, M 1..8, every kind."""
+    rng = random.Random(2024)
+    for i in range(150):
+        L = rng.choice([1, 2, 3, 5, 7, 9, 12, 16, 20, 24, 31, 40])
+        M = rng.choice([1, 2, 3, 4, 5, 8])
+        kind = rng.choice(["integer", "uniform", "lognormal", "spiky", "constant"])
+        mode = rng.choice(["real", "dyadic"])
+        prof = random_profile(7000 + i, L, M, kind, mode)
+        n0 = rng.randint(1, max(1, min(L, 3)))
+        f = rng.randint(0, 3)
+        N = (f + 1) * n0 + rng.randint(0, 2 * L)
+        n_hi = min(N - f * n0, L)
+        ts = _gpu_set(planner, [prof], (L, M, N, f, n0))
+        want, _ = coracle.template_set(prof.fwd_ms, prof.bwd_ms, M, n0, n_hi)
+        _assert_same(ts.templates(0), want, f"case {i} L={L} M={M} {kind}")
+
+
+def test_batched_profiles_vs_oracle(planner):
+    """Batched sweep (cfg5 shape): several profiles in one call, each vs the oracle."""
+    cfg = CONFIGS["cfg5"]
+    rec = load_golden("cfg5", "real")
+    profs = config_profiles(cfg, "real", count=4 if rec else 2)
+    ts = _gpu_set(planner, profs, (cfg.L, cfg.M, cfg.N, cfg.f, cfg.n0))
+    for i, p in enumerate(profs):
+        want = rec["profiles"][i]["templates"] if rec else \
+            coracle.template_set(p.fwd_ms, p.bwd_ms, cfg.M, cfg.n0, cfg.n_max)[0]
+        _assert_same(ts.templates(i), want, f"cfg5 profile {i}")
+
+
+@pytest.mark.parametrize("mode", ["real", "dyadic"])
+def test_cfg4_full_vs_golden(planner, mode):
+    """Full template set of the north-star config (96 layers, 512 x 8 GPUs, f=4, n0=3)
+    vs the C oracle's output stored by scripts/make_golden.py."""
+    rec = load_golden("cfg4", mode)
+    if rec is None:
+        pytest.skip(f"tests/golden/cfg4_{mode}.json not generated")
+    cfg = CONFIGS["cfg4"]
+    prof = config_profiles(cfg, mode)[0]
+    ts = _gpu_set(planner, [prof], (cfg.L, cfg.M, cfg.N, cfg.f, cfg.n0))
+    _assert_same(ts.templates(0), rec["profiles"][0]["templates"], "cfg4")
+
+
+def test_cfg4_sampled_templates_vs_oracle(planner):
+    """Full-size config, fresh seed: the oracle recomputes the smallest templates one by one
+    (cheap: they touch few cells) and they must match the GPU's full-set run."""
+    cfg = CONFIGS["cfg4"]
+    prof = config_profiles(cfg, "real", count=2)[1]
+    ts = _gpu_set(planner, [prof], (cfg.L, cfg.M, cfg.N, cfg.f, cfg.n0))
+    got = ts.templates(0)
+    want, _ = coracle.template_set(prof.fwd_ms, prof.bwd_ms, cfg.M, cfg.n0, cfg.n0 + 5)
+    _assert_same(got[:6], want, "cfg4 seed 2 small templates")
+
+
+def test_device_resident_path_matches(planner):
+    """oob_dp_run on device-resident inputs == oob_generate_templates; deterministic."""
+    import torch
+    cfg = CONFIGS["cfg3"]
+    profs = config_profiles(cfg, "real", count=3)
+    plan = planner.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, len(profs))
+    info = plan.info
+    fwd = torch.tensor(np.stack([p.fwd_ms for p in profs]), dtype=torch.float64, device="cuda")
+    bwd = torch.tensor(np.stack([p.bwd_ms for p in profs]), dtype=torch.float64, device="cuda")
+    ws = torch.empty(info.workspace_bytes, dtype=torch.uint8, device="cuda")
+    outs = []
+    for _ in range(2):
+        packed = torch.zeros(info.packed_bytes, dtype=torch.uint8, device="cuda")
+        plan.run(fwd.data_ptr(), bwd.data_ptr(), ws.data_ptr(), ws.numel(), packed.data_ptr(),
+                 torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        outs.append(packed.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+    ts = plan.template_set(outs[0])
+    ref = _gpu_set(planner, profs, (cfg.L, cfg.M, cfg.N, cfg.f, cfg.n0))
+    for i in range(len(profs)):
+        assert ts.templates(i) == ref.templates(i)
+
+
+def test_edge_cases(planner):
+    # single layer, single template; N exactly (f+1) n0; M = 1 with many nodes
+    for (L, M, N, f, n0) in [(1, 1, 1, 0, 1), (1, 8, 2, 1, 1), (6, 1, 6, 1, 3), (10, 1, 30, 0, 1),
+                             (4, 8, 5, 0, 1)]:
+        prof = random_profile(31 + L + M, L, M, "uniform")
+        ts = _gpu_set(planner, [prof], (L, M, N, f, n0))
+        want, _ = coracle.template_set(prof.fwd_ms, prof.bwd_ms, M, n0, min(N - f * n0, L))
+        _assert_same(ts.templates(0), want, f"edge L={L} M={M} N={N}")
+    from paper_2309_08125_b200._lib import OOB_E_INFEASIBLE, OobError
+    prof = random_profile(3, 4, 2, "uniform")
+    with pytest.raises(OobError) as e:
+        _gpu_set(planner, [prof], (4, 2, 3, 1, 2))
+    assert e.value.status == OOB_E_INFEASIBLE
