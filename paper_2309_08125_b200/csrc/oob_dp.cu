@@ -15,6 +15,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -62,6 +65,10 @@ __device__ __forceinline__ void d_dsplit(const DevGeom &g, int a, int j, int &a1
 __device__ __forceinline__ int64_t d_cell(const DevGeom &g, int Sp, int u, int l, int a) {
     return g.base[l] + (int64_t)u * g.cells[l] + g.off[l * g.A + a] + (Sp - d_lo(g, a));
 }
+
+}  // namespace oob
+#include "oob_wave_w.cuh"
+namespace oob {
 
 // ------------------------------------------------------------------ K_base: Eq.4
 // One thread per (profile, u, base alloc) of wavefront l = blockIdx.y + 1.  Base allocs:
@@ -214,18 +221,59 @@ __global__ void k_extract(DevGeom g, unsigned char *packed, size_t tpl_bytes) {
 
 }  // namespace oob
 
+
 // ==================================================================== plan + C ABI
 using namespace oob;
+
+namespace {
+
+// k_wave_w launch configurations: (TE cells per lane tile, threads per CTA)
+struct WCfg { int te, nt; };
+constexpr WCfg WCFGS[] = {{4, 128}, {4, 256}, {8, 128}, {8, 256}};
+constexpr int NWCFG = 4;
+
+struct WaveHost {
+    int cfg = 0;                   // index into WCFGS
+    int nitems = 0, ns_max = 0, nout = 0;
+    size_t items_off = 0;          // byte offset of this wavefront's int4 items in the blob
+    std::vector<int32_t> items;    // 4 ints per item
+    size_t smem = 0;
+    int64_t small_warps = 0;
+    double cost = 0.0;
+};
+
+int Q_of(const Geometry &g, int l) { return (l == g.L) ? g.n_hi : std::max(1, g.n_hi - 1); }
+int wlen_h(const Geometry &g, int l, int q) {
+    int hi = std::min(l, q * g.M);
+    return hi >= q ? hi - q + 1 : 0;
+}
+int wcells_h(const Geometry &g, int l) { return g.cells[l] - g.off[(size_t)l * g.A + (g.M - 1)]; }
+
+struct TileTab {
+    std::vector<int32_t> off, np;            // [L+1]
+    std::vector<std::vector<int>> active;    // [L+1][pass] active warps
+};
+
+}  // namespace
 
 struct oob_dp_plan {
     Geometry g;
     int32_t P = 1;
+    int kernel = 2;                      // 1 = v1 (thread per cell), 2 = tiled W kernel
+    int force_cfg = -1;
     size_t geom_bytes = 0, ws_bytes = 0, tpl_bytes = 0;
     std::vector<unsigned char> geom_blob;   // host image of the geometry region
-    size_t off_cells = 0, off_base = 0, off_off = 0, off_T1 = 0, off_T3 = 0, off_TS = 0, off_KD = 0, off_ARG = 0, off_STK = 0;
+    size_t off_cells = 0, off_base = 0, off_off = 0, off_tiles = 0, off_tile_off = 0, off_tile_np = 0,
+           off_items = 0;
+    size_t off_T1 = 0, off_T3 = 0, off_TS = 0, off_KD = 0, off_ARG = 0, off_STK = 0, off_PB = 0, off_PK = 0;
+    std::vector<int32_t> tiles;          // all configs' tables concatenated
+    TileTab tab[NWCFG];
+    std::vector<WaveHost> waves;         // [L+1]
+    size_t max_smem = 0;
+    int64_t launches = 0;
     void *uploaded_to = nullptr;
     int timing = 0;
-    std::vector<cudaEvent_t> ev;            // pairs per wavefront launch
+    std::vector<cudaEvent_t> ev;
     int ev_used = 0;
     double acc_ms = 0.0;
     int64_t acc_launches = 0;
@@ -237,6 +285,122 @@ static oob_status cuda_fail(cudaError_t e, const char *what) {
     return fail(OOB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Tile tables for one (TE, NT): for a big side of length lb, its W rows j = 1..min(Q, lb)
+// are cut into ceil(len/TE) lane tiles; rows are assigned IN ORDER to consecutive warps
+// (a row never straddles warps; warp w's rows all precede warp w+1's — the neighbour
+// chain of k_wave_w relies on it), NT/32 warps per pass.
+static void build_tiles(oob_dp_plan *pl, int ci) {
+    const Geometry &g = pl->g;
+    const int TE = WCFGS[ci].te, NT = WCFGS[ci].nt, WARPS = NT / 32;
+    TileTab &T = pl->tab[ci];
+    T.off.assign(g.L + 1, 0);
+    T.np.assign(g.L + 1, 0);
+    T.active.assign(g.L + 1, {});
+    for (int lb = 1; lb <= g.L; ++lb) {
+        const int J = std::min(Q_of(g, lb), lb);
+        std::vector<std::vector<std::pair<int, int>>> wrows;   // per warp: (row, lanes)
+        int used = 32;
+        for (int j = 1; j <= J; ++j) {
+            const int len = wlen_h(g, lb, j);
+            if (len <= 0) continue;
+            const int need = (len + TE - 1) / TE;
+            if (used + need > 32) { wrows.push_back({}); used = 0; }
+            wrows.back().push_back({j, need});
+            used += need;
+        }
+        const int nw = (int)wrows.size();
+        const int np = (nw + WARPS - 1) / WARPS;
+        T.off[lb] = (int32_t)pl->tiles.size();
+        T.np[lb] = np;
+        std::vector<int32_t> tab((size_t)np * NT, -1);
+        for (int w = 0; w < nw; ++w) {
+            int lane = 0;
+            for (auto &rr : wrows[w])
+                for (int t = 0; t < rr.second; ++t, ++lane)
+                    tab[(size_t)(w / WARPS) * NT + (w % WARPS) * 32 + lane] = (rr.first << 16) | (t * TE);
+        }
+        for (int p = 0; p < np; ++p) T.active[lb].push_back(std::min(WARPS, nw - p * WARPS));
+        pl->tiles.insert(pl->tiles.end(), tab.begin(), tab.end());
+    }
+}
+
+// Issue-cycle model of one k (SMSP issue slots): every active warp of every pass walks all
+// staged rows; a step costs TE splits (~22 instructions each) plus the flush (~14).
+static double k_cost(const oob_dp_plan *pl, int ci, int l, int l1, int it_lo, int it_hi) {
+    const Geometry &g = pl->g;
+    const int TE = WCFGS[ci].te;
+    const int l2 = l - l1;
+    const bool lt = wcells_h(g, l1) >= wcells_h(g, l2);
+    const int ls = lt ? l2 : l1, lb = lt ? l1 : l2;
+    const int JS = std::min(Q_of(g, ls), ls);
+    double steps = 0.0;
+    for (int r = std::max(1, it_lo); r <= std::min(JS, it_hi - 1); ++r) steps += wlen_h(g, ls, r) + 3;
+    double aw = 0.0;
+    for (int a : pl->tab[ci].active[lb]) aw += a;
+    return aw * steps * (TE * 22.0 + 14.0) + 2000.0;
+}
+
+// Work items of wavefront l, balanced by the cost model: items are (l1 range, staged-row
+// range); a k heavier than 1.5x the per-item target is split by staged rows.
+static void build_items(oob_dp_plan *pl, int l, int ci, int target_ctas, WaveHost &wh) {
+    const Geometry &g = pl->g;
+    const int nr = g.L - l + 1;
+    std::vector<double> cost(l, 0.0);
+    double total = 0.0;
+    int ns_max = 0;
+    for (int l1 = 1; l1 < l; ++l1) {
+        cost[l1] = k_cost(pl, ci, l, l1, 1, 1 << 20);
+        total += cost[l1];
+        const int l2 = l - l1;
+        ns_max = std::max(ns_max, std::min(wcells_h(g, l1), wcells_h(g, l2)));
+    }
+    const int per_range = std::max(1, (target_ctas + pl->P * nr - 1) / (pl->P * nr));
+    const double target = total / per_range;
+    std::vector<int32_t> items;
+    int cur_lo = 1;
+    double cur = 0.0;
+    for (int l1 = 1; l1 < l; ++l1) {
+        if (cost[l1] > 1.5 * target && per_range > 1) {
+            if (cur_lo < l1) items.insert(items.end(), {cur_lo, l1, 1, 1 << 20});
+            const int pieces = std::max(1, (int)std::lround(cost[l1] / target));
+            const int l2 = l - l1;
+            const bool lt = wcells_h(g, l1) >= wcells_h(g, l2);
+            const int ls = lt ? l2 : l1;
+            const int JS = std::min(Q_of(g, ls), ls);
+            const double piece = cost[l1] / pieces;
+            int r0 = 1;
+            for (int r = 1; r <= JS; ++r) {
+                if (k_cost(pl, ci, l, l1, r0, r + 1) >= piece && r < JS) {
+                    items.insert(items.end(), {l1, l1 + 1, r0, r + 1});
+                    r0 = r + 1;
+                }
+            }
+            items.insert(items.end(), {l1, l1 + 1, r0, 1 << 20});
+            cur_lo = l1 + 1;
+            cur = 0.0;
+            continue;
+        }
+        cur += cost[l1];
+        if (cur >= target && per_range > 1) {
+            items.insert(items.end(), {cur_lo, l1 + 1, 1, 1 << 20});
+            cur_lo = l1 + 1;
+            cur = 0.0;
+        }
+    }
+    if (cur_lo < l) items.insert(items.end(), {cur_lo, l, 1, 1 << 20});
+    wh.cfg = ci;
+    wh.items = items;
+    wh.nitems = (int)items.size() / 4;
+    wh.ns_max = ns_max;
+    wh.nout = wcells_h(g, l);
+    wh.smem = align_up((size_t)wh.nout * 12, 16) + (size_t)ns_max * 40 + 3 * (size_t)(g.L + 2) * 4 +
+              (size_t)(WCFGS[ci].nt / 32) * 4;
+    wh.cost = total * pl->P * nr;
+    int per = 0;
+    for (int a = 0; a < std::min(g.A, g.M); ++a) per += std::max(0, std::min(l, g.gpus(a)) - 1);
+    wh.small_warps = (int64_t)pl->P * nr * per;
+}
+
 extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int32_t n_hi,
                                          int32_t num_profiles, oob_dp_plan **out) {
     if (!out) return fail(OOB_E_INVALID, "oob_dp_plan_create: out is NULL");
@@ -246,10 +410,59 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     if (!build_geometry(L, M, n_lo, n_hi, pl->g)) { delete pl; return OOB_E_INVALID; }
     pl->P = num_profiles;
     const Geometry &g = pl->g;
+    const char *kv = std::getenv("OOB_DP_KERNEL");
+    pl->kernel = (kv && std::string(kv) == "v1") ? 1 : 2;
+    if (const char *fc = std::getenv("OOB_DP_WCFG")) pl->force_cfg = std::atoi(fc);
+    if (L > 32 * 4) pl->kernel = 1;            // a row must fit one warp of tiles
+    for (int ci = 0; ci < NWCFG; ++ci) build_tiles(pl, ci);
+    pl->waves.assign(L + 1, WaveHost());
+    size_t items_total = 0, part_max = 0;
+    for (int l = 2; l <= L; ++l) {
+        WaveHost best;
+        double best_t = 1e300;
+        for (int ci = 0; ci < NWCFG; ++ci) {
+            if (pl->force_cfg >= 0 && ci != pl->force_cfg) continue;
+            if (L > 32 * WCFGS[ci].te) continue;
+            WaveHost wh;
+            build_items(pl, l, ci, 4 * 148, wh);
+            // resident CTAs per SM: 16 warps by registers (launch bounds 256 x 2), smem
+            const int by_warps = (WCFGS[ci].te <= 4 ? 16 : 8) / (WCFGS[ci].nt / 32);
+            const int by_smem = std::max<int>(1, (int)((227 * 1024) / std::max<size_t>(wh.smem, 1)));
+            const int per_sm = std::max(1, std::min(by_warps, by_smem));
+            const double warps_per_smsp = per_sm * (WCFGS[ci].nt / 32) / 4.0;
+            // issue efficiency saturates at ~4 resident warps per scheduler
+            const double eff = std::min(1.0, warps_per_smsp / 4.0);
+            const double t = wh.cost / (4.0 * 148.0 * eff);
+            if (t < best_t) { best_t = t; best = wh; }
+        }
+        pl->waves[l] = best;
+        WaveHost &wh = pl->waves[l];
+        wh.items_off = items_total;
+        items_total += wh.items.size() * sizeof(int32_t);
+        part_max = std::max(part_max, (size_t)num_profiles * (L - l + 1) * wh.nitems * wh.nout);
+        pl->max_smem = std::max(pl->max_smem, wh.smem);
+    }
+    if (pl->max_smem > 227 * 1024) pl->kernel = 1;
+    if (std::getenv("OOB_DP_DEBUG")) {
+        for (int l = 2; l <= L; ++l) {
+            const WaveHost &wh = pl->waves[l];
+            std::fprintf(stderr, "l=%d cfg=%d (TE=%d NT=%d) items=%d ctas=%lld smem=%zu cost=%.3g\n", l, wh.cfg,
+                         WCFGS[wh.cfg].te, WCFGS[wh.cfg].nt, wh.nitems,
+                         (long long)wh.nitems * (L - l + 1) * num_profiles, wh.smem, wh.cost);
+        }
+    }
+    pl->launches = 1 + 1 + (pl->kernel == 1 ? (L - 1) : 0);
+    if (pl->kernel == 2)
+        for (int l = 2; l <= L; ++l) pl->launches += 2 + (pl->waves[l].small_warps > 0 ? 1 : 0);
+
     size_t o = 0;
     pl->off_cells = o; o = align_up(o + sizeof(int32_t) * (L + 1), 256);
     pl->off_base = o;  o = align_up(o + sizeof(int64_t) * (L + 2), 256);
     pl->off_off = o;   o = align_up(o + sizeof(int32_t) * (size_t)(L + 1) * g.A, 256);
+    pl->off_tiles = o; o = align_up(o + sizeof(int32_t) * pl->tiles.size(), 256);
+    pl->off_tile_off = o; o = align_up(o + sizeof(int32_t) * (L + 1) * NWCFG, 256);
+    pl->off_tile_np = o;  o = align_up(o + sizeof(int32_t) * (L + 1) * NWCFG, 256);
+    pl->off_items = o;    o = align_up(o + items_total, 256);
     pl->geom_bytes = o;
     const size_t n = (size_t)g.total_cells * num_profiles;
     pl->off_T1 = o;  o = align_up(o + 8 * n, 256);
@@ -258,12 +471,27 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     pl->off_KD = o;  o = align_up(o + 8 * n, 256);
     pl->off_ARG = o; o = align_up(o + 4 * n, 256);
     pl->off_STK = o; o = align_up(o + 8 * (size_t)num_profiles * (n_hi - n_lo + 1) * (L + 1), 256);
+    if (pl->kernel == 2) {
+        pl->off_PB = o; o = align_up(o + 8 * part_max, 256);
+        pl->off_PK = o; o = align_up(o + 4 * part_max, 256);
+    }
     pl->ws_bytes = o;
     pl->tpl_bytes = packed_template_bytes(L);
     pl->geom_blob.assign(pl->geom_bytes, 0);
-    std::memcpy(pl->geom_blob.data() + pl->off_cells, g.cells.data(), sizeof(int32_t) * (L + 1));
-    std::memcpy(pl->geom_blob.data() + pl->off_base, g.base.data(), sizeof(int64_t) * (L + 2));
-    std::memcpy(pl->geom_blob.data() + pl->off_off, g.off.data(), sizeof(int32_t) * (size_t)(L + 1) * g.A);
+    unsigned char *b = pl->geom_blob.data();
+    std::memcpy(b + pl->off_cells, g.cells.data(), sizeof(int32_t) * (L + 1));
+    std::memcpy(b + pl->off_base, g.base.data(), sizeof(int64_t) * (L + 2));
+    std::memcpy(b + pl->off_off, g.off.data(), sizeof(int32_t) * (size_t)(L + 1) * g.A);
+    if (!pl->tiles.empty()) std::memcpy(b + pl->off_tiles, pl->tiles.data(), sizeof(int32_t) * pl->tiles.size());
+    for (int ci = 0; ci < NWCFG; ++ci) {
+        std::memcpy(b + pl->off_tile_off + sizeof(int32_t) * (L + 1) * ci, pl->tab[ci].off.data(), sizeof(int32_t) * (L + 1));
+        std::memcpy(b + pl->off_tile_np + sizeof(int32_t) * (L + 1) * ci, pl->tab[ci].np.data(), sizeof(int32_t) * (L + 1));
+    }
+    for (int l = 2; l <= L; ++l) {
+        const WaveHost &wh = pl->waves[l];
+        if (!wh.items.empty())
+            std::memcpy(b + pl->off_items + wh.items_off, wh.items.data(), wh.items.size() * sizeof(int32_t));
+    }
     *out = pl;
     return OOB_OK;
 }
@@ -282,7 +510,7 @@ extern "C" oob_status oob_dp_plan_info(const oob_dp_plan *pl, oob_dp_info *out) 
     out->wavefronts = g.L - 1;
     out->cells_per_profile = g.total_cells;
     out->splits_per_profile = g.total_splits;
-    out->kernel_launches = 1 + (g.L - 1) + 1;
+    out->kernel_launches = pl->launches;
     out->workspace_bytes = pl->ws_bytes;
     out->packed_template_bytes = pl->tpl_bytes;
     out->packed_profile_bytes = pl->tpl_bytes * (size_t)(g.n_hi - g.n_lo + 1);
@@ -336,6 +564,13 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
         e = cudaStreamSynchronize(stream);
         if (e != cudaSuccess) return cuda_fail(e, "geometry upload sync");
         pl->uploaded_to = d_ws;
+        if (pl->kernel == 2) {
+            const int sm = (int)std::max<size_t>(pl->max_smem, 48 * 1024);
+            e = cudaFuncSetAttribute(k_wave_w<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(k_wave_w<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(k_wave_w)");
+        }
     }
     DevGeom dg;
     dg.L = G.L; dg.M = G.M; dg.n_lo = G.n_lo; dg.n_hi = G.n_hi; dg.A = G.A; dg.P = pl->P;
@@ -367,13 +602,48 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
         }
     }
     for (int l = 2; l <= G.L; ++l) {
-        int64_t n = (int64_t)(G.L - l + 1) * G.cells[l] * pl->P;
-        if (n == 0) continue;
+        if (pl->kernel == 1) {
+            int64_t n = (int64_t)(G.L - l + 1) * G.cells[l] * pl->P;
+            if (n == 0) continue;
+            if (pl->timing) cudaEventRecord(pl->ev[pl->ev_used], stream);
+            k_wave_v1<<<(unsigned)((n + 127) / 128), 128, 0, stream>>>(dg, l);
+            if (pl->timing) { cudaEventRecord(pl->ev[pl->ev_used + 1], stream); pl->ev_used += 2; }
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_fail(e, "k_wave_v1 launch");
+            continue;
+        }
+        const WaveHost &wh = pl->waves[l];
+        if (wh.small_warps > 0) {
+            const int64_t threads = wh.small_warps * 32;
+            k_wave_small<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(dg, l);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_fail(e, "k_wave_small launch");
+        }
+        WaveW w;
+        w.l = l;
+        w.nranges = G.L - l + 1;
+        w.nitems = wh.nitems;
+        w.items = (const int4 *)(ws + pl->off_items + wh.items_off);
+        w.nout = wh.nout;
+        w.ns_max = wh.ns_max;
+        w.PB = (double *)(ws + pl->off_PB);
+        w.PK = (uint32_t *)(ws + pl->off_PK);
+        w.tile_off = (const int32_t *)(ws + pl->off_tile_off) + (size_t)(G.L + 1) * wh.cfg;
+        w.tile_np = (const int32_t *)(ws + pl->off_tile_np) + (size_t)(G.L + 1) * wh.cfg;
+        w.tiles = (const int32_t *)(ws + pl->off_tiles);
+        const int64_t ctas = (int64_t)pl->P * w.nranges * w.nitems;
         if (pl->timing) cudaEventRecord(pl->ev[pl->ev_used], stream);
-        k_wave_v1<<<(unsigned)((n + 127) / 128), 128, 0, stream>>>(dg, l);
+        if (WCFGS[wh.cfg].te == 4)
+            k_wave_w<4><<<(unsigned)ctas, WCFGS[wh.cfg].nt, wh.smem, stream>>>(dg, w);
+        else
+            k_wave_w<8><<<(unsigned)ctas, WCFGS[wh.cfg].nt, wh.smem, stream>>>(dg, w);
         if (pl->timing) { cudaEventRecord(pl->ev[pl->ev_used + 1], stream); pl->ev_used += 2; }
         e = cudaGetLastError();
-        if (e != cudaSuccess) return cuda_fail(e, "k_wave launch");
+        if (e != cudaSuccess) return cuda_fail(e, "k_wave_w launch");
+        const int64_t nf = (int64_t)pl->P * w.nranges * w.nout;
+        k_wave_w_finalize<<<(unsigned)((nf + 255) / 256), 256, 0, stream>>>(dg, w);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "k_wave_w_finalize launch");
     }
     {
         int n = (G.n_hi - G.n_lo + 1) * pl->P;

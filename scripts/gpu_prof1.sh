@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+python scripts/dp_once.py cfg4 1 > gpurun_out/plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg4.csv python scripts/dp_once.py cfg4 1 > gpurun_out/ncu1.log 2>&1
+echo launches=$?
+ncu --set full --clock-control none --import-source on -k regex:k_wave_w -s 58 -c 1 -o gpurun_out/prof_w60 python scripts/dp_once.py cfg4 1 > gpurun_out/ncu2.log 2>&1
+echo full=$?
+tail -3 gpurun_out/ncu2.log

@@ -143,3 +143,14 @@ def test_edge_cases(planner):
     with pytest.raises(OobError) as e:
         _gpu_set(planner, [prof], (4, 2, 3, 1, 2))
     assert e.value.status == OOB_E_INFEASIBLE
+
+
+@pytest.mark.parametrize("key", ["cfg2", "cfg3"])
+def test_v1_kernel_still_matches(planner, key, monkeypatch):
+    """The simple thread-per-cell kernel (OOB_DP_KERNEL=v1) stays parity-green too."""
+    monkeypatch.setenv("OOB_DP_KERNEL", "v1")
+    cfg = CONFIGS[key]
+    prof = config_profiles(cfg, "real")[0]
+    ts = _gpu_set(planner, [prof], (cfg.L, cfg.M, cfg.N, cfg.f, cfg.n0))
+    want, _ = coracle.template_set(prof.fwd_ms, prof.bwd_ms, cfg.M, cfg.n0, cfg.n_max)
+    _assert_same(ts.templates(0), want, key + " v1")
