@@ -20,7 +20,8 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 
 CU_SOURCES = ["oob_dp.cu"]
 CPP_SOURCES = ["oob_host.cpp", "oob_geometry.cpp", "oob_instantiate.cpp"]
-HEADERS = [os.path.join(CSRC, "oob_internal.h"), os.path.join(INC, "oobleck_plan.h")]
+HEADERS = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".h", ".cuh"))] + \
+    [os.path.join(INC, "oobleck_plan.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false",
               "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-I", INC, "-I", CSRC]

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -23,56 +24,14 @@
 #include <vector>
 
 #include "oob_internal.h"
-
-namespace oob {
-
-// ------------------------------------------------------------------ device geometry
-struct DevGeom {
-    int L, M, n_lo, n_hi, A, P;
-    int64_t C;                // cells per profile
-    const int32_t *cells;     // [L+1]
-    const int64_t *base;      // [L+2]
-    const int32_t *off;       // [(L+1)*A]
-    double *T1, *T3, *TS, *KD;  // [P*C]
-    uint32_t *ARG;              // [P*C]
-    uint64_t *STK;              // [P*p*(L+1)] backtrack stacks
-};
-
-__device__ __forceinline__ bool d_is_whole(const DevGeom &g, int a) { return a >= g.M - 1; }
-__device__ __forceinline__ int d_alloc_n(const DevGeom &g, int a) {
-    return d_is_whole(g, a) ? a - (g.M - 1) + 1 : a + 1;
-}
-__device__ __forceinline__ int d_lo(const DevGeom &g, int a) { return d_is_whole(g, a) ? d_alloc_n(g, a) : 1; }
-__device__ __forceinline__ int d_gpus(const DevGeom &g, int a) {
-    return d_is_whole(g, a) ? d_alloc_n(g, a) * g.M : d_alloc_n(g, a);
-}
-__device__ __forceinline__ int d_hi(const DevGeom &g, int a, int l) {
-    int gg = d_gpus(g, a);
-    return l < gg ? l : gg;
-}
-__device__ __forceinline__ int d_num_dsplits(const DevGeom &g, int a) {
-    int n = d_alloc_n(g, a);
-    return d_is_whole(g, a) ? (n >= 2 ? n - 1 : g.M - 1) : n - 1;
-}
-// j-th device split of a (same order as the oracle's device_splits)
-__device__ __forceinline__ void d_dsplit(const DevGeom &g, int a, int j, int &a1, int &a2) {
-    int n = d_alloc_n(g, a);
-    int m = j + 1;
-    if (d_is_whole(g, a) && n >= 2) { a1 = (g.M - 1) + m - 1; a2 = (g.M - 1) + (n - m) - 1; }
-    else if (d_is_whole(g, a))      { a1 = m - 1; a2 = g.M - m - 1; }
-    else                            { a1 = m - 1; a2 = n - m - 1; }
-}
-__device__ __forceinline__ int64_t d_cell(const DevGeom &g, int Sp, int u, int l, int a) {
-    return g.base[l] + (int64_t)u * g.cells[l] + g.off[l * g.A + a] + (Sp - d_lo(g, a));
-}
-
-}  // namespace oob
+#include "oob_dp_common.cuh"
 #include "oob_wave_w.cuh"
+
 namespace oob {
 
 // ------------------------------------------------------------------ K_base: Eq.4
 // One thread per (profile, u, base alloc) of wavefront l = blockIdx.y + 1.  Base allocs:
-// I(r), r = 1..M-1 (d = r) and W(1) (d = M).
+// I(r), r = 1..M-1 (d = r) and W(1) (d = M).  t = sum_{k=u}^{v-1}(F + B) left to right.
 __global__ void k_base(DevGeom g, const double *__restrict__ fwd, const double *__restrict__ bwd) {
     const int l = blockIdx.y + 1;
     const int nu = g.L - l + 1;
@@ -82,21 +41,21 @@ __global__ void k_base(DevGeom g, const double *__restrict__ fwd, const double *
     const int p = (int)(t / per_prof);
     const int r = (int)(t % per_prof);
     const int u = r / g.M;
-    const int ai = r % g.M;                 // 0..M-2 -> I(ai+1); M-1 -> W(1)
-    const int a = ai;                        // alloc index coincides (W(1) = M-1)
-    const int d = ai + 1;                    // I(r): r GPUs; W(1): M GPUs
+    const int a = r % g.M;                 // 0..M-2 -> I(a+1); M-1 -> W(1)
+    const int d = a + 1;                   // I(r): r GPUs; W(1): M GPUs
     if (g.off[l * g.A + a] < 0) return;
     const double *F = fwd + (size_t)p * g.L * g.M;
     const double *B = bwd + (size_t)p * g.L * g.M;
     double s = 0.0;
     for (int k = u; k < u + l; ++k) s = __dadd_rn(s, __dadd_rn(F[k * g.M + d - 1], B[k * g.M + d - 1]));
     const int64_t c = (int64_t)p * g.C + d_cell(g, 1, u, l, a);
-    g.T1[c] = s; g.T3[c] = s; g.TS[c] = s; g.KD[c] = 0.0;
+    d_store(g.CELL + c, s, s, s, 2.0);    // T1 = T3 = t* = t; C1 = 3*1 - 1 + k*(=0)
     g.ARG[c] = 0xFFFFFFFFu;
 }
 
 // ------------------------------------------------------------------ K_wave (v1)
-// One thread per (profile, u, cell of the slab) for wavefront l; S' = 1 cells are skipped.
+// Reference kernel: one thread per (profile, u, cell of the slab) for wavefront l; loops the
+// splits in the oracle's (k, m, s) order with a strict "<".  S' = 1 cells are skipped.
 __global__ void k_wave_v1(DevGeom g, int l) {
     const int nu = g.L - l + 1;
     const int cl = g.cells[l];
@@ -106,7 +65,6 @@ __global__ void k_wave_v1(DevGeom g, int l) {
     const int rem = (int)(t % ((int64_t)nu * cl));
     const int u = rem / cl;
     const int i = rem % cl;
-    // find the allocation holding slab offset i
     int a = 0, Sp = 0;
     for (int aa = 0; aa < g.A; ++aa) {
         int o = g.off[l * g.A + aa];
@@ -119,8 +77,7 @@ __global__ void k_wave_v1(DevGeom g, int l) {
     const int64_t pc = (int64_t)p * g.C;
     const double dSp3 = (double)(3 * Sp - 1);
     double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
-    double bT1 = 0, bT3 = 0, bTS = 0, bKD = 0;
-    uint32_t barg = 0xFFFFFFFFu;
+    int bl1 = 0, bj = 0, bs = 0;
     const int nd = d_num_dsplits(g, a);
     for (int k = u + 1; k < v; ++k) {
         const int l1 = k - u, l2 = v - k;
@@ -131,26 +88,20 @@ __global__ void k_wave_v1(DevGeom g, int l) {
             int s_lo = max(max(1, d_lo(g, a1)), Sp - d_hi(g, a2, l2));
             int s_hi = min(min(Sp - 1, d_hi(g, a1, l1)), Sp - d_lo(g, a2));
             for (int s = s_lo; s <= s_hi; ++s) {
-                const int64_t cL = pc + d_cell(g, s, u, l1, a1);
-                const int64_t cR = pc + d_cell(g, Sp - s, k, l2, a2);
-                const double LT1 = g.T1[cL], LT3 = g.T3[cL], LTS = g.TS[cL], LKD = g.KD[cL];
-                const double RT1 = g.T1[cR], RT3 = g.T3[cR], RTS = g.TS[cR], RKD = g.KD[cR];
-                const double T1 = __dadd_rn(LT1, RT1);
-                const bool left = LTS >= RTS;
-                const double T3 = left ? __dadd_rn(LT3, RT1) : RT3;
-                const double TS = left ? LTS : RTS;
-                const double KD = left ? LKD : __dadd_rn((double)s, RKD);
+                const Cell4 Lc = d_load(g.CELL + pc + d_cell(g, s, u, l1, a1));
+                const Cell4 Rc = d_load(g.CELL + pc + d_cell(g, Sp - s, k, l2, a2));
+                const double T1 = __dadd_rn(Lc.T1, Rc.T1);
+                const bool left = Lc.TS >= Rc.TS;
+                const double T3 = left ? __dadd_rn(Lc.T3, Rc.T1) : Rc.T3;
+                const double TS = left ? Lc.TS : Rc.TS;
+                const double KD = left ? d_kd(Lc.C1, s) : __dadd_rn((double)s, d_kd(Rc.C1, Sp - s));
                 const double T2 = __dmul_rn(__dadd_rn(KD, dSp3), TS);
                 const double tot = __dadd_rn(__dadd_rn(T1, T2), T3);
-                if (tot < best) {
-                    best = tot; bT1 = T1; bT3 = T3; bTS = TS; bKD = KD;
-                    barg = (uint32_t)(l1 - 1) | ((uint32_t)j << 10) | ((uint32_t)s << 20);
-                }
+                if (tot < best) { best = tot; bl1 = l1; bj = j; bs = s; }
             }
         }
     }
-    const int64_t c = pc + d_cell(g, Sp, u, l, a);
-    g.T1[c] = bT1; g.T3[c] = bT3; g.TS[c] = bTS; g.KD[c] = bKD; g.ARG[c] = barg;
+    d_write_winner(g, pc, Sp, u, l, a, bl1, bj, bs);
 }
 
 // ------------------------------------------------------------------ K_extract
@@ -171,15 +122,15 @@ __global__ void k_extract(DevGeom g, unsigned char *packed, size_t tpl_bytes) {
     double best = 0.0;
     const int Smax = min(L, n * g.M);
     for (int S = n; S <= Smax; ++S) {
-        const int64_t c = pc + d_cell(g, S, 0, L, aW);
-        const double T2 = __dmul_rn(__dadd_rn(g.KD[c], (double)(3 * S - 1)), g.TS[c]);
-        const double tot = __dadd_rn(__dadd_rn(g.T1[c], T2), g.T3[c]);
+        const Cell4 c = d_load(g.CELL + pc + d_cell(g, S, 0, L, aW));
+        const double T2 = __dmul_rn(c.C1, c.TS);      // (4S - S + k* - 1) t*, Eq.2
+        const double tot = __dadd_rn(__dadd_rn(c.T1, T2), c.T3);
         if (bestS < 0 || tot < best) { best = tot; bestS = S; }
     }
-    const int64_t c = pc + d_cell(g, bestS, 0, L, aW);
-    h->nodes = n; h->S = bestS; h->kstar = (int)g.KD[c]; h->status = 0;
-    h->T1 = g.T1[c]; h->T3 = g.T3[c]; h->tstar = g.TS[c];
-    h->T2 = __dmul_rn(__dadd_rn(g.KD[c], (double)(3 * bestS - 1)), g.TS[c]);
+    const Cell4 c = d_load(g.CELL + pc + d_cell(g, bestS, 0, L, aW));
+    h->nodes = n; h->S = bestS; h->kstar = (int)d_kd(c.C1, bestS); h->status = 0;
+    h->T1 = c.T1; h->T3 = c.T3; h->tstar = c.TS;
+    h->T2 = __dmul_rn(c.C1, c.TS);
     h->iter = best;
     h->pad = 0.0;
     // explicit DFS stack in the workspace (<= L pending entries): packed
@@ -221,7 +172,6 @@ __global__ void k_extract(DevGeom g, unsigned char *packed, size_t tpl_bytes) {
 
 }  // namespace oob
 
-
 // ==================================================================== plan + C ABI
 using namespace oob;
 
@@ -235,8 +185,10 @@ constexpr int NWCFG = 4;
 struct WaveHost {
     int cfg = 0;                   // index into WCFGS
     int nitems = 0, ns_max = 0, nout = 0;
-    size_t items_off = 0;          // byte offset of this wavefront's int4 items in the blob
-    std::vector<int32_t> items;    // 4 ints per item
+    size_t items_off = 0, ents_off = 0, cb_off = 0;   // byte offsets in the blob's items region
+    std::vector<int32_t> items;    // 4 ints per item: (entry_lo, entry_hi, 0, 0)
+    std::vector<int32_t> ents;     // 4 ints per entry: (l1, nblocks, nchunks, chunk_off)
+    std::vector<int32_t> cb;       // chunk row boundaries
     size_t smem = 0;
     int64_t small_warps = 0;
     double cost = 0.0;
@@ -250,8 +202,7 @@ int wlen_h(const Geometry &g, int l, int q) {
 int wcells_h(const Geometry &g, int l) { return g.cells[l] - g.off[(size_t)l * g.A + (g.M - 1)]; }
 
 struct TileTab {
-    std::vector<int32_t> off, np;            // [L+1]
-    std::vector<std::vector<int>> active;    // [L+1][pass] active warps
+    std::vector<int32_t> off, cnt;           // [L+1] flat tile list of a big side of length lb
 };
 
 }  // namespace
@@ -263,11 +214,11 @@ struct oob_dp_plan {
     int force_cfg = -1;
     size_t geom_bytes = 0, ws_bytes = 0, tpl_bytes = 0;
     std::vector<unsigned char> geom_blob;   // host image of the geometry region
-    size_t off_cells = 0, off_base = 0, off_off = 0, off_tiles = 0, off_tile_off = 0, off_tile_np = 0,
+    size_t off_cells = 0, off_base = 0, off_off = 0, off_tiles = 0, off_tile_off = 0, off_tile_cnt = 0,
            off_items = 0;
-    size_t off_T1 = 0, off_T3 = 0, off_TS = 0, off_KD = 0, off_ARG = 0, off_STK = 0, off_PB = 0, off_PK = 0;
-    std::vector<int32_t> tiles;          // all configs' tables concatenated
-    TileTab tab[NWCFG];
+    size_t off_CELL = 0, off_ARG = 0, off_STK = 0, off_PB = 0, off_PK = 0;
+    std::vector<int32_t> tiles;          // all TE's tables concatenated
+    TileTab tab[2];                      // TE = 4, TE = 8
     std::vector<WaveHost> waves;         // [L+1]
     size_t max_smem = 0;
     int64_t launches = 0;
@@ -285,116 +236,121 @@ static oob_status cuda_fail(cudaError_t e, const char *what) {
     return fail(OOB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-// Tile tables for one (TE, NT): for a big side of length lb, its W rows j = 1..min(Q, lb)
-// are cut into ceil(len/TE) lane tiles; rows are assigned IN ORDER to consecutive warps
-// (a row never straddles warps; warp w's rows all precede warp w+1's — the neighbour
-// chain of k_wave_w relies on it), NT/32 warps per pass.
-static void build_tiles(oob_dp_plan *pl, int ci) {
+static int te_index(int te) { return te == 4 ? 0 : 1; }
+
+// Flat tile lists: for a big side of length lb, its W rows j = 1..min(Q, lb) cut into
+// ceil(len/TE) tiles of TE consecutive cells, in row order; 32 consecutive tiles form one
+// warp work unit of k_wave_w.
+static void build_tiles(oob_dp_plan *pl, int TE) {
     const Geometry &g = pl->g;
-    const int TE = WCFGS[ci].te, NT = WCFGS[ci].nt, WARPS = NT / 32;
-    TileTab &T = pl->tab[ci];
+    TileTab &T = pl->tab[te_index(TE)];
     T.off.assign(g.L + 1, 0);
-    T.np.assign(g.L + 1, 0);
-    T.active.assign(g.L + 1, {});
+    T.cnt.assign(g.L + 1, 0);
     for (int lb = 1; lb <= g.L; ++lb) {
         const int J = std::min(Q_of(g, lb), lb);
-        std::vector<std::vector<std::pair<int, int>>> wrows;   // per warp: (row, lanes)
-        int used = 32;
+        T.off[lb] = (int32_t)pl->tiles.size();
         for (int j = 1; j <= J; ++j) {
             const int len = wlen_h(g, lb, j);
-            if (len <= 0) continue;
-            const int need = (len + TE - 1) / TE;
-            if (used + need > 32) { wrows.push_back({}); used = 0; }
-            wrows.back().push_back({j, need});
-            used += need;
+            for (int e0 = 0; e0 < len; e0 += TE) pl->tiles.push_back((j << 16) | e0);
         }
-        const int nw = (int)wrows.size();
-        const int np = (nw + WARPS - 1) / WARPS;
-        T.off[lb] = (int32_t)pl->tiles.size();
-        T.np[lb] = np;
-        std::vector<int32_t> tab((size_t)np * NT, -1);
-        for (int w = 0; w < nw; ++w) {
-            int lane = 0;
-            for (auto &rr : wrows[w])
-                for (int t = 0; t < rr.second; ++t, ++lane)
-                    tab[(size_t)(w / WARPS) * NT + (w % WARPS) * 32 + lane] = (rr.first << 16) | (t * TE);
-        }
-        for (int p = 0; p < np; ++p) T.active[lb].push_back(std::min(WARPS, nw - p * WARPS));
-        pl->tiles.insert(pl->tiles.end(), tab.begin(), tab.end());
+        T.cnt[lb] = (int32_t)pl->tiles.size() - T.off[lb];
     }
 }
 
-// Issue-cycle model of one k (SMSP issue slots): every active warp of every pass walks all
-// staged rows; a step costs TE splits (~22 instructions each) plus the flush (~14).
-static double k_cost(const oob_dp_plan *pl, int ci, int l, int l1, int it_lo, int it_hi) {
+// Issue-cycle model of one k restricted to small-side rows [it_lo, it_hi): every unit
+// (32 lanes) walks its rows; a step costs TE splits (~20 instructions each) plus the load
+// and the merge (~24).
+static double k_cost(const oob_dp_plan *pl, int TE, int l, int l1, int it_lo, int it_hi) {
     const Geometry &g = pl->g;
-    const int TE = WCFGS[ci].te;
     const int l2 = l - l1;
     const bool lt = wcells_h(g, l1) >= wcells_h(g, l2);
     const int ls = lt ? l2 : l1, lb = lt ? l1 : l2;
     const int JS = std::min(Q_of(g, ls), ls);
     double steps = 0.0;
-    for (int r = std::max(1, it_lo); r <= std::min(JS, it_hi - 1); ++r) steps += wlen_h(g, ls, r) + 3;
-    double aw = 0.0;
-    for (int a : pl->tab[ci].active[lb]) aw += a;
-    return aw * steps * (TE * 22.0 + 14.0) + 2000.0;
+    for (int r = std::max(1, it_lo); r <= std::min(JS, it_hi - 1); ++r) steps += wlen_h(g, ls, r) + 2.0;
+    const double units = (pl->tab[te_index(TE)].cnt[lb] + 31) / 32;
+    return units * (steps * (TE * 20.0 + 24.0) + 400.0);
 }
 
-// Work items of wavefront l, balanced by the cost model: items are (l1 range, staged-row
-// range); a k heavier than 1.5x the per-item target is split by staged rows.
+// Work items of wavefront l, balanced by the cost model: an item is a list of entries
+// (l1, small-side rows) — a k range, or one k's row range when that k alone exceeds 1.5x
+// the per-item target.  Each entry's rows are cut into chunks of ~CH steps; a warp unit
+// is (entry, chunk, 32-tile block).
 static void build_items(oob_dp_plan *pl, int l, int ci, int target_ctas, WaveHost &wh) {
     const Geometry &g = pl->g;
+    const int TE = WCFGS[ci].te;
     const int nr = g.L - l + 1;
+    const int CH = 96;
     std::vector<double> cost(l, 0.0);
     double total = 0.0;
-    int ns_max = 0;
     for (int l1 = 1; l1 < l; ++l1) {
-        cost[l1] = k_cost(pl, ci, l, l1, 1, 1 << 20);
+        cost[l1] = k_cost(pl, TE, l, l1, 1, 1 << 20);
         total += cost[l1];
-        const int l2 = l - l1;
-        ns_max = std::max(ns_max, std::min(wcells_h(g, l1), wcells_h(g, l2)));
     }
     const int per_range = std::max(1, (target_ctas + pl->P * nr - 1) / (pl->P * nr));
     const double target = total / per_range;
-    std::vector<int32_t> items;
-    int cur_lo = 1;
-    double cur = 0.0;
+    // (l1, row_lo, row_hi) triples grouped into items
+    std::vector<std::vector<std::array<int, 3>>> items;
+    std::vector<std::array<int, 3>> cur;
+    double curc = 0.0;
+    auto small_rows = [&](int l1) {
+        const int l2 = l - l1;
+        const bool lt = wcells_h(g, l1) >= wcells_h(g, l2);
+        const int ls = lt ? l2 : l1;
+        return std::make_pair(ls, std::min(Q_of(g, ls), ls));
+    };
     for (int l1 = 1; l1 < l; ++l1) {
+        const int JS = small_rows(l1).second;
         if (cost[l1] > 1.5 * target && per_range > 1) {
-            if (cur_lo < l1) items.insert(items.end(), {cur_lo, l1, 1, 1 << 20});
+            if (!cur.empty()) { items.push_back(cur); cur.clear(); curc = 0.0; }
             const int pieces = std::max(1, (int)std::lround(cost[l1] / target));
-            const int l2 = l - l1;
-            const bool lt = wcells_h(g, l1) >= wcells_h(g, l2);
-            const int ls = lt ? l2 : l1;
-            const int JS = std::min(Q_of(g, ls), ls);
             const double piece = cost[l1] / pieces;
             int r0 = 1;
             for (int r = 1; r <= JS; ++r) {
-                if (k_cost(pl, ci, l, l1, r0, r + 1) >= piece && r < JS) {
-                    items.insert(items.end(), {l1, l1 + 1, r0, r + 1});
+                if (k_cost(pl, TE, l, l1, r0, r + 1) >= piece && r < JS) {
+                    items.push_back({{l1, r0, r + 1}});
                     r0 = r + 1;
                 }
             }
-            items.insert(items.end(), {l1, l1 + 1, r0, 1 << 20});
-            cur_lo = l1 + 1;
-            cur = 0.0;
+            items.push_back({{l1, r0, JS + 1}});
             continue;
         }
-        cur += cost[l1];
-        if (cur >= target && per_range > 1) {
-            items.insert(items.end(), {cur_lo, l1 + 1, 1, 1 << 20});
-            cur_lo = l1 + 1;
-            cur = 0.0;
-        }
+        cur.push_back({l1, 1, JS + 1});
+        curc += cost[l1];
+        if (curc >= target && per_range > 1) { items.push_back(cur); cur.clear(); curc = 0.0; }
     }
-    if (cur_lo < l) items.insert(items.end(), {cur_lo, l, 1, 1 << 20});
+    if (!cur.empty()) items.push_back(cur);
+    wh.items.clear();
+    wh.ents.clear();
+    wh.cb.clear();
+    for (auto &itv : items) {
+        const int elo = (int)(wh.ents.size() / 4);
+        for (auto &tr : itv) {
+            const int l1 = tr[0];
+            const int l2 = l - l1;
+            const bool lt = wcells_h(g, l1) >= wcells_h(g, l2);
+            const int ls = lt ? l2 : l1, lb = lt ? l1 : l2;
+            const int nblocks = (pl->tab[te_index(TE)].cnt[lb] + 31) / 32;
+            const int coff = (int)wh.cb.size();
+            // chunk c holds the rows whose preceding-step count floor-divides to c
+            int nchunks = 0, acc = 0, last = -1;
+            for (int r = tr[1]; r < tr[2]; ++r) {
+                const int c = acc / CH;
+                if (c != last) { wh.cb.push_back(r); ++nchunks; last = c; }
+                acc += wlen_h(g, ls, r);
+            }
+            wh.cb.push_back(tr[2]);
+            if (nchunks == 0 || nblocks == 0) { wh.cb.resize(coff); continue; }
+            wh.ents.insert(wh.ents.end(), {l1, nblocks, nchunks, coff});
+        }
+        const int ehi = (int)(wh.ents.size() / 4);
+        if (ehi > elo) wh.items.insert(wh.items.end(), {elo, ehi, 0, 0});
+    }
     wh.cfg = ci;
-    wh.items = items;
-    wh.nitems = (int)items.size() / 4;
-    wh.ns_max = ns_max;
+    wh.nitems = (int)wh.items.size() / 4;
+    wh.ns_max = 0;
     wh.nout = wcells_h(g, l);
-    wh.smem = align_up((size_t)wh.nout * 12, 16) + (size_t)ns_max * 40 + 3 * (size_t)(g.L + 2) * 4 +
-              (size_t)(WCFGS[ci].nt / 32) * 4;
+    wh.smem = align_up((size_t)wh.nout * 16, 16) + 2 * (size_t)(g.L + 2) * 4 + 16;
     wh.cost = total * pl->P * nr;
     int per = 0;
     for (int a = 0; a < std::min(g.A, g.M); ++a) per += std::max(0, std::min(l, g.gpus(a)) - 1);
@@ -413,8 +369,8 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     const char *kv = std::getenv("OOB_DP_KERNEL");
     pl->kernel = (kv && std::string(kv) == "v1") ? 1 : 2;
     if (const char *fc = std::getenv("OOB_DP_WCFG")) pl->force_cfg = std::atoi(fc);
-    if (L > 32 * 4) pl->kernel = 1;            // a row must fit one warp of tiles
-    for (int ci = 0; ci < NWCFG; ++ci) build_tiles(pl, ci);
+    build_tiles(pl, 4);
+    build_tiles(pl, 8);
     pl->waves.assign(L + 1, WaveHost());
     size_t items_total = 0, part_max = 0;
     for (int l = 2; l <= L; ++l) {
@@ -422,7 +378,6 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
         double best_t = 1e300;
         for (int ci = 0; ci < NWCFG; ++ci) {
             if (pl->force_cfg >= 0 && ci != pl->force_cfg) continue;
-            if (L > 32 * WCFGS[ci].te) continue;
             WaveHost wh;
             build_items(pl, l, ci, 4 * 148, wh);
             // resident CTAs per SM: 16 warps by registers (launch bounds 256 x 2), smem
@@ -438,7 +393,11 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
         pl->waves[l] = best;
         WaveHost &wh = pl->waves[l];
         wh.items_off = items_total;
-        items_total += wh.items.size() * sizeof(int32_t);
+        items_total += align_up(wh.items.size() * sizeof(int32_t), 16);
+        wh.ents_off = items_total;
+        items_total += align_up(wh.ents.size() * sizeof(int32_t), 16);
+        wh.cb_off = items_total;
+        items_total += align_up(wh.cb.size() * sizeof(int32_t), 16);
         part_max = std::max(part_max, (size_t)num_profiles * (L - l + 1) * wh.nitems * wh.nout);
         pl->max_smem = std::max(pl->max_smem, wh.smem);
     }
@@ -460,15 +419,12 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     pl->off_base = o;  o = align_up(o + sizeof(int64_t) * (L + 2), 256);
     pl->off_off = o;   o = align_up(o + sizeof(int32_t) * (size_t)(L + 1) * g.A, 256);
     pl->off_tiles = o; o = align_up(o + sizeof(int32_t) * pl->tiles.size(), 256);
-    pl->off_tile_off = o; o = align_up(o + sizeof(int32_t) * (L + 1) * NWCFG, 256);
-    pl->off_tile_np = o;  o = align_up(o + sizeof(int32_t) * (L + 1) * NWCFG, 256);
+    pl->off_tile_off = o; o = align_up(o + sizeof(int32_t) * (L + 1) * 2, 256);
+    pl->off_tile_cnt = o; o = align_up(o + sizeof(int32_t) * (L + 1) * 2, 256);
     pl->off_items = o;    o = align_up(o + items_total, 256);
     pl->geom_bytes = o;
     const size_t n = (size_t)g.total_cells * num_profiles;
-    pl->off_T1 = o;  o = align_up(o + 8 * n, 256);
-    pl->off_T3 = o;  o = align_up(o + 8 * n, 256);
-    pl->off_TS = o;  o = align_up(o + 8 * n, 256);
-    pl->off_KD = o;  o = align_up(o + 8 * n, 256);
+    pl->off_CELL = o; o = align_up(o + 32 * n, 256);
     pl->off_ARG = o; o = align_up(o + 4 * n, 256);
     pl->off_STK = o; o = align_up(o + 8 * (size_t)num_profiles * (n_hi - n_lo + 1) * (L + 1), 256);
     if (pl->kernel == 2) {
@@ -483,14 +439,18 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     std::memcpy(b + pl->off_base, g.base.data(), sizeof(int64_t) * (L + 2));
     std::memcpy(b + pl->off_off, g.off.data(), sizeof(int32_t) * (size_t)(L + 1) * g.A);
     if (!pl->tiles.empty()) std::memcpy(b + pl->off_tiles, pl->tiles.data(), sizeof(int32_t) * pl->tiles.size());
-    for (int ci = 0; ci < NWCFG; ++ci) {
-        std::memcpy(b + pl->off_tile_off + sizeof(int32_t) * (L + 1) * ci, pl->tab[ci].off.data(), sizeof(int32_t) * (L + 1));
-        std::memcpy(b + pl->off_tile_np + sizeof(int32_t) * (L + 1) * ci, pl->tab[ci].np.data(), sizeof(int32_t) * (L + 1));
+    for (int ti = 0; ti < 2; ++ti) {
+        std::memcpy(b + pl->off_tile_off + sizeof(int32_t) * (L + 1) * ti, pl->tab[ti].off.data(), sizeof(int32_t) * (L + 1));
+        std::memcpy(b + pl->off_tile_cnt + sizeof(int32_t) * (L + 1) * ti, pl->tab[ti].cnt.data(), sizeof(int32_t) * (L + 1));
     }
     for (int l = 2; l <= L; ++l) {
         const WaveHost &wh = pl->waves[l];
         if (!wh.items.empty())
             std::memcpy(b + pl->off_items + wh.items_off, wh.items.data(), wh.items.size() * sizeof(int32_t));
+        if (!wh.ents.empty())
+            std::memcpy(b + pl->off_items + wh.ents_off, wh.ents.data(), wh.ents.size() * sizeof(int32_t));
+        if (!wh.cb.empty())
+            std::memcpy(b + pl->off_items + wh.cb_off, wh.cb.data(), wh.cb.size() * sizeof(int32_t));
     }
     *out = pl;
     return OOB_OK;
@@ -578,10 +538,7 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
     dg.cells = (const int32_t *)(ws + pl->off_cells);
     dg.base = (const int64_t *)(ws + pl->off_base);
     dg.off = (const int32_t *)(ws + pl->off_off);
-    dg.T1 = (double *)(ws + pl->off_T1);
-    dg.T3 = (double *)(ws + pl->off_T3);
-    dg.TS = (double *)(ws + pl->off_TS);
-    dg.KD = (double *)(ws + pl->off_KD);
+    dg.CELL = (Cell4 *)(ws + pl->off_CELL);
     dg.ARG = (uint32_t *)(ws + pl->off_ARG);
     dg.STK = (uint64_t *)(ws + pl->off_STK);
 
@@ -624,12 +581,13 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
         w.nranges = G.L - l + 1;
         w.nitems = wh.nitems;
         w.items = (const int4 *)(ws + pl->off_items + wh.items_off);
+        w.ents = (const int4 *)(ws + pl->off_items + wh.ents_off);
+        w.cb = (const int32_t *)(ws + pl->off_items + wh.cb_off);
         w.nout = wh.nout;
-        w.ns_max = wh.ns_max;
         w.PB = (double *)(ws + pl->off_PB);
         w.PK = (uint32_t *)(ws + pl->off_PK);
-        w.tile_off = (const int32_t *)(ws + pl->off_tile_off) + (size_t)(G.L + 1) * wh.cfg;
-        w.tile_np = (const int32_t *)(ws + pl->off_tile_np) + (size_t)(G.L + 1) * wh.cfg;
+        w.tile_off = (const int32_t *)(ws + pl->off_tile_off) + (size_t)(G.L + 1) * te_index(WCFGS[wh.cfg].te);
+        w.tile_cnt = (const int32_t *)(ws + pl->off_tile_cnt) + (size_t)(G.L + 1) * te_index(WCFGS[wh.cfg].te);
         w.tiles = (const int32_t *)(ws + pl->off_tiles);
         const int64_t ctas = (int64_t)pl->P * w.nranges * w.nitems;
         if (pl->timing) cudaEventRecord(pl->ev[pl->ev_used], stream);
