@@ -64,13 +64,32 @@ __device__ __forceinline__ int d_wlen(const DevGeom &g, int l, int q) {
 // integers:
 //   T1 = L.T1 + R.T1; left = L.t* >= R.t*; T3 = left ? L.T3 + R.T1 : R.T3;
 //   T2 = coef * t*; total = (T1 + T2) + T3; keep if total <= best.
+// skip_r / skip_l: the second operand of that coefficient is +0 (t == 0), use the first.
 __device__ __forceinline__ void split_eval(double LT1, double LT3, double LTS, double cla, double clb,
                                            double RT1, double RT3, double RTS, double cra, double crb,
-                                           double &best, int &widx, int code) {
+                                           double &best, int &widx, int code, bool skip_r = false) {
     const double T1 = __dadd_rn(LT1, RT1);
     const double T3a = __dadd_rn(LT3, RT1);
     const bool left = LTS >= RTS;
     const double cL = __dadd_rn(cla, clb);
+    const double cR = skip_r ? cra : __dadd_rn(cra, crb);
+    const double TS = left ? LTS : RTS;
+    const double T3 = left ? T3a : RT3;
+    const double c = left ? cL : cR;
+    const double T2 = __dmul_rn(c, TS);
+    const double tot = __dadd_rn(__dadd_rn(T1, T2), T3);
+    const bool upd = tot <= best;
+    best = upd ? tot : best;
+    widx = upd ? code : widx;
+}
+
+__device__ __forceinline__ void split_eval2(double LT1, double LT3, double LTS, double cla, double clb,
+                                            double RT1, double RT3, double RTS, double cra, double crb,
+                                            double &best, int &widx, int code, bool skip_l) {
+    const double T1 = __dadd_rn(LT1, RT1);
+    const double T3a = __dadd_rn(LT3, RT1);
+    const bool left = LTS >= RTS;
+    const double cL = skip_l ? cla : __dadd_rn(cla, clb);
     const double cR = __dadd_rn(cra, crb);
     const double TS = left ? LTS : RTS;
     const double T3 = left ? T3a : RT3;
@@ -96,22 +115,31 @@ __device__ __forceinline__ void cas128(unsigned addr, unsigned long long &olo, u
                  : "memory");
 }
 
-// acc entry = {double total bits, key}: lexicographic-min update (exact under races)
-__device__ __forceinline__ void acc_merge(ulonglong2 *acc, int idx, double b, uint32_t key) {
-    const unsigned addr = (unsigned)__cvta_generic_to_shared(acc + idx);
-    unsigned long long cx, cy;   // one 16-byte shared load (single transaction)
-    asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(cx), "=l"(cy) : "r"(addr) : "memory");
+// acc entry = {double total bits, key}: lexicographic-min update (exact under races).
+// The slow path (a CAS loop) is out of line: most flushes lose the comparison.
+__device__ __noinline__ void acc_merge_slow(unsigned addr, unsigned long long cx, unsigned long long cy,
+                                            double b, uint32_t key) {
     const unsigned long long nb = (unsigned long long)__double_as_longlong(b);
     for (;;) {
-        const double A = __longlong_as_double((long long)cx);
-        const uint32_t K = (uint32_t)cy;
-        if (!(b < A || (b == A && key < K))) return;
         unsigned long long olo, ohi;
         cas128(addr, olo, ohi, cx, cy, nb, (unsigned long long)key);
         if (olo == cx && ohi == cy) return;
         cx = olo;
         cy = ohi;
+        const double A = __longlong_as_double((long long)cx);
+        const uint32_t K = (uint32_t)cy;
+        if (!(b < A || (b == A && key < K))) return;
     }
+}
+
+// flush one ring slot into the accumulator entry `idx` if `ok` (valid output, finite)
+__device__ __forceinline__ void acc_flush(const ulonglong2 *acc, int idx, bool ok, double b, uint32_t key) {
+    const unsigned addr = (unsigned)__cvta_generic_to_shared(acc + (ok ? idx : 0));
+    unsigned long long cx, cy;   // one 16-byte shared load (single transaction)
+    asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(cx), "=l"(cy) : "r"(addr) : "memory");
+    const double A = __longlong_as_double((long long)cx);
+    const uint32_t K = (uint32_t)cy;
+    if (ok && (b < A || (b == A && key < K))) acc_merge_slow(addr, cx, cy, b, key);
 }
 
 constexpr double D_INF = __builtin_huge_val();
@@ -210,39 +238,37 @@ __global__ void __launch_bounds__(NT_MAX, (TE <= 4 ? 2 : 1)) k_wave_w(DevGeom g,
                 // coef_right = 4 s_t + C1_R = (C1_R + 4 S0) + 4t.
                 // Ring slot r <-> output E with (E - e0) % TE == r.
                 const int j = rowB;
+                const uint32_t kb = ((uint32_t)l1 << 20) | ((uint32_t)j << 10) | (uint32_t)(j + e0);
                 double c3 = (double)(3 * rs);          // 3 S_R
                 const double s4 = 4.0 * S0;
+                Cell4 x = d_load(rp);
+                int ep = 0;
+#define OOB_LT_STEP(I)                                                                          \
+    {                                                                                           \
+        const Cell4 nx = d_load(rp + min(ep + (I) + 1, rl - 1));                                \
+        const double xr = __dadd_rn(x.C1, s4);                                                  \
+        _Pragma("unroll") for (int t = 0; t < TE; ++t)                                          \
+            split_eval(RT1[t], RT3[t], RTS[t], c3, RC1[t], x.T1, x.T3, x.TS, xr,                \
+                       (double)(4 * t), best[((I) + t) % TE], widx[((I) + t) % TE], t, t == 0); \
+        c3 = __dadd_rn(c3, 3.0);                                                                \
+        acc_flush(acc, ob + e0 + ep + (I), qok && best[(I)] < D_INF, best[(I)],                \
+                  kb + (uint32_t)widx[(I)]);                                                    \
+        best[(I)] = D_INF;                                                                      \
+        x = nx;                                                                                 \
+    }
 #pragma unroll 1
-                for (int base = 0; base < rl; base += TE) {
+                for (; ep + TE <= rl; ep += TE) {
 #pragma unroll
-                    for (int i = 0; i < TE; ++i) {
-                        const int ep = base + i;
-                        if (ep < rl) {
-                            const Cell4 x = d_load(rp + ep);
-                            const double xr = __dadd_rn(x.C1, s4);
-#pragma unroll
-                            for (int t = 0; t < TE; ++t)
-                                split_eval(RT1[t], RT3[t], RTS[t], c3, RC1[t],
-                                           x.T1, x.T3, x.TS, xr, (double)(4 * t),
-                                           best[(i + t) % TE], widx[(i + t) % TE], t);
-                            c3 = __dadd_rn(c3, 3.0);
-                            if (qok && best[i] < D_INF) {
-                                const uint32_t key = ((uint32_t)l1 << 20) | ((uint32_t)j << 10) |
-                                                     (uint32_t)(j + e0 + widx[i]);
-                                acc_merge(acc, ob + e0 + ep, best[i], key);
-                            }
-                            best[i] = D_INF;
-                        }
-                    }
+                    for (int i = 0; i < TE; ++i) OOB_LT_STEP(i)
                 }
 #pragma unroll
+                for (int i = 0; i < TE - 1; ++i)
+                    if (ep + i < rl) OOB_LT_STEP(i)
+#undef OOB_LT_STEP
+#pragma unroll
                 for (int r = 0; r < TE; ++r) {
-                    if (qok && best[r] < D_INF) {
-                        const int E = e0 + rl + (((r - rl) % TE) + TE) % TE;
-                        const uint32_t key = ((uint32_t)l1 << 20) | ((uint32_t)j << 10) |
-                                             (uint32_t)(j + e0 + widx[r]);
-                        acc_merge(acc, ob + E, best[r], key);
-                    }
+                    const int E = e0 + rl + (((r - rl) % TE) + TE) % TE;
+                    acc_flush(acc, ob + E, qok && best[r] < D_INF, best[r], kb + (uint32_t)widx[r]);
                 }
             } else {
                 // big = right row j' = rowB (S_R,t = S0 + t); iterate left row j = rs, e
@@ -250,44 +276,43 @@ __global__ void __launch_bounds__(NT_MAX, (TE <= 4 ? 2 : 1)) k_wave_w(DevGeom g,
                 // coef_right = 4s + C1_R[t].  Step i = rl-1-e; slot (t - i) % TE holds output
                 // E = e + e0 + t; the t = TE-1 output completes at each step.
                 const int jl = rs;
+                const uint32_t kb = ((uint32_t)l1 << 20) | ((uint32_t)jl << 10);
                 double c4 = (double)(4 * (rs + rl - 1));   // 4 s
                 const double s3 = 3.0 * S0;
+                Cell4 x = d_load(rp + rl - 1);
+                int st = 0;
+#define OOB_RT_STEP(I)                                                                          \
+    {                                                                                           \
+        const int e = rl - 1 - st - (I);                                                        \
+        const Cell4 nx = d_load(rp + max(e - 1, 0));                                            \
+        const double xl = __dadd_rn(x.C1, s3);                                                  \
+        _Pragma("unroll") for (int t = 0; t < TE; ++t)                                          \
+            split_eval2(x.T1, x.T3, x.TS, xl, (double)(3 * t), RT1[t], RT3[t], RTS[t], c4,      \
+                       RC1[t], best[((t - (I)) % TE + TE) % TE], widx[((t - (I)) % TE + TE) % TE], t, t == 0); \
+        c4 = __dadd_rn(c4, -4.0);                                                               \
+        const int sf = ((TE - 1 - (I)) % TE + TE) % TE;                                         \
+        const int E = e + e0 + TE - 1;                                                          \
+        acc_flush(acc, ob + E, qok && best[sf] < D_INF, best[sf],                               \
+                  kb + (uint32_t)(jl + E - e0 - widx[sf]));                                     \
+        best[sf] = D_INF;                                                                       \
+        x = nx;                                                                                 \
+    }
 #pragma unroll 1
-                for (int base = 0; base < rl; base += TE) {
+                for (; st + TE <= rl; st += TE) {
 #pragma unroll
-                    for (int i = 0; i < TE; ++i) {
-                        const int st = base + i;
-                        if (st < rl) {
-                            const int e = rl - 1 - st;
-                            const Cell4 x = d_load(rp + e);
-                            const double xl = __dadd_rn(x.C1, s3);
-#pragma unroll
-                            for (int t = 0; t < TE; ++t)
-                                split_eval(x.T1, x.T3, x.TS, xl, (double)(3 * t),
-                                           RT1[t], RT3[t], RTS[t], c4, RC1[t],
-                                           best[((t - i) % TE + TE) % TE], widx[((t - i) % TE + TE) % TE], t);
-                            c4 = __dadd_rn(c4, -4.0);
-                            const int sf = ((TE - 1 - i) % TE + TE) % TE;
-                            if (qok && best[sf] < D_INF) {
-                                const int E = e + e0 + TE - 1;
-                                const int s = jl + E - e0 - widx[sf];
-                                const uint32_t key = ((uint32_t)l1 << 20) | ((uint32_t)jl << 10) | (uint32_t)s;
-                                acc_merge(acc, ob + E, best[sf], key);
-                            }
-                            best[sf] = D_INF;
-                        }
-                    }
+                    for (int i = 0; i < TE; ++i) OOB_RT_STEP(i)
                 }
+#pragma unroll
+                for (int i = 0; i < TE - 1; ++i)
+                    if (st + i < rl) OOB_RT_STEP(i)
+#undef OOB_RT_STEP
                 // after the last step (i = rl-1, e = 0) slot sg holds t = (sg + rl - 1) % TE
 #pragma unroll
                 for (int sg = 0; sg < TE; ++sg) {
-                    if (qok && best[sg] < D_INF) {
-                        const int t = (sg + rl - 1) % TE;
-                        const int E = e0 + t;
-                        const int s = jl + E - e0 - widx[sg];
-                        const uint32_t key = ((uint32_t)l1 << 20) | ((uint32_t)jl << 10) | (uint32_t)s;
-                        acc_merge(acc, ob + E, best[sg], key);
-                    }
+                    const int t = (sg + rl - 1) % TE;
+                    const int E = e0 + t;
+                    acc_flush(acc, ob + E, qok && best[sg] < D_INF, best[sg],
+                              kb + (uint32_t)(jl + E - e0 - widx[sg]));
                 }
             }
         }
