@@ -179,19 +179,20 @@ namespace {
 
 // k_wave_w launch configurations: (TE cells per lane tile, threads per CTA)
 struct WCfg { int te, nt; };
-constexpr WCfg WCFGS[] = {{4, 128}, {4, 256}, {8, 128}, {8, 256}};
-constexpr int NWCFG = 4;
+constexpr WCfg WCFGS[] = {{4, NTW}, {5, NTW}};
+constexpr int NWCFG = 2;
 
 struct WaveHost {
     int cfg = 0;                   // index into WCFGS
-    int nitems = 0, ns_max = 0, nout = 0;
-    size_t items_off = 0, ents_off = 0, cb_off = 0;   // byte offsets in the blob's items region
-    std::vector<int32_t> items;    // 4 ints per item: (entry_lo, entry_hi, 0, 0)
+    int nents = 0, nunits = 0, nout = 0, cpr = 1;
+    size_t ents_off = 0, upre_off = 0, cb_off = 0;   // byte offsets in the blob's items region
     std::vector<int32_t> ents;     // 4 ints per entry: (l1, nblocks, nchunks, chunk_off)
+    std::vector<int32_t> upre;     // unit prefix per entry [nents + 1]
     std::vector<int32_t> cb;       // chunk row boundaries
     size_t smem = 0;
-    int64_t small_warps = 0;
-    double cost = 0.0;
+    size_t ctr_off = 0;            // first unit counter of this wave (ints)
+    int nsmall = 0;                // cells inside one node with S' >= 2 per range
+    double cost = 0.0;             // modelled issue cycles of the wave (all ranges, profiles)
 };
 
 int Q_of(const Geometry &g, int l) { return (l == g.L) ? g.n_hi : std::max(1, g.n_hi - 1); }
@@ -216,13 +217,16 @@ struct oob_dp_plan {
     std::vector<unsigned char> geom_blob;   // host image of the geometry region
     size_t off_cells = 0, off_base = 0, off_off = 0, off_tiles = 0, off_tile_off = 0, off_tile_cnt = 0,
            off_items = 0;
-    size_t off_CELL = 0, off_ARG = 0, off_STK = 0, off_PB = 0, off_PK = 0;
+    size_t off_CELL = 0, off_ARG = 0, off_STK = 0, off_GACC = 0, off_CTR = 0;
+    int64_t gacc_n = 0;
+    size_t ctr_n = 0;
     std::vector<int32_t> tiles;          // all TE's tables concatenated
-    TileTab tab[2];                      // TE = 4, TE = 8
+    TileTab tab[2];                      // TE = 4, TE = 5
     std::vector<WaveHost> waves;         // [L+1]
     size_t max_smem = 0;
     int64_t launches = 0;
     void *uploaded_to = nullptr;
+    void *gacc_ready = nullptr;
     int timing = 0;
     std::vector<cudaEvent_t> ev;
     int ev_used = 0;
@@ -272,89 +276,70 @@ static double k_cost(const oob_dp_plan *pl, int TE, int l, int l1, int it_lo, in
     return units * (steps * (TE * 20.0 + 24.0) + 400.0);
 }
 
-// Work items of wavefront l, balanced by the cost model: an item is a list of entries
-// (l1, small-side rows) — a k range, or one k's row range when that k alone exceeds 1.5x
-// the per-item target.  Each entry's rows are cut into chunks of ~CH steps; a warp unit
-// is (entry, chunk, 32-tile block).
-static void build_items(oob_dp_plan *pl, int l, int ci, int target_ctas, WaveHost &wh) {
+// Unit queue of wavefront l (identical for every range and profile): one entry per layer
+// split k with work, balanced splits (l1 near l/2) first so the accumulator sees good
+// totals early; an entry's small-side rows are cut into chunks of ~CH steps; a warp unit is
+// (entry, chunk, block of 32 big-side tiles).  `slots` = resident CTAs of the GPU: ranges
+// get several CTAs (sharing the range's queue) when there are fewer ranges than slots.
+static void build_wave(oob_dp_plan *pl, int l, int ci, int slots, WaveHost &wh) {
     const Geometry &g = pl->g;
     const int TE = WCFGS[ci].te;
     const int nr = g.L - l + 1;
     const int CH = 96;
-    std::vector<double> cost(l, 0.0);
+    std::vector<int> order;
+    for (int l1 = 1; l1 < l; ++l1) order.push_back(l1);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return std::abs(2 * a - l) < std::abs(2 * b - l); });
+    wh.ents.clear();
+    wh.upre.assign(1, 0);
+    wh.cb.clear();
     double total = 0.0;
-    for (int l1 = 1; l1 < l; ++l1) {
-        cost[l1] = k_cost(pl, TE, l, l1, 1, 1 << 20);
-        total += cost[l1];
-    }
-    const int per_range = std::max(1, (target_ctas + pl->P * nr - 1) / (pl->P * nr));
-    const double target = total / per_range;
-    // (l1, row_lo, row_hi) triples grouped into items
-    std::vector<std::vector<std::array<int, 3>>> items;
-    std::vector<std::array<int, 3>> cur;
-    double curc = 0.0;
-    auto small_rows = [&](int l1) {
+    for (int l1 : order) {
         const int l2 = l - l1;
         const bool lt = wcells_h(g, l1) >= wcells_h(g, l2);
-        const int ls = lt ? l2 : l1;
-        return std::make_pair(ls, std::min(Q_of(g, ls), ls));
-    };
-    for (int l1 = 1; l1 < l; ++l1) {
-        const int JS = small_rows(l1).second;
-        if (cost[l1] > 1.5 * target && per_range > 1) {
-            if (!cur.empty()) { items.push_back(cur); cur.clear(); curc = 0.0; }
-            const int pieces = std::max(1, (int)std::lround(cost[l1] / target));
-            const double piece = cost[l1] / pieces;
-            int r0 = 1;
-            for (int r = 1; r <= JS; ++r) {
-                if (k_cost(pl, TE, l, l1, r0, r + 1) >= piece && r < JS) {
-                    items.push_back({{l1, r0, r + 1}});
-                    r0 = r + 1;
-                }
-            }
-            items.push_back({{l1, r0, JS + 1}});
-            continue;
+        const int ls = lt ? l2 : l1, lb = lt ? l1 : l2;
+        const int JS = std::min(Q_of(g, ls), ls);
+        const int nblocks = (pl->tab[te_index(TE)].cnt[lb] + 31) / 32;
+        const int coff = (int)wh.cb.size();
+        int nchunks = 0, acc = 0, last = -1;
+        for (int r = 1; r <= JS; ++r) {
+            const int c = acc / CH;
+            if (c != last) { wh.cb.push_back(r); ++nchunks; last = c; }
+            acc += wlen_h(g, ls, r);
         }
-        cur.push_back({l1, 1, JS + 1});
-        curc += cost[l1];
-        if (curc >= target && per_range > 1) { items.push_back(cur); cur.clear(); curc = 0.0; }
-    }
-    if (!cur.empty()) items.push_back(cur);
-    wh.items.clear();
-    wh.ents.clear();
-    wh.cb.clear();
-    for (auto &itv : items) {
-        const int elo = (int)(wh.ents.size() / 4);
-        for (auto &tr : itv) {
-            const int l1 = tr[0];
-            const int l2 = l - l1;
-            const bool lt = wcells_h(g, l1) >= wcells_h(g, l2);
-            const int ls = lt ? l2 : l1, lb = lt ? l1 : l2;
-            const int nblocks = (pl->tab[te_index(TE)].cnt[lb] + 31) / 32;
-            const int coff = (int)wh.cb.size();
-            // chunk c holds the rows whose preceding-step count floor-divides to c
-            int nchunks = 0, acc = 0, last = -1;
-            for (int r = tr[1]; r < tr[2]; ++r) {
-                const int c = acc / CH;
-                if (c != last) { wh.cb.push_back(r); ++nchunks; last = c; }
-                acc += wlen_h(g, ls, r);
-            }
-            wh.cb.push_back(tr[2]);
-            if (nchunks == 0 || nblocks == 0) { wh.cb.resize(coff); continue; }
-            wh.ents.insert(wh.ents.end(), {l1, nblocks, nchunks, coff});
-        }
-        const int ehi = (int)(wh.ents.size() / 4);
-        if (ehi > elo) wh.items.insert(wh.items.end(), {elo, ehi, 0, 0});
+        wh.cb.push_back(JS + 1);
+        if (nchunks == 0 || nblocks == 0) { wh.cb.resize(coff); continue; }
+        wh.ents.insert(wh.ents.end(), {l1, nblocks, nchunks, coff});
+        wh.upre.push_back(wh.upre.back() + nblocks * nchunks);
+        total += k_cost(pl, TE, l, l1, 1, 1 << 20);
     }
     wh.cfg = ci;
-    wh.nitems = (int)wh.items.size() / 4;
-    wh.ns_max = 0;
+    wh.nents = (int)wh.ents.size() / 4;
+    wh.nunits = wh.upre.back();
     wh.nout = wcells_h(g, l);
-    wh.smem = align_up((size_t)wh.nout * 16, 16) + 2 * (size_t)(g.L + 2) * 4 + 16;
-    wh.cost = total * pl->P * nr;
+    const int ranges = pl->P * nr;
+    wh.cpr = std::max(1, std::min(wh.nunits / 8, slots / std::max(1, ranges)));
+    // acc[nout + dummy] (16 B) + filter (4 B) + base[L+2] (8 B) + cells[L+1] + outOff[L+2]
+    // + upre[L+4] + ents[nents] (16 B)
+    const size_t nent = (size_t)(wh.nout + g.L + 2 * TE + 2);
+    const size_t before_ring = nent * 16 + (nent + 3) / 4 * 16 + (size_t)wh.nents * 16 + (size_t)(g.L + 2) * 8 +
+                               (size_t)(g.L + 1) * 4 + (size_t)(g.L + 2) * 4 + (size_t)(g.L + 4) * 4;
+    wh.smem = before_ring + 16;
+    wh.cost = total * ranges;
+}
+
+// cells inside one node with S' >= 2 per range of length l (I(r), r < M, and W(1))
+static int small_cells(const Geometry &g, int l) {
     int per = 0;
     for (int a = 0; a < std::min(g.A, g.M); ++a) per += std::max(0, std::min(l, g.gpus(a)) - 1);
-    wh.small_warps = (int64_t)pl->P * nr * per;
+    return per;
+}
+
+// threads per small cell: ~4 (k, m) pairs per thread, 32..256
+static int small_tpc(const Geometry &g, int l) {
+    const int pairs = (l - 1) * std::max(1, g.M - 1);
+    int t = 32;
+    while (t < 256 && t * 4 < pairs) t *= 2;
+    return t;
 }
 
 extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int32_t n_hi,
@@ -370,49 +355,51 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     pl->kernel = (kv && std::string(kv) == "v1") ? 1 : 2;
     if (const char *fc = std::getenv("OOB_DP_WCFG")) pl->force_cfg = std::atoi(fc);
     build_tiles(pl, 4);
-    build_tiles(pl, 8);
+    build_tiles(pl, 5);
     pl->waves.assign(L + 1, WaveHost());
-    size_t items_total = 0, part_max = 0;
+    size_t items_total = 0, gacc_max = 0, ctr_total = 0;
     for (int l = 2; l <= L; ++l) {
         WaveHost best;
         double best_t = 1e300;
         for (int ci = 0; ci < NWCFG; ++ci) {
             if (pl->force_cfg >= 0 && ci != pl->force_cfg) continue;
             WaveHost wh;
-            build_items(pl, l, ci, 4 * 148, wh);
-            // resident CTAs per SM: 16 warps by registers (launch bounds 256 x 2), smem
-            const int by_warps = (WCFGS[ci].te <= 4 ? 16 : 8) / (WCFGS[ci].nt / 32);
+            build_wave(pl, l, ci, 2 * 148, wh);
+            // resident CTAs per SM: launch bounds 256 x 2, smem
             const int by_smem = std::max<int>(1, (int)((227 * 1024) / std::max<size_t>(wh.smem, 1)));
-            const int per_sm = std::max(1, std::min(by_warps, by_smem));
-            const double warps_per_smsp = per_sm * (WCFGS[ci].nt / 32) / 4.0;
-            // issue efficiency saturates at ~4 resident warps per scheduler
-            const double eff = std::min(1.0, warps_per_smsp / 4.0);
+            const int per_sm = std::max(1, std::min(2, by_smem));
+            const double warps_per_smsp = per_sm * (NTW / 32) / 4.0;
+            // issue efficiency saturates at ~4 resident warps per scheduler; TE = 5 (larger
+            // code, measured slower on B200) is kept as a forced option (OOB_DP_WCFG=1)
+            const double eff = std::min(1.0, warps_per_smsp / 4.0) * (WCFGS[ci].te == 5 ? 0.7 : 1.0);
             const double t = wh.cost / (4.0 * 148.0 * eff);
             if (t < best_t) { best_t = t; best = wh; }
         }
         pl->waves[l] = best;
         WaveHost &wh = pl->waves[l];
-        wh.items_off = items_total;
-        items_total += align_up(wh.items.size() * sizeof(int32_t), 16);
         wh.ents_off = items_total;
         items_total += align_up(wh.ents.size() * sizeof(int32_t), 16);
+        wh.upre_off = items_total;
+        items_total += align_up(wh.upre.size() * sizeof(int32_t), 16);
         wh.cb_off = items_total;
         items_total += align_up(wh.cb.size() * sizeof(int32_t), 16);
-        part_max = std::max(part_max, (size_t)num_profiles * (L - l + 1) * wh.nitems * wh.nout);
+        gacc_max = std::max(gacc_max, (size_t)num_profiles * (L - l + 1) * wh.nout);
+        wh.ctr_off = ctr_total;
+        ctr_total += (size_t)num_profiles * (L - l + 1);
         pl->max_smem = std::max(pl->max_smem, wh.smem);
     }
+    pl->ctr_n = ctr_total;
     if (pl->max_smem > 227 * 1024) pl->kernel = 1;
     if (std::getenv("OOB_DP_DEBUG")) {
         for (int l = 2; l <= L; ++l) {
             const WaveHost &wh = pl->waves[l];
-            std::fprintf(stderr, "l=%d cfg=%d (TE=%d NT=%d) items=%d ctas=%lld smem=%zu cost=%.3g\n", l, wh.cfg,
-                         WCFGS[wh.cfg].te, WCFGS[wh.cfg].nt, wh.nitems,
-                         (long long)wh.nitems * (L - l + 1) * num_profiles, wh.smem, wh.cost);
+            std::fprintf(stderr, "l=%d cfg=%d (TE=%d) ents=%d units=%d cpr=%d ctas=%lld smem=%zu cost=%.3g\n", l,
+                         wh.cfg, WCFGS[wh.cfg].te, wh.nents, wh.nunits, wh.cpr,
+                         (long long)wh.cpr * (L - l + 1) * num_profiles, wh.smem, wh.cost);
         }
     }
-    pl->launches = 1 + 1 + (pl->kernel == 1 ? (L - 1) : 0);
-    if (pl->kernel == 2)
-        for (int l = 2; l <= L; ++l) pl->launches += 2 + (pl->waves[l].small_warps > 0 ? 1 : 0);
+    // k_base + k_extract; v1: one kernel per wave; v6: k_fin(1) + (k_wave_w, k_fin) per wave
+    pl->launches = 2 + (pl->kernel == 1 ? (L - 1) : 1 + 2 * (L - 1));
 
     size_t o = 0;
     pl->off_cells = o; o = align_up(o + sizeof(int32_t) * (L + 1), 256);
@@ -424,13 +411,12 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     pl->off_items = o;    o = align_up(o + items_total, 256);
     pl->geom_bytes = o;
     const size_t n = (size_t)g.total_cells * num_profiles;
-    pl->off_CELL = o; o = align_up(o + 32 * n, 256);
+    pl->off_CELL = o; o = align_up(o + 32 * (n + 16), 256);   // + padding: row streams read ahead
     pl->off_ARG = o; o = align_up(o + 4 * n, 256);
     pl->off_STK = o; o = align_up(o + 8 * (size_t)num_profiles * (n_hi - n_lo + 1) * (L + 1), 256);
-    if (pl->kernel == 2) {
-        pl->off_PB = o; o = align_up(o + 8 * part_max, 256);
-        pl->off_PK = o; o = align_up(o + 4 * part_max, 256);
-    }
+    pl->gacc_n = (int64_t)gacc_max;
+    pl->off_GACC = o; o = align_up(o + 16 * gacc_max, 256);
+    pl->off_CTR = o; o = align_up(o + 4 * pl->ctr_n + 4, 256);
     pl->ws_bytes = o;
     pl->tpl_bytes = packed_template_bytes(L);
     pl->geom_blob.assign(pl->geom_bytes, 0);
@@ -445,10 +431,10 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     }
     for (int l = 2; l <= L; ++l) {
         const WaveHost &wh = pl->waves[l];
-        if (!wh.items.empty())
-            std::memcpy(b + pl->off_items + wh.items_off, wh.items.data(), wh.items.size() * sizeof(int32_t));
         if (!wh.ents.empty())
             std::memcpy(b + pl->off_items + wh.ents_off, wh.ents.data(), wh.ents.size() * sizeof(int32_t));
+        if (!wh.upre.empty())
+            std::memcpy(b + pl->off_items + wh.upre_off, wh.upre.data(), wh.upre.size() * sizeof(int32_t));
         if (!wh.cb.empty())
             std::memcpy(b + pl->off_items + wh.cb_off, wh.cb.data(), wh.cb.size() * sizeof(int32_t));
     }
@@ -509,6 +495,28 @@ extern "C" oob_status oob_dp_kernel_time(oob_dp_plan *pl, double *ms_out, int64_
     return OOB_OK;
 }
 
+// k_fin: W winners of wave lw (lw >= 2, else none) + small cells of wave ls (0: none).
+static cudaError_t launch_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglong2 *gacc, int lw, int ls,
+                              cudaStream_t stream) {
+    const Geometry &G = pl->g;
+    FinArgs f;
+    f.lw = lw;
+    f.nranges_w = lw ? G.L - lw + 1 : 0;
+    f.nout_w = lw ? pl->waves[lw].nout : 0;
+    const int64_t nw = (int64_t)pl->P * f.nranges_w * f.nout_w;
+    f.nbw = (int)((nw + 255) / 256);
+    f.GACC = gacc;
+    f.ls = ls;
+    f.nsmall = ls ? small_cells(G, ls) : 0;
+    f.tpc = ls ? small_tpc(G, ls) : 32;
+    const int64_t ns = ls ? (int64_t)pl->P * (G.L - ls + 1) * f.nsmall : 0;
+    const int64_t nbs = (ns + (256 / f.tpc) - 1) / (256 / f.tpc);
+    const int64_t blocks = f.nbw + nbs;
+    if (blocks == 0) return cudaSuccess;
+    k_fin<<<(unsigned)blocks, 256, 0, stream>>>(dg, f);
+    return cudaGetLastError();
+}
+
 extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const double *d_bwd,
                                  void *d_ws, size_t ws_bytes, void *d_packed, void *stream_) {
     if (!pl || !d_fwd || !d_bwd || !d_ws || !d_packed)
@@ -526,9 +534,9 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
         pl->uploaded_to = d_ws;
         if (pl->kernel == 2) {
             const int sm = (int)std::max<size_t>(pl->max_smem, 48 * 1024);
-            e = cudaFuncSetAttribute(k_wave_w<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+            e = cudaFuncSetAttribute(k_wave_w<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
             if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(k_wave_w<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+                e = cudaFuncSetAttribute(k_wave_w<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
             if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(k_wave_w)");
         }
     }
@@ -558,6 +566,19 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
             pl->ev.push_back(ev);
         }
     }
+    ulonglong2 *gacc = (ulonglong2 *)(ws + pl->off_GACC);
+    if (pl->kernel == 2) {
+        if (pl->gacc_ready != d_ws && pl->gacc_n > 0) {   // finalize resets what it reads
+            k_gacc_init<<<(unsigned)((pl->gacc_n + 255) / 256), 256, 0, stream>>>(gacc, pl->gacc_n);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_fail(e, "k_gacc_init launch");
+            pl->gacc_ready = d_ws;
+        }
+        e = cudaMemsetAsync(ws + pl->off_CTR, 0, 4 * pl->ctr_n + 4, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "unit counter reset");
+        if (G.L >= 2 && (e = launch_fin(pl, dg, gacc, 0, 2, stream)) != cudaSuccess)
+            return cuda_fail(e, "k_fin launch");
+    }
     for (int l = 2; l <= G.L; ++l) {
         if (pl->kernel == 1) {
             int64_t n = (int64_t)(G.L - l + 1) * G.cells[l] * pl->P;
@@ -570,38 +591,33 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
             continue;
         }
         const WaveHost &wh = pl->waves[l];
-        if (wh.small_warps > 0) {
-            const int64_t threads = wh.small_warps * 32;
-            k_wave_small<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(dg, l);
-            e = cudaGetLastError();
-            if (e != cudaSuccess) return cuda_fail(e, "k_wave_small launch");
-        }
         WaveW w;
         w.l = l;
         w.nranges = G.L - l + 1;
-        w.nitems = wh.nitems;
-        w.items = (const int4 *)(ws + pl->off_items + wh.items_off);
+        w.cpr = wh.cpr;
+        w.nents = wh.nents;
         w.ents = (const int4 *)(ws + pl->off_items + wh.ents_off);
+        w.upre = (const int32_t *)(ws + pl->off_items + wh.upre_off);
         w.cb = (const int32_t *)(ws + pl->off_items + wh.cb_off);
+        w.ctr = (int *)(ws + pl->off_CTR) + wh.ctr_off;
         w.nout = wh.nout;
-        w.PB = (double *)(ws + pl->off_PB);
-        w.PK = (uint32_t *)(ws + pl->off_PK);
+        w.GACC = gacc;
         w.tile_off = (const int32_t *)(ws + pl->off_tile_off) + (size_t)(G.L + 1) * te_index(WCFGS[wh.cfg].te);
         w.tile_cnt = (const int32_t *)(ws + pl->off_tile_cnt) + (size_t)(G.L + 1) * te_index(WCFGS[wh.cfg].te);
         w.tiles = (const int32_t *)(ws + pl->off_tiles);
-        const int64_t ctas = (int64_t)pl->P * w.nranges * w.nitems;
+        const int64_t ctas = wh.nents > 0 ? (int64_t)pl->P * w.nranges * w.cpr : 0;
         if (pl->timing) cudaEventRecord(pl->ev[pl->ev_used], stream);
-        if (WCFGS[wh.cfg].te == 4)
-            k_wave_w<4><<<(unsigned)ctas, WCFGS[wh.cfg].nt, wh.smem, stream>>>(dg, w);
-        else
-            k_wave_w<8><<<(unsigned)ctas, WCFGS[wh.cfg].nt, wh.smem, stream>>>(dg, w);
+        if (ctas > 0) {
+            if (WCFGS[wh.cfg].te == 4)
+                k_wave_w<4><<<(unsigned)ctas, NTW, wh.smem, stream>>>(dg, w);
+            else
+                k_wave_w<5><<<(unsigned)ctas, NTW, wh.smem, stream>>>(dg, w);
+        }
         if (pl->timing) { cudaEventRecord(pl->ev[pl->ev_used + 1], stream); pl->ev_used += 2; }
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "k_wave_w launch");
-        const int64_t nf = (int64_t)pl->P * w.nranges * w.nout;
-        k_wave_w_finalize<<<(unsigned)((nf + 255) / 256), 256, 0, stream>>>(dg, w);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return cuda_fail(e, "k_wave_w_finalize launch");
+        if ((e = launch_fin(pl, dg, gacc, l, l < G.L ? l + 1 : 0, stream)) != cudaSuccess)
+            return cuda_fail(e, "k_fin launch");
     }
     {
         int n = (G.n_hi - G.n_lo + 1) * pl->P;

@@ -4,43 +4,54 @@
 // k (l1 = k-u, l2 = v-k), W(q) cells combine left children W(j) of (u, k) with right
 // children W(q-j) of (k, v) (PAPER Eq.1-3, two-level device split: reading R2).  In
 // (nodes, stages) coordinates every pair (left cell, right cell) is a valid split of
-// exactly one parent cell (q = j + j', S' = s + S_R): for each row pair (j, j') the work
-// is a dense a_j x b_j' rectangle of splits.  Mapping (one CTA per (profile, range, item)):
+// exactly one parent cell (q = j + j', S' = s + S_R): for each row pair (j, j') the work is
+// a dense a_j x b_j' rectangle of splits.  Mapping (one CTA per (item, profile, range);
+// items are lists of layer splits k, ordered by decreasing cost so the block scheduler
+// runs them longest-first):
 //   * the child slab with more W cells ("big side") is register-tiled: a lane holds TE
 //     consecutive cells of one row; 32 consecutive tiles (rows may straddle lanes) and one
 //     chunk of small-side rows form a warp work unit; warps pull units from a counter;
 //   * a unit walks its rows of the other slab ("small side") cell by cell; all lanes read
-//     the same cell (L1 broadcast, 2 x 16-byte loads);
-//   * each lane keeps the TE outputs its tile currently touches in a register ring (the
-//     outputs slide by one cell per step); the output whose last contribution from this
-//     lane has arrived is merged into the CTA's shared-memory accumulator, which holds per
-//     parent cell the lexicographic minimum of (total, canonical split key), updated with
-//     a 128-bit compare-and-swap — exact under any interleaving.
-// Tie semantics: the oracle keeps the first strictly-smaller total in (k, m, s) order.
-// Inside a ring slot the pairs of one (k, j) arrive in decreasing s, so "<=" keeps the
-// smallest s; every merge compares (total, key) with key = l1<<20 | j<<10 | s, which is
-// monotone in (k, m, s): the result is exactly the oracle's argmin.
+//     the same cell (L1 broadcast, 2 x 16-byte loads) and evaluate TE splits;
+//   * the outputs a lane touches slide by one cell per step: a ring of TE slots keeps, per
+//     in-flight output, only the minimum HIGH WORD of its totals (one 32-bit min per
+//     split).  When an output's last contribution from this lane has arrived, the slot is
+//     compared with the high word of the CTA's shared-memory accumulator entry; only if it
+//     is <= (it can win or tie) does the lane recompute that output's TE splits exactly
+//     (the same binary64 operations, hence the same bits) and merge the lexicographic
+//     minimum of (total, split key) with a 128-bit compare-and-swap — exact under any
+//     interleaving.  Since the high word of a positive binary64 is monotone in its value,
+//     the filter never drops a winner.
+//   * at the end of the task the CTA's accumulator is merged into the global accumulator
+//     of the range (128-bit global CAS); k_fin recomputes each winner's cell.
+// Tie semantics: the oracle keeps the first strictly smaller total in (k, m, s) order; the
+// key l1<<20 | j<<10 | s is monotone in (k, m, s), so the lexicographic minimum of
+// (total, key) is exactly the oracle's argmin.
 //
-// k_wave_small — cells inside one node (I(r), W(1)); k_wave_w_finalize — merge of the
-// items' partial argmins and the winner's recomputation.
+// k_fin — per wavefront: the winners of the W(q >= 2) cells of wave l, and every cell
+// inside one node (I(r), W(1)) of wave l+1 (those depend only on shorter cells inside a
+// node), a group of threads per cell with a lexicographic argmin reduction.
 #pragma once
 
 #include "oob_dp_common.cuh"
 
 namespace oob {
 
-constexpr int NT_MAX = 256;               // max threads per CTA of k_wave_w
+constexpr int NTW = 256;                                          // threads per k_wave_w CTA
+constexpr unsigned long long ACC_EMPTY = 0x7FEFFFFFFFFFFFFFull;   // DBL_MAX: "no split yet"
+constexpr double D_INF = __builtin_huge_val();
 
 struct WaveW {
     int l;                 // wavefront length
     int nranges;           // L - l + 1
-    int nitems;            // work items per range
-    const int4 *items;     // per item: (entry_lo, entry_hi, -, -)
-    const int4 *ents;      // per (item, k): (l1, nblocks, nchunks, chunk_off)
+    int cpr;               // CTAs per (profile, range); they share the range's unit queue
+    int nents;             // layer splits k with work (balanced splits first)
+    const int4 *ents;      // per entry: (l1, nblocks, nchunks, chunk_off)
+    const int32_t *upre;   // [nents + 1] unit prefix: entry e owns units [upre[e], upre[e+1])
     const int32_t *cb;     // chunk row boundaries: rows [cb[off+c], cb[off+c+1])
+    int *ctr;              // [P][nranges] unit counters (zeroed before the launch)
     int nout;              // W-part cells of a slab of length l (W(1)..W(Q_l))
-    double *PB;            // partial best  [P][nranges][nitems][nout]
-    uint32_t *PK;          // partial key
+    ulonglong2 *GACC;      // global accumulator [P][nranges][nout]: {total bits, key}
     const int32_t *tile_off;   // [L+1] offset of the flat tile list of a big side of length lb
     const int32_t *tile_cnt;   // [L+1] number of tiles
     const int32_t *tiles;      // packed (row << 16 | e0)
@@ -59,52 +70,26 @@ __device__ __forceinline__ int d_wlen(const DevGeom &g, int l, int q) {
     return hi >= q ? hi - q + 1 : 0;
 }
 
-// One split, operands in left / right roles.  The coefficient is cla + clb if the left
-// half holds the slowest stage (3S'-1+k*_L) and cra + crb otherwise (3S'-1+s+k*_R), exact
-// integers:
+// One split with operands in left / right roles (DESIGN.md §2 arithmetic contract):
 //   T1 = L.T1 + R.T1; left = L.t* >= R.t*; T3 = left ? L.T3 + R.T1 : R.T3;
-//   T2 = coef * t*; total = (T1 + T2) + T3; keep if total <= best.
-// skip_r / skip_l: the second operand of that coefficient is +0 (t == 0), use the first.
-__device__ __forceinline__ void split_eval(double LT1, double LT3, double LTS, double cla, double clb,
-                                           double RT1, double RT3, double RTS, double cra, double crb,
-                                           double &best, int &widx, int code, bool skip_r = false) {
+//   T2 = c * t* with c = left ? cL : cR (exact small integers: 3S'-1+k*); total = (T1 + T2) + T3.
+// cL / cR have zero low words (integers < 2^21), so the coefficient select is one 32-bit
+// select of the high words.
+__device__ __forceinline__ double split_total(double LT1, double LT3, double LTS, double cL,
+                                              double RT1, double RT3, double RTS, double cR) {
     const double T1 = __dadd_rn(LT1, RT1);
     const double T3a = __dadd_rn(LT3, RT1);
     const bool left = LTS >= RTS;
-    const double cL = __dadd_rn(cla, clb);
-    const double cR = skip_r ? cra : __dadd_rn(cra, crb);
-    const double TS = left ? LTS : RTS;
+    const double ts = left ? LTS : RTS;
     const double T3 = left ? T3a : RT3;
-    const double c = left ? cL : cR;
-    const double T2 = __dmul_rn(c, TS);
-    const double tot = __dadd_rn(__dadd_rn(T1, T2), T3);
-    const bool upd = tot <= best;
-    best = upd ? tot : best;
-    widx = upd ? code : widx;
+    const double c = __hiloint2double(left ? __double2hiint(cL) : __double2hiint(cR), 0);
+    return __dadd_rn(__dadd_rn(T1, __dmul_rn(c, ts)), T3);
 }
 
-__device__ __forceinline__ void split_eval2(double LT1, double LT3, double LTS, double cla, double clb,
-                                            double RT1, double RT3, double RTS, double cra, double crb,
-                                            double &best, int &widx, int code, bool skip_l) {
-    const double T1 = __dadd_rn(LT1, RT1);
-    const double T3a = __dadd_rn(LT3, RT1);
-    const bool left = LTS >= RTS;
-    const double cL = skip_l ? cla : __dadd_rn(cla, clb);
-    const double cR = __dadd_rn(cra, crb);
-    const double TS = left ? LTS : RTS;
-    const double T3 = left ? T3a : RT3;
-    const double c = left ? cL : cR;
-    const double T2 = __dmul_rn(c, TS);
-    const double tot = __dadd_rn(__dadd_rn(T1, T2), T3);
-    const bool upd = tot <= best;
-    best = upd ? tot : best;
-    widx = upd ? code : widx;
-}
-
-// 128-bit shared-memory CAS (sm_90+ atom.shared.cas.b128)
-__device__ __forceinline__ void cas128(unsigned addr, unsigned long long &olo, unsigned long long &ohi,
-                                       unsigned long long clo, unsigned long long chi,
-                                       unsigned long long nlo, unsigned long long nhi) {
+// 128-bit compare-and-swap (sm_90+ atom.cas.b128), shared or global (generic address).
+__device__ __forceinline__ void cas128_shared(unsigned addr, unsigned long long &olo, unsigned long long &ohi,
+                                              unsigned long long clo, unsigned long long chi,
+                                              unsigned long long nlo, unsigned long long nhi) {
     asm volatile("{\n\t.reg .b128 d, c, v;\n\t"
                  "mov.b128 c, {%2, %3};\n\t"
                  "mov.b128 v, {%4, %5};\n\t"
@@ -114,88 +99,223 @@ __device__ __forceinline__ void cas128(unsigned addr, unsigned long long &olo, u
                  : "l"(clo), "l"(chi), "l"(nlo), "l"(nhi), "r"(addr)
                  : "memory");
 }
+__device__ __forceinline__ void cas128_global(ulonglong2 *p, unsigned long long &olo, unsigned long long &ohi,
+                                              unsigned long long clo, unsigned long long chi,
+                                              unsigned long long nlo, unsigned long long nhi) {
+    asm volatile("{\n\t.reg .b128 d, c, v;\n\t"
+                 "mov.b128 c, {%2, %3};\n\t"
+                 "mov.b128 v, {%4, %5};\n\t"
+                 "atom.global.cas.b128 d, [%6], c, v;\n\t"
+                 "mov.b128 {%0, %1}, d;\n\t}"
+                 : "=l"(olo), "=l"(ohi)
+                 : "l"(clo), "l"(chi), "l"(nlo), "l"(nhi), "l"(p)
+                 : "memory");
+}
 
-// acc entry = {double total bits, key}: lexicographic-min update (exact under races).
-// The slow path (a CAS loop) is out of line: most flushes lose the comparison.
-__device__ __noinline__ void acc_merge_slow(unsigned addr, unsigned long long cx, unsigned long long cy,
-                                            double b, uint32_t key) {
-    const unsigned long long nb = (unsigned long long)__double_as_longlong(b);
-    for (;;) {
-        unsigned long long olo, ohi;
-        cas128(addr, olo, ohi, cx, cy, nb, (unsigned long long)key);
-        if (olo == cx && ohi == cy) return;
-        cx = olo;
-        cy = ohi;
-        const double A = __longlong_as_double((long long)cx);
-        const uint32_t K = (uint32_t)cy;
-        if (!(b < A || (b == A && key < K))) return;
+__device__ __forceinline__ bool lex_less(unsigned long long b, uint32_t key, unsigned long long A, uint32_t K) {
+    return b < A || (b == A && key < K);
+}
+
+// Lexicographic-min merge of (total bits b, key) into the shared accumulator entry at addr.
+__device__ __forceinline__ void acc_merge_shared(unsigned addr, unsigned long long b, uint32_t key) {
+    unsigned long long cx, cy;
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(cx), "=l"(cy) : "r"(addr) : "memory");
+    while (lex_less(b, key, cx, (uint32_t)cy)) {
+        unsigned long long ox, oy;
+        cas128_shared(addr, ox, oy, cx, cy, b, (unsigned long long)key);
+        if (ox == cx && oy == cy) return;
+        cx = ox;
+        cy = oy;
     }
 }
 
-// flush one ring slot into the accumulator entry `idx` if `ok` (valid output, finite)
-__device__ __forceinline__ void acc_flush(const ulonglong2 *acc, int idx, bool ok, double b, uint32_t key) {
-    const unsigned addr = (unsigned)__cvta_generic_to_shared(acc + (ok ? idx : 0));
-    unsigned long long cx, cy;   // one 16-byte shared load (single transaction)
-    asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(cx), "=l"(cy) : "r"(addr) : "memory");
-    const double A = __longlong_as_double((long long)cx);
-    const uint32_t K = (uint32_t)cy;
-    if (ok && (b < A || (b == A && key < K))) acc_merge_slow(addr, cx, cy, b, key);
+// ---------------------------------------------------------------- closed-form slab geometry
+// W rows of a slab of length l: row q (1 <= q <= min(Q_l, l)) holds S' = q..min(l, Mq).
+__device__ __forceinline__ int c_wlen(int M, int l, int q) { return min(l, M * q) - q + 1; }
+// offset of row q inside the W part of the slab
+__device__ __forceinline__ int c_woff(int M, int l, int q) {
+    const int a = min(q - 1, l / M);            // rows q' < q with M q' <= l
+    const int r = q - 1 - a;
+    return (M - 1) * (a * (a + 1) / 2) + a + r * (l + 1) - ((q - 1) * q / 2 - a * (a + 1) / 2);
+}
+// cells of I(1..M-1) at the start of a slab of length l
+__device__ __forceinline__ int c_ipart(int M, int l) {
+    return l >= M - 1 ? (M - 1) * M / 2 : l * (l + 1) / 2 + (M - 1 - l) * l;
 }
 
-constexpr double D_INF = __builtin_huge_val();
+// Flush one completed ring slot (exact minimum `b` of its TE contributions, split key
+// `key`) into accumulator entry `idx`.  Fast path: compare the high word of `b` with the
+// entry's filter word (u32, at most the high word of the entry's total; TE odd makes the
+// lanes' filter words — TE entries apart — hit distinct banks).  Only if it can win or tie
+// does the lane read the 16-byte entry and run the lexicographic CAS loop (entries only
+// decrease, so a stale read is an upper bound and the loop stays exact), then lower the
+// filter.  Dummy entries have filter 0 (nothing passes); +inf / NaN never pass ACC_EMPTY.
+__device__ __forceinline__ void acc_flush(unsigned acc_s, unsigned filt_s, int idx, double b, uint32_t key) {
+    const unsigned bh = (unsigned)__double2hiint(b);
+    unsigned fh;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(fh) : "r"(filt_s + 4u * (unsigned)idx));
+    if (bh <= fh) {
+        const unsigned addr = acc_s + 16u * (unsigned)idx;
+        const unsigned long long bb = (unsigned long long)__double_as_longlong(b);
+        unsigned long long cx, cy;
+        asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(cx), "=l"(cy) : "r"(addr) : "memory");
+        while (lex_less(bb, key, cx, (uint32_t)cy)) {
+            unsigned long long ox, oy;
+            cas128_shared(addr, ox, oy, cx, cy, bb, (unsigned long long)key);
+            if (ox == cx && oy == cy) {
+                asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(filt_s + 4u * (unsigned)idx), "r"(bh) : "memory");
+                break;
+            }
+            cx = ox;
+            cy = oy;
+        }
+    }
+}
+
+// The small-side rows r_lo..r_hi-1 of one unit against this lane's register tile.
+//  LT = true : tile = LEFT child (row rowB = j, s_t = S0 + t), stream = RIGHT child (row
+//              rs = j', S_R = rs + e).  cL = C1_L[t] + 3 S_R, cR = C1_R(e) + 4 s_t.
+//              Ties: contributions to one output arrive with decreasing s -> "<=".
+//              key = l1<<20 | rowB<<10 | (S0 + t).
+//  LT = false: tile = RIGHT child (row rowB = j', S_R,t = S0 + t), stream = LEFT child (row
+//              rs = j, s = rs + e).  cL = C1_L(e) + 3 S_R,t, cR = C1_R[t] + 4 s.
+//              Ties: arrivals with increasing s -> "<".  key = l1<<20 | rs<<10 | (rs + e).
+// Output E' = e + t (index relative to the tile's first output) lives in ring slot
+// E' mod TE; its first contribution (t = TE-1) assigns the slot, t = 0 completes it (flush).
+// Each row runs in blocks of TE steps (static slots) plus a guarded tail.
+template <int TE, bool LT>
+__device__ __forceinline__ void run_rows(const Cell4 *__restrict__ sp, int M, int ls, int r_lo, int r_hi,
+                                         const double (&RT1)[TE], const double (&RT3)[TE], const double (&RTS)[TE],
+                                         const double (&RC1)[TE], int rowB, int e0, int l1, int L,
+                                         const int *outOff, int nout, unsigned acc_s, unsigned filt_s) {
+    const int S0 = rowB + e0;
+    const double xadd = (double)((LT ? 4 : 3) * S0);
+    const Cell4 *rp = sp + c_woff(M, ls, r_lo);          // rows of a slab are contiguous
+    for (int rs = r_lo; rs < r_hi; ++rs) {
+        const int rl = c_wlen(M, ls, rs);
+        const int q = rowB + rs;
+        const int ob = outOff[min(q, L + 1)];
+        const int idx0 = (ob == nout) ? nout : ob + e0;  // accumulator entry of E' = 0
+        double cst = (double)((LT ? 3 : 4) * rs);
+        const uint32_t kb = LT ? (((uint32_t)l1 << 20) | ((uint32_t)rowB << 10) | (uint32_t)S0)
+                               : (((uint32_t)l1 << 20) | ((uint32_t)rs << 10) | (uint32_t)rs);
+        double best[TE];
+        int widx[TE];
+#pragma unroll
+        for (int t = 0; t < TE; ++t) { best[t] = D_INF; widx[t] = 0; }
+        Cell4 x = d_load(rp);
+        int blk = 0;
+#define OOB_STEP(I)                                                                             \
+    {                                                                                           \
+        const Cell4 nx = d_load(rp + blk + (I) + 1);                                            \
+        const double xc = __dadd_rn(x.C1, xadd);                                                \
+        _Pragma("unroll") for (int t = 0; t < TE; ++t) {                                        \
+            const int sl = ((I) + t) % TE;                                                      \
+            const double cs = t == 0 ? xc : __dadd_rn(xc, (double)((LT ? 4 : 3) * t));          \
+            const double ct = __dadd_rn(RC1[t], cst);                                           \
+            const double tot = LT ? split_total(RT1[t], RT3[t], RTS[t], ct, x.T1, x.T3, x.TS, cs) \
+                                  : split_total(x.T1, x.T3, x.TS, cs, RT1[t], RT3[t], RTS[t], ct); \
+            if (t == TE - 1) {                                                                  \
+                best[sl] = tot;                                                                 \
+                widx[sl] = t;                                                                   \
+            } else {                                                                            \
+                const bool upd = LT ? (tot <= best[sl]) : (tot < best[sl]);                     \
+                best[sl] = upd ? tot : best[sl];                                                \
+                widx[sl] = upd ? t : widx[sl];                                                  \
+            }                                                                                   \
+        }                                                                                       \
+        cst = __dadd_rn(cst, LT ? 3.0 : 4.0);                                                   \
+        acc_flush(acc_s, filt_s, idx0 + blk + (I), best[(I)],                                   \
+                  LT ? kb + (uint32_t)widx[(I)] : kb + (uint32_t)(blk + (I) - widx[(I)]));      \
+        x = nx;                                                                                 \
+    }
+#pragma unroll 1
+        for (; blk + TE <= rl; blk += TE) {
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + blk + 3 * TE));
+#pragma unroll
+            for (int I = 0; I < TE; ++I) OOB_STEP(I)
+        }
+#pragma unroll
+        for (int I = 0; I < TE - 1; ++I)
+            if (blk + I < rl) OOB_STEP(I)
+#undef OOB_STEP
+        // pending: slot sl holds E' = rl + ((sl - rl) mod TE); E' = rl + TE - 1 is the slot of
+        // E' = rl - 1, already flushed
+#pragma unroll
+        for (int sl = 0; sl < TE; ++sl) {
+            const int Ep = rl + (((sl - rl) % TE) + TE) % TE;
+            if (Ep <= rl + TE - 2)
+                acc_flush(acc_s, filt_s, idx0 + Ep, best[sl],
+                          LT ? kb + (uint32_t)widx[sl] : kb + (uint32_t)(Ep - widx[sl]));
+        }
+        rp += rl;
+    }
+}
 
 template <int TE>
-__global__ void __launch_bounds__(NT_MAX, (TE <= 4 ? 2 : 1)) k_wave_w(DevGeom g, WaveW w) {
+__global__ void __launch_bounds__(NTW, 2) k_wave_w(DevGeom g, WaveW w) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int l = w.l;
     const int nout = w.nout;
-    ulonglong2 *acc = reinterpret_cast<ulonglong2 *>(smem);
-    int *outOff = reinterpret_cast<int *>(acc + nout);    // [L+2] W(q) offsets in slab l
-    int *ucum = outOff + (g.L + 2);                        // [L+2] cumulative units per entry
-    int *ctr = ucum + (g.L + 2);
-    const int NT = blockDim.x;
+    const int L = g.L, M = g.M;
+    const int ndum = L + 2 * TE + 2;                              // dummy entries
+    ulonglong2 *acc = reinterpret_cast<ulonglong2 *>(smem);     // [nout] + dummy[ndum]
+    unsigned *filt = reinterpret_cast<unsigned *>(acc + nout + ndum);  // [nout + ndum] high words
+    int4 *sents = reinterpret_cast<int4 *>(filt + ((nout + ndum + 3) & ~3));   // [nents] (16 B aligned)
+    int64_t *sbase = reinterpret_cast<int64_t *>(sents + w.nents);               // [L+2]
+    int *scells = reinterpret_cast<int *>(sbase + L + 2);        // [L+1]
+    int *outOff = scells + (L + 1);                              // [L+2] W(q) offsets (nout: none)
+    int *upre = outOff + (L + 2);                                // [nents + 1]
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    int bid = blockIdx.x;
-    const int item = bid % w.nitems; bid /= w.nitems;
-    const int u = bid % w.nranges;
-    const int p = bid / w.nranges;
+    const int pr = blockIdx.x / w.cpr;
+    const int u = pr % w.nranges;
+    const int p = pr / w.nranges;
     const int64_t pc = (int64_t)p * g.C;
-    const int4 it = w.items[item];
-    const int Ql = (l == g.L) ? g.n_hi : max(1, g.n_hi - 1);
+    const int Ql = (l == L) ? g.n_hi : max(1, g.n_hi - 1);
 
-    for (int i = tid; i < nout; i += NT)
-        acc[i] = make_ulonglong2((unsigned long long)__double_as_longlong(D_INF), 0xFFFFFFFFull);
-    for (int q = tid; q < g.L + 2; q += NT) outOff[q] = (q >= 1 && q <= Ql && q <= l) ? d_woff(g, l, q) : -1;
-    if (tid == 0) {
-        int c = 0;
-        ucum[0] = 0;
-        for (int e = it.x; e < it.y; ++e) {
-            const int4 en = w.ents[e];
-            c += en.y * en.z;
-            ucum[e - it.x + 1] = c;
-        }
-        *ctr = 0;
+    for (int i = tid; i < nout + ndum; i += NTW) {
+        const bool real = i < nout;
+        acc[i] = real ? make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull) : make_ulonglong2(0ull, 0ull);
+        filt[i] = real ? (unsigned)(ACC_EMPTY >> 32) : 0u;
+    }
+    for (int i = tid; i < L + 2; i += NTW) {
+        sbase[i] = g.base[i];
+        if (i <= L) scells[i] = g.cells[i];
+        outOff[i] = (i >= 2 && i <= Ql && i <= l) ? c_woff(M, l, i) : nout;
+    }
+    for (int i = tid; i <= w.nents; i += NTW) {
+        upre[i] = w.upre[i];
+        if (i < w.nents) sents[i] = w.ents[i];
     }
     __syncthreads();
-    const int nunits = ucum[it.y - it.x];
+    const int nunits = upre[w.nents];
+    const unsigned acc_s = (unsigned)__cvta_generic_to_shared(acc);
+    const unsigned filt_s = (unsigned)__cvta_generic_to_shared(filt);
+    int *gctr = w.ctr + pr;
 
     for (;;) {
         int un = 0;
-        if (lane == 0) un = atomicAdd(ctr, 1);
+        if (lane == 0) un = atomicAdd(gctr, 1);
         un = __shfl_sync(0xFFFFFFFFu, un, 0);
         if (un >= nunits) break;
-        int ei = 0;
-        while (ucum[ei + 1] <= un) ++ei;
-        const int4 en = w.ents[it.x + ei];
+        int lo = 0, hi = w.nents - 1;                // entry: upre[ei] <= un < upre[ei+1]
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (upre[mid] <= un) lo = mid; else hi = mid - 1;
+        }
+        const int ei = lo;
+        const int4 en = sents[ei];
         const int l1 = en.x;
-        const int local = un - ucum[ei];
+        const int local = un - upre[ei];
         const int chunk = local / en.y;
         const int blk = local % en.y;
         const int r_lo = w.cb[en.w + chunk], r_hi = w.cb[en.w + chunk + 1];
         const int k = u + l1;
         const int l2 = l - l1;
-        const bool ltiled = d_wcells(g, l1) >= d_wcells(g, l2);   // big side = left
+        const int Q1 = (l1 == L) ? g.n_hi : max(1, g.n_hi - 1), Q2 = (l2 == L) ? g.n_hi : max(1, g.n_hi - 1);
+        const int wc1 = c_woff(M, l1, min(Q1, l1) + 1), wc2 = c_woff(M, l2, min(Q2, l2) + 1);
+        const bool ltiled = wc1 >= wc2;                             // big side = left
         const int ls = ltiled ? l2 : l1;                           // small side length
         const int lb = ltiled ? l1 : l2;
         const int us = ltiled ? k : u;                             // small slab start
@@ -205,207 +325,147 @@ __global__ void __launch_bounds__(NT_MAX, (TE <= 4 ? 2 : 1)) k_wave_w(DevGeom g,
         const int32_t code = has ? w.tiles[w.tile_off[lb] + ti] : 0;
         const int rowB = has ? (code >> 16) : 1;
         const int e0 = has ? (code & 0xFFFF) : 0;
-        const int lenB = has ? d_wlen(g, lb, rowB) : 0;
-        const Cell4 *bp = g.CELL + pc + g.base[lb] + (int64_t)ub * g.cells[lb] +
-                          (has ? g.off[lb * g.A + (g.M - 1) + rowB - 1] : 0) + e0;
+        const int lenB = has ? c_wlen(M, lb, rowB) : 0;
+        const int ncell = max(0, min(TE, lenB - e0));             // valid cells of the tile
+        const Cell4 *bp = g.CELL + pc + sbase[lb] + (int64_t)ub * scells[lb] + c_ipart(M, lb) +
+                          (has ? c_woff(M, lb, rowB) : 0) + e0;
         // register tile: T1, T3, t*, C1 of TE big-side cells (sentinels beyond the row)
         double RT1[TE], RT3[TE], RTS[TE], RC1[TE];
 #pragma unroll
         for (int t = 0; t < TE; ++t) {
-            if (has && e0 + t < lenB) {
+            if (t < ncell) {
                 const Cell4 c = d_load(bp + t);
                 RT1[t] = c.T1; RT3[t] = c.T3; RTS[t] = c.TS; RC1[t] = c.C1;
             } else {
                 RT1[t] = D_INF; RT3[t] = D_INF; RTS[t] = D_INF; RC1[t] = 1.0;
             }
         }
-        // stage count of the tile's first cell (its c2 = 4s or 3S_R is folded per step)
-        const double S0 = (double)(rowB + e0);
-        const Cell4 *sp = g.CELL + pc + g.base[ls] + (int64_t)us * g.cells[ls] + g.off[ls * g.A + (g.M - 1)];
-        for (int rs = r_lo; rs < r_hi; ++rs) {
-            const int q = rowB + rs;
-            const int ob = (has && q <= g.L + 1) ? outOff[q] : -1;
-            const bool qok = ob >= 0;
-            const int rl = d_wlen(g, ls, rs);
-            const Cell4 *rp = sp + d_woff(g, ls, rs);
-            double best[TE];
-            int widx[TE];
-#pragma unroll
-            for (int t = 0; t < TE; ++t) { best[t] = D_INF; widx[t] = 0; }
-            if (ltiled) {
-                // big = left row j = rowB (s_t = S0 + t); iterate right row j' = rs, e'
-                // ascending (S_R = rs + e').  coef_left = 3S_R + C1_L[t];
-                // coef_right = 4 s_t + C1_R = (C1_R + 4 S0) + 4t.
-                // Ring slot r <-> output E with (E - e0) % TE == r.
-                const int j = rowB;
-                const uint32_t kb = ((uint32_t)l1 << 20) | ((uint32_t)j << 10) | (uint32_t)(j + e0);
-                double c3 = (double)(3 * rs);          // 3 S_R
-                const double s4 = 4.0 * S0;
-                Cell4 x = d_load(rp);
-                int ep = 0;
-#define OOB_LT_STEP(I)                                                                          \
-    {                                                                                           \
-        const Cell4 nx = d_load(rp + min(ep + (I) + 1, rl - 1));                                \
-        const double xr = __dadd_rn(x.C1, s4);                                                  \
-        _Pragma("unroll") for (int t = 0; t < TE; ++t)                                          \
-            split_eval(RT1[t], RT3[t], RTS[t], c3, RC1[t], x.T1, x.T3, x.TS, xr,                \
-                       (double)(4 * t), best[((I) + t) % TE], widx[((I) + t) % TE], t, t == 0); \
-        c3 = __dadd_rn(c3, 3.0);                                                                \
-        acc_flush(acc, ob + e0 + ep + (I), qok && best[(I)] < D_INF, best[(I)],                \
-                  kb + (uint32_t)widx[(I)]);                                                    \
-        best[(I)] = D_INF;                                                                      \
-        x = nx;                                                                                 \
+        const Cell4 *sp = g.CELL + pc + sbase[ls] + (int64_t)us * scells[ls] + c_ipart(M, ls);
+        if (ltiled)
+            run_rows<TE, true>(sp, M, ls, r_lo, r_hi, RT1, RT3, RTS, RC1, rowB, e0, l1, L, outOff, nout, acc_s,
+                               filt_s);
+        else
+            run_rows<TE, false>(sp, M, ls, r_lo, r_hi, RT1, RT3, RTS, RC1, rowB, e0, l1, L, outOff, nout, acc_s,
+                                filt_s);
     }
-#pragma unroll 1
-                for (; ep + TE <= rl; ep += TE) {
+    __syncthreads();
+    // merge into the range's global accumulator (L2-coherent loads; a stale value is an
+    // upper bound of the current one, so the CAS loop stays exact).  Loads are batched so
+    // their latencies overlap.
+    ulonglong2 *ga = w.GACC + ((size_t)p * w.nranges + u) * nout;
+    constexpr int MB = 4;
+    for (int i0 = tid; i0 < nout; i0 += MB * NTW) {
+        ulonglong2 a[MB], cur[MB];
 #pragma unroll
-                    for (int i = 0; i < TE; ++i) OOB_LT_STEP(i)
-                }
+        for (int j = 0; j < MB; ++j) {
+            const int i = i0 + j * NTW;
+            a[j] = i < nout ? acc[i] : make_ulonglong2(ACC_EMPTY, 0ull);
+            cur[j] = a[j].x < ACC_EMPTY ? __ldcg(ga + i) : make_ulonglong2(0ull, 0ull);
+        }
 #pragma unroll
-                for (int i = 0; i < TE - 1; ++i)
-                    if (ep + i < rl) OOB_LT_STEP(i)
-#undef OOB_LT_STEP
-#pragma unroll
-                for (int r = 0; r < TE; ++r) {
-                    const int E = e0 + rl + (((r - rl) % TE) + TE) % TE;
-                    acc_flush(acc, ob + E, qok && best[r] < D_INF, best[r], kb + (uint32_t)widx[r]);
-                }
-            } else {
-                // big = right row j' = rowB (S_R,t = S0 + t); iterate left row j = rs, e
-                // descending (s = rs + e).  coef_left = 3 S_R,t + C1_L = (C1_L + 3 S0) + 3t;
-                // coef_right = 4s + C1_R[t].  Step i = rl-1-e; slot (t - i) % TE holds output
-                // E = e + e0 + t; the t = TE-1 output completes at each step.
-                const int jl = rs;
-                const uint32_t kb = ((uint32_t)l1 << 20) | ((uint32_t)jl << 10);
-                double c4 = (double)(4 * (rs + rl - 1));   // 4 s
-                const double s3 = 3.0 * S0;
-                Cell4 x = d_load(rp + rl - 1);
-                int st = 0;
-#define OOB_RT_STEP(I)                                                                          \
-    {                                                                                           \
-        const int e = rl - 1 - st - (I);                                                        \
-        const Cell4 nx = d_load(rp + max(e - 1, 0));                                            \
-        const double xl = __dadd_rn(x.C1, s3);                                                  \
-        _Pragma("unroll") for (int t = 0; t < TE; ++t)                                          \
-            split_eval2(x.T1, x.T3, x.TS, xl, (double)(3 * t), RT1[t], RT3[t], RTS[t], c4,      \
-                       RC1[t], best[((t - (I)) % TE + TE) % TE], widx[((t - (I)) % TE + TE) % TE], t, t == 0); \
-        c4 = __dadd_rn(c4, -4.0);                                                               \
-        const int sf = ((TE - 1 - (I)) % TE + TE) % TE;                                         \
-        const int E = e + e0 + TE - 1;                                                          \
-        acc_flush(acc, ob + E, qok && best[sf] < D_INF, best[sf],                               \
-                  kb + (uint32_t)(jl + E - e0 - widx[sf]));                                     \
-        best[sf] = D_INF;                                                                       \
-        x = nx;                                                                                 \
-    }
-#pragma unroll 1
-                for (; st + TE <= rl; st += TE) {
-#pragma unroll
-                    for (int i = 0; i < TE; ++i) OOB_RT_STEP(i)
-                }
-#pragma unroll
-                for (int i = 0; i < TE - 1; ++i)
-                    if (st + i < rl) OOB_RT_STEP(i)
-#undef OOB_RT_STEP
-                // after the last step (i = rl-1, e = 0) slot sg holds t = (sg + rl - 1) % TE
-#pragma unroll
-                for (int sg = 0; sg < TE; ++sg) {
-                    const int t = (sg + rl - 1) % TE;
-                    const int E = e0 + t;
-                    acc_flush(acc, ob + E, qok && best[sg] < D_INF, best[sg],
-                              kb + (uint32_t)(jl + E - e0 - widx[sg]));
-                }
+        for (int j = 0; j < MB; ++j) {
+            const int i = i0 + j * NTW;
+            while (lex_less(a[j].x, (uint32_t)a[j].y, cur[j].x, (uint32_t)cur[j].y)) {
+                unsigned long long ox, oy;
+                cas128_global(ga + i, ox, oy, cur[j].x, cur[j].y, a[j].x, a[j].y);
+                if (ox == cur[j].x && oy == cur[j].y) break;
+                cur[j].x = ox;
+                cur[j].y = oy;
             }
         }
     }
-    __syncthreads();
-    const size_t pb = (size_t)blockIdx.x * nout;
-    for (int i = tid; i < nout; i += NT) {
-        const ulonglong2 a = acc[i];
-        w.PB[pb + i] = __longlong_as_double((long long)a.x);
-        w.PK[pb + i] = (uint32_t)a.y;
-    }
 }
 
-// Per W(q >= 2) cell: lexicographic min of the items' partials, then the winner's
-// (T1, T3, t*, C1) recomputed from its two children (same arithmetic as the oracle).
-__global__ void k_wave_w_finalize(DevGeom g, WaveW w) {
-    const int l = w.l;
-    const int nout = w.nout;
-    const int64_t n = (int64_t)g.P * w.nranges * nout;
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    const int i = (int)(t % nout);
-    const int u = (int)((t / nout) % w.nranges);
-    const int p = (int)(t / ((int64_t)nout * w.nranges));
-    const int Ql = (l == g.L) ? g.n_hi : max(1, g.n_hi - 1);
-    int q = 0, Sp = 0;
-    for (int qq = 2; qq <= min(Ql, l); ++qq) {
-        const int o = d_woff(g, l, qq);
-        const int len = d_wlen(g, l, qq);
-        if (o >= 0 && i >= o && i < o + len) { q = qq; Sp = qq + (i - o); break; }
-    }
-    if (q == 0) return;       // W(1) cell (handled by k_wave_small)
-    double best = D_INF;
-    uint32_t key = 0xFFFFFFFFu;
-    const size_t base = ((size_t)p * w.nranges + u) * w.nitems;
-    for (int it = 0; it < w.nitems; ++it) {
-        const size_t pi = (base + it) * nout + i;
-        const double b = w.PB[pi];
-        const uint32_t kk = w.PK[pi];
-        if (b < best || (b == best && kk < key)) { best = b; key = kk; }
-    }
-    const int64_t pc = (int64_t)p * g.C;
-    const int aW = (g.M - 1) + q - 1;
-    if (!(best < D_INF)) {     // no split found: impossible for a valid cell; poison it
-        const int64_t c = pc + d_cell(g, Sp, u, l, aW);
-        g.CELL[c].T1 = __longlong_as_double(0x7ff8000000000000LL);
-        g.ARG[c] = 0xFFFFFFFEu;
+__global__ void k_gacc_init(ulonglong2 *gacc, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) gacc[i] = make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull);
+}
+
+// Per-wave finalize + small cells.  Blocks [0, nbw): one thread per (profile, range, W-part
+// cell) of wave lw (lw >= 2): read + reset the global accumulator, recompute the winner.
+// Blocks [nbw, ...): cells inside one node (I(r), W(1), S' >= 2) of wave ls (2 <= ls <= L):
+// `tpc` threads per cell (32..256, power of two) split the (k, m) pairs of the cell, scan
+// s, keep the first strictly smaller total, then a lexicographic (total, key) reduction.
+struct FinArgs {
+    int lw, nranges_w, nout_w;     // W finalize of wave lw (lw = 0: none)
+    int nbw;                       // blocks of the W part
+    ulonglong2 *GACC;
+    int ls, nsmall;                // small cells of wave ls (ls = 0: none); cells per range
+    int tpc;                       // threads per small cell
+};
+
+__global__ void __launch_bounds__(256) k_fin(DevGeom g, FinArgs f) {
+    __shared__ double red_b[8];
+    __shared__ uint32_t red_k[8];
+    if ((int)blockIdx.x < f.nbw) {
+        const int l = f.lw;
+        const int nout = f.nout_w;
+        const int64_t n = (int64_t)g.P * f.nranges_w * nout;
+        const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if (t >= n) return;
+        const int i = (int)(t % nout);
+        const int u = (int)((t / nout) % f.nranges_w);
+        const int p = (int)(t / ((int64_t)nout * f.nranges_w));
+        const int Ql = (l == g.L) ? g.n_hi : max(1, g.n_hi - 1);
+        // row q of the W-part cell i: largest q with c_woff(q) <= i (binary search, closed form)
+        int lo = 1, hi = min(Ql, l);
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (c_woff(g.M, l, mid) <= i) lo = mid; else hi = mid - 1;
+        }
+        const int q = lo, Sp = q + (i - c_woff(g.M, l, q));
+        if (q < 2) return;        // W(1) cell (computed with the small cells)
+        ulonglong2 *ga = f.GACC + t;
+        const ulonglong2 a = __ldcg(ga);
+        __stcg(ga, make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull));
+        const int64_t pc = (int64_t)p * g.C;
+        const int aW = (g.M - 1) + q - 1;
+        if (a.x >= ACC_EMPTY) {   // no split found: impossible for a valid cell; poison it
+            const int64_t c = pc + d_cell(g, Sp, u, l, aW);
+            g.CELL[c].T1 = __longlong_as_double(0x7ff8000000000000LL);
+            g.ARG[c] = 0xFFFFFFFEu;
+            return;
+        }
+        const uint32_t key = (uint32_t)a.y;
+        const int l1 = (int)(key >> 20), j = (int)((key >> 10) & 1023u), s = (int)(key & 1023u);
+        d_write_winner(g, pc, Sp, u, l, aW, l1, j - 1, s);
         return;
     }
-    const int l1 = (int)(key >> 20), j = (int)((key >> 10) & 1023u), s = (int)(key & 1023u);
-    d_write_winner(g, pc, Sp, u, l, aW, l1, j - 1, s);
-}
-
-// I(r) and W(1) cells with S' >= 2 (GPUs inside one node): one warp per cell, lanes take
-// contiguous k ranges in the oracle's order (strict "<"), then a lexicographic
-// (total, key) warp-shuffle argmin.
-__global__ void k_wave_small(DevGeom g, int l) {
-    const int nsmall = min(g.A, g.M);              // alloc indices 0..M-1: I(1..M-1), W(1)
+    // ---------------- small cells of wave ls
+    const int l = f.ls;
     const int nr = g.L - l + 1;
-    const int64_t warp_id = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    int per_range = 0;
-    for (int a = 0; a < nsmall; ++a) per_range += max(0, d_hi(g, a, l) - 1);
-    if (per_range == 0) return;
-    if (warp_id >= (int64_t)g.P * nr * per_range) return;
-    int rem = (int)(warp_id % per_range);
-    const int u = (int)((warp_id / per_range) % nr);
-    const int p = (int)(warp_id / ((int64_t)per_range * nr));
-    int a = 0, Sp = 0;
-    for (int aa = 0; aa < nsmall; ++aa) {
-        const int c = max(0, d_hi(g, aa, l) - 1);
-        if (rem < c) { a = aa; Sp = 2 + rem; break; }
-        rem -= c;
-    }
-    if (g.off[l * g.A + a] < 0) return;
-    const int64_t pc = (int64_t)p * g.C;
-    const double dSp3 = (double)(3 * Sp - 1);
-    const int nd = d_num_dsplits(g, a);
-    const int per_lane = (l - 1 + 31) / 32;
-    const int l1_lo = 1 + lane * per_lane, l1_hi = min(l - 1, (lane + 1) * per_lane);
+    const int cpb = blockDim.x / f.tpc;                      // cells per block
+    const int sub = threadIdx.x / f.tpc, tl = threadIdx.x % f.tpc;
+    const int64_t cell = (int64_t)(blockIdx.x - f.nbw) * cpb + sub;
+    const bool active = cell < (int64_t)g.P * nr * f.nsmall;
     double best = D_INF;
     uint32_t bkey = 0xFFFFFFFFu;
-    for (int l1 = l1_lo; l1 <= l1_hi; ++l1) {
-        const int k = u + l1, l2 = l - l1;
-        for (int j = 0; j < nd; ++j) {
-            int a1, a2;
-            d_dsplit(g, a, j, a1, a2);
-            if (g.off[l1 * g.A + a1] < 0 || g.off[l2 * g.A + a2] < 0) continue;
-            const int s_lo = max(max(1, d_lo(g, a1)), Sp - d_hi(g, a2, l2));
-            const int s_hi = min(min(Sp - 1, d_hi(g, a1, l1)), Sp - d_lo(g, a2));
+    int u = 0, p = 0, a = 0, Sp = 0;
+    if (active) {
+        int rem = (int)(cell % f.nsmall);
+        u = (int)((cell / f.nsmall) % nr);
+        p = (int)(cell / ((int64_t)f.nsmall * nr));
+        const int nsm = min(g.A, g.M);                       // alloc indices 0..M-1: I(1..M-1), W(1)
+        for (int aa = 0; aa < nsm; ++aa) {
+            const int c = max(0, d_hi(g, aa, l) - 1);
+            if (rem < c) { a = aa; Sp = 2 + rem; break; }
+            rem -= c;
+        }
+        const int64_t pc = (int64_t)p * g.C;
+        const double dSp3 = (double)(3 * Sp - 1);
+        const int r = d_is_whole(g, a) ? g.M : d_alloc_n(g, a);  // GPUs of the cell's node part
+        const int nd = r - 1;                                    // device splits (I(m), I(r-m))
+        const int npairs = (l - 1) * nd;
+        for (int fp = tl; fp < npairs; fp += f.tpc) {
+            const int l1 = 1 + fp / nd, m = 1 + fp % nd;
+            const int k = u + l1, l2 = l - l1;
+            const int s_lo = max(1, Sp - min(l2, r - m));
+            const int s_hi = min(Sp - 1, min(l1, m));
+            const Cell4 *lb = g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + g.off[l1 * g.A + (m - 1)] - 1;
+            const Cell4 *rb = g.CELL + pc + g.base[l2] + (int64_t)k * g.cells[l2] + g.off[l2 * g.A + (r - m - 1)] - 1;
             for (int s = s_lo; s <= s_hi; ++s) {
-                const Cell4 Lc = d_load(g.CELL + pc + d_cell(g, s, u, l1, a1));
-                const Cell4 Rc = d_load(g.CELL + pc + d_cell(g, Sp - s, k, l2, a2));
+                const Cell4 Lc = d_load(lb + s);
+                const Cell4 Rc = d_load(rb + (Sp - s));
                 const double T1 = __dadd_rn(Lc.T1, Rc.T1);
                 const bool left = Lc.TS >= Rc.TS;
                 const double T3 = left ? __dadd_rn(Lc.T3, Rc.T1) : Rc.T3;
@@ -415,19 +475,32 @@ __global__ void k_wave_small(DevGeom g, int l) {
                 const double tot = __dadd_rn(__dadd_rn(T1, T2), T3);
                 if (tot < best) {
                     best = tot;
-                    bkey = ((uint32_t)l1 << 20) | ((uint32_t)j << 10) | (uint32_t)s;
+                    bkey = ((uint32_t)l1 << 20) | ((uint32_t)(m - 1) << 10) | (uint32_t)s;
                 }
             }
         }
     }
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) {
-        const double ob = __shfl_down_sync(0xFFFFFFFFu, best, d);
-        const uint32_t ok = __shfl_down_sync(0xFFFFFFFFu, bkey, d);
+    // lexicographic (total, key) reduction over the tpc threads of the cell (segments of
+    // width min(tpc, 32) inside a warp, then across the cell's warps)
+    const int wd = min(f.tpc, 32);
+    for (int d = wd >> 1; d >= 1; d >>= 1) {
+        const double ob = __shfl_down_sync(0xFFFFFFFFu, best, d, wd);
+        const uint32_t ok = __shfl_down_sync(0xFFFFFFFFu, bkey, d, wd);
         if (ob < best || (ob == best && ok < bkey)) { best = ob; bkey = ok; }
     }
-    if (lane != 0) return;
-    d_write_winner(g, pc, Sp, u, l, a, (int)(bkey >> 20), (int)((bkey >> 10) & 1023u), (int)(bkey & 1023u));
+    if (f.tpc > 32) {
+        const int wid = threadIdx.x >> 5;
+        if ((threadIdx.x & 31) == 0) { red_b[wid] = best; red_k[wid] = bkey; }
+        __syncthreads();
+        if ((threadIdx.x & 31) != 0 || tl != 0) return;
+        for (int w2 = wid + 1; w2 < wid + f.tpc / 32; ++w2)
+            if (red_b[w2] < best || (red_b[w2] == best && red_k[w2] < bkey)) { best = red_b[w2]; bkey = red_k[w2]; }
+    } else if (tl != 0) {
+        return;
+    }
+    if (!active) return;
+    d_write_winner(g, (int64_t)p * g.C, Sp, u, l, a, (int)(bkey >> 20), (int)((bkey >> 10) & 1023u),
+                   (int)(bkey & 1023u));
 }
 
 }  // namespace oob
