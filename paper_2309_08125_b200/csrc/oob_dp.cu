@@ -281,11 +281,10 @@ static double k_cost(const oob_dp_plan *pl, int TE, int l, int l1, int it_lo, in
 // totals early; an entry's small-side rows are cut into chunks of ~CH steps; a warp unit is
 // (entry, chunk, block of 32 big-side tiles).  `slots` = resident CTAs of the GPU: ranges
 // get several CTAs (sharing the range's queue) when there are fewer ranges than slots.
-static void build_wave(oob_dp_plan *pl, int l, int ci, int slots, WaveHost &wh) {
+static void build_wave(oob_dp_plan *pl, int l, int ci, int slots, WaveHost &wh, int CH = 96) {
     const Geometry &g = pl->g;
     const int TE = WCFGS[ci].te;
     const int nr = g.L - l + 1;
-    const int CH = 96;
     std::vector<int> order;
     for (int l1 = 1; l1 < l; ++l1) order.push_back(l1);
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return std::abs(2 * a - l) < std::abs(2 * b - l); });
@@ -364,7 +363,11 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
         for (int ci = 0; ci < NWCFG; ++ci) {
             if (pl->force_cfg >= 0 && ci != pl->force_cfg) continue;
             WaveHost wh;
-            build_wave(pl, l, ci, 2 * 148, wh);
+            // smaller chunks (more, shorter units) until every warp slot has ~4 units
+            for (int CH = 96;; CH /= 2) {
+                build_wave(pl, l, ci, 2 * 148, wh, CH);
+                if (CH <= 12 || (int64_t)wh.nunits * num_profiles * (L - l + 1) >= 4LL * 2 * 148 * (NTW / 32)) break;
+            }
             // resident CTAs per SM: launch bounds 256 x 2, smem
             const int by_smem = std::max<int>(1, (int)((227 * 1024) / std::max<size_t>(wh.smem, 1)));
             const int per_sm = std::max(1, std::min(2, by_smem));
