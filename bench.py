@@ -180,10 +180,15 @@ def main():
 
     from paper_2309_08125_b200 import planner
 
+    from paper_2309_08125_b200 import dist as odist
     if cfg.key == "cfg5":
-        P = args.profiles_per_rank or max(1, cfg.num_profiles // world)
+        # the 1024-profile sweep sharded in contiguous blocks (weak scaling: --profiles-per-rank)
         from workloads import random_profile
-        profs = [random_profile(cfg.seed + rank * P + i, cfg.L, cfg.M, "lognormal") for i in range(P)]
+        if args.profiles_per_rank:
+            first, P = rank * args.profiles_per_rank, args.profiles_per_rank
+        else:
+            first, P = odist.shard(cfg.num_profiles, world, rank)
+        profs = [random_profile(cfg.seed + first + i, cfg.L, cfg.M, "lognormal") for i in range(P)]
     else:
         P = args.profiles_per_rank or 1
         from workloads import gpt_profile
@@ -196,15 +201,14 @@ def main():
     bwd = torch.tensor(np.stack([p.bwd_ms for p in profs]), dtype=torch.float64, device=dev)
     ws = torch.empty(info.workspace_bytes, dtype=torch.uint8, device=dev)
     packed = torch.empty(info.packed_bytes, dtype=torch.uint8, device=dev)
-    gathered = torch.empty(info.packed_bytes * world, dtype=torch.uint8, device=dev) if world > 1 else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
 
     def step():
         plan.run(fwd.data_ptr(), bwd.data_ptr(), ws.data_ptr(), ws.numel(), packed.data_ptr(), sptr)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, packed)
+        if world > 1:   # one NCCL all-gather assembles every rank's packed template sets
+            odist.allgather_packed(packed, info.packed_bytes)
 
     for _ in range(args.warmup):
         step()
@@ -234,6 +238,9 @@ def main():
     total_ms, kern_ms_max = float(t[0]), float(t[1])
     ms_per_step = total_ms / args.steps
     cells_step = info.cells_per_profile * P * world
+    # cfg5 default: the fixed 1024-profile sweep is split across ranks (strong scaling);
+    # otherwise every rank plans its own profile(s) of the workload's shape (weak scaling)
+    scaling = "strong" if (cfg.key == "cfg5" and not args.profiles_per_rank) else "weak"
     splits_step = info.splits_per_profile * P * world
     value = cells_step / (ms_per_step / 1e3)
 
@@ -243,9 +250,15 @@ def main():
     kern_ms_per_step = kern_ms / args.steps
     achieved = info.splits_per_profile * P * FP64_PER_SPLIT / (kern_ms_per_step / 1e3) / 1e12
     peak = SMS * FP64_LANES_PER_SM * sm_max * 1e6 / 1e12
+    traffic = None
+    try:   # DRAM bytes per launch of the dominant kernel, from the committed ncu capture
+        with open(os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.key}.json")) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        traffic = None
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFP64inst/s",
-                "frac": achieved / peak, "traffic": None,
-                "kernel": "k_wave (DP wavefront)", "kernel_ms_per_step": kern_ms_per_step,
+                "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes/launch (ncu, k_wave_w)",
+                "kernel": "k_wave_w (W-cell wavefront DP)", "kernel_ms_per_step": kern_ms_per_step,
                 "kernel_share_of_step": kern_ms_per_step / (total_ms / args.steps) if world == 1 else None,
                 "peak_basis": f"148 SMs x 64 FP64 lanes x {sm_max:.0f} MHz (max clock)",
                 "frac_at_observed_clock": (achieved / (SMS * FP64_LANES_PER_SM * clocks["sm_mhz"] * 1e6 / 1e12))
@@ -302,7 +315,7 @@ def main():
                    "host_cpu": _cpu_model(), "host_cores": os.cpu_count()}
         line = {"metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": cfg.key, "label": cfg.label, "L": cfg.L, "M": cfg.M, "N": cfg.N,
                            "f": cfg.f, "n0": cfg.n0, "sizes": [cfg.n0, cfg.n_max], "profiles_per_rank": P,
                            "cells_per_step": cells_step, "splits_per_step": splits_step,

@@ -154,3 +154,42 @@ def test_v1_kernel_still_matches(planner, key, monkeypatch):
     ts = _gpu_set(planner, [prof], (cfg.L, cfg.M, cfg.N, cfg.f, cfg.n0))
     want, _ = coracle.template_set(prof.fwd_ms, prof.bwd_ms, cfg.M, cfg.n0, cfg.n_max)
     _assert_same(ts.templates(0), want, key + " v1")
+
+
+@pytest.mark.parametrize("key", ["cfg2", "cfg3"])
+def test_te5_kernel_config_matches(planner, key, monkeypatch):
+    """The alternative W-kernel configuration (TE = 5 register tile, OOB_DP_WCFG=1)."""
+    monkeypatch.setenv("OOB_DP_WCFG", "1")
+    cfg = CONFIGS[key]
+    prof = config_profiles(cfg, "real")[0]
+    ts = _gpu_set(planner, [prof], (cfg.L, cfg.M, cfg.N, cfg.f, cfg.n0))
+    want, _ = coracle.template_set(prof.fwd_ms, prof.bwd_ms, cfg.M, cfg.n0, cfg.n_max)
+    _assert_same(ts.templates(0), want, key + " TE5")
+
+
+def test_cfg5_full_sweep_sampled(planner):
+    """The full batched sweep at BASELINE size (1024 profiles of 48 layers, one DP launch
+    sequence, as bench.py --workload cfg5 times it); profiles 0..3 vs the oracle's stored
+    sets, and a fresh oracle recomputation of two more sampled profiles' small templates."""
+    import torch
+    cfg = CONFIGS["cfg5"]
+    rec = load_golden("cfg5", "real")
+    if rec is None:
+        pytest.skip("tests/golden/cfg5_real.json not generated")
+    profs = config_profiles(cfg, "real")                     # all 1024
+    plan = planner.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, len(profs))
+    info = plan.info
+    fwd = torch.tensor(np.stack([p.fwd_ms for p in profs]), dtype=torch.float64, device="cuda")
+    bwd = torch.tensor(np.stack([p.bwd_ms for p in profs]), dtype=torch.float64, device="cuda")
+    ws = torch.empty(info.workspace_bytes, dtype=torch.uint8, device="cuda")
+    packed = torch.zeros(info.packed_bytes, dtype=torch.uint8, device="cuda")
+    plan.run(fwd.data_ptr(), bwd.data_ptr(), ws.data_ptr(), ws.numel(), packed.data_ptr(),
+             torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    ts = plan.template_set(packed.cpu().numpy())
+    for i in range(4):
+        _assert_same(ts.templates(i), rec["profiles"][i]["templates"], f"cfg5 profile {i}")
+    for i in (517, 1023):
+        p = profs[i]
+        want, _ = coracle.template_set(p.fwd_ms, p.bwd_ms, cfg.M, cfg.n0, cfg.n0 + 3)
+        _assert_same(ts.templates(i)[:4], want, f"cfg5 profile {i} sizes 1..4")
