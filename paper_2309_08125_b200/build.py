@@ -25,6 +25,8 @@ HEADERS = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false",
               "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-I", INC, "-I", CSRC]
+if os.environ.get("OOB_FLUSH_STATS"):          # diagnostic build (scripts/flush_stats.py)
+    NVCC_FLAGS += ["-DOOB_FLUSH_STATS"]
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall",
              "-I", INC, "-I", CSRC, "-I", os.path.join(CUDA, "include")]
 

@@ -21,6 +21,7 @@
 #include <string>
 #include <cstring>
 #include <mutex>
+#include <numeric>
 #include <vector>
 
 #include "oob_internal.h"
@@ -180,6 +181,8 @@ namespace {
 // k_wave_w launch configurations: (TE cells per lane tile, threads per CTA)
 struct WCfg { int te, nt; };
 constexpr WCfg WCFGS[] = {{4, NTW}, {5, NTW}};
+constexpr int SEED_MIN_L = 6;      // waves seeded with proportional splits (k_fin)
+constexpr int CTAS_PER_SM = 512 / NTW;   // k_wave_w: 16 resident warps per SM (register bound: 128 regs)
 constexpr int NWCFG = 2;
 
 struct WaveHost {
@@ -190,7 +193,8 @@ struct WaveHost {
     std::vector<int32_t> upre;     // unit prefix per entry [nents + 1]
     std::vector<int32_t> cb;       // chunk row boundaries
     size_t smem = 0;
-    size_t ctr_off = 0;            // first unit counter of this wave (ints)
+    size_t ctr_off = 0;            // first unit counter of this wave (ints; two passes)
+    int seed_units = 0;            // units of the seeding pass (balanced splits), 0 = one pass
     int nsmall = 0;                // cells inside one node with S' >= 2 per range
     double cost = 0.0;             // modelled issue cycles of the wave (all ranges, profiles)
 };
@@ -213,6 +217,10 @@ struct oob_dp_plan {
     int32_t P = 1;
     int kernel = 2;                      // 1 = v1 (thread per cell), 2 = tiled W kernel
     int force_cfg = -1;
+    int seed_pass = 0;                   // OOB_DP_SEED=1 enables the seeding pass
+    int seed_init = 1;                   // OOB_DP_SEEDINIT=0: no proportional-split seeds
+    int perm_order = 0;                  // OOB_DP_PERM=1: pseudo-random unit order
+    int rev_lanes = 0;                   // OOB_DP_REV=1: reversed lane <-> tile order
     size_t geom_bytes = 0, ws_bytes = 0, tpl_bytes = 0;
     std::vector<unsigned char> geom_blob;   // host image of the geometry region
     size_t off_cells = 0, off_base = 0, off_off = 0, off_tiles = 0, off_tile_off = 0, off_tile_cnt = 0,
@@ -264,14 +272,13 @@ static void build_tiles(oob_dp_plan *pl, int TE) {
 // Issue-cycle model of one k restricted to small-side rows [it_lo, it_hi): every unit
 // (32 lanes) walks its rows; a step costs TE splits (~20 instructions each) plus the load
 // and the merge (~24).
-static double k_cost(const oob_dp_plan *pl, int TE, int l, int l1, int it_lo, int it_hi) {
+static double k_cost(const oob_dp_plan *pl, int TE, int l, int l1, bool lt) {
     const Geometry &g = pl->g;
     const int l2 = l - l1;
-    const bool lt = wcells_h(g, l1) >= wcells_h(g, l2);
-    const int ls = lt ? l2 : l1, lb = lt ? l1 : l2;
+    const int ls = lt ? l2 : l1, lb = lt ? l1 : l2;       // streamed side, tiled side
     const int JS = std::min(Q_of(g, ls), ls);
     double steps = 0.0;
-    for (int r = std::max(1, it_lo); r <= std::min(JS, it_hi - 1); ++r) steps += wlen_h(g, ls, r) + 2.0;
+    for (int r = 1; r <= JS; ++r) steps += wlen_h(g, ls, r) + 6.0;   // + per-row tail/flush/setup
     const double units = (pl->tab[te_index(TE)].cnt[lb] + 31) / 32;
     return units * (steps * (TE * 20.0 + 24.0) + 400.0);
 }
@@ -294,7 +301,11 @@ static void build_wave(oob_dp_plan *pl, int l, int ci, int slots, WaveHost &wh, 
     double total = 0.0;
     for (int l1 : order) {
         const int l2 = l - l1;
-        const bool lt = wcells_h(g, l1) >= wcells_h(g, l2);
+        // tile the left child (stream the right) or the reverse, whichever the model finds
+        // cheaper: tiling the bigger side fills the 32 lanes, streaming the longer rows cuts
+        // the per-row overhead
+        const double cl = k_cost(pl, TE, l, l1, true), cr = k_cost(pl, TE, l, l1, false);
+        const bool lt = cl <= cr;
         const int ls = lt ? l2 : l1, lb = lt ? l1 : l2;
         const int JS = std::min(Q_of(g, ls), ls);
         const int nblocks = (pl->tab[te_index(TE)].cnt[lb] + 31) / 32;
@@ -307,9 +318,9 @@ static void build_wave(oob_dp_plan *pl, int l, int ci, int slots, WaveHost &wh, 
         }
         wh.cb.push_back(JS + 1);
         if (nchunks == 0 || nblocks == 0) { wh.cb.resize(coff); continue; }
-        wh.ents.insert(wh.ents.end(), {l1, nblocks, nchunks, coff});
+        wh.ents.insert(wh.ents.end(), {l1 | (lt ? 1 << 16 : 0), nblocks, nchunks, coff});
         wh.upre.push_back(wh.upre.back() + nblocks * nchunks);
-        total += k_cost(pl, TE, l, l1, 1, 1 << 20);
+        total += std::min(cl, cr);
     }
     wh.cfg = ci;
     wh.nents = (int)wh.ents.size() / 4;
@@ -353,6 +364,10 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     const char *kv = std::getenv("OOB_DP_KERNEL");
     pl->kernel = (kv && std::string(kv) == "v1") ? 1 : 2;
     if (const char *fc = std::getenv("OOB_DP_WCFG")) pl->force_cfg = std::atoi(fc);
+    if (const char *sp = std::getenv("OOB_DP_SEED")) pl->seed_pass = std::atoi(sp) != 0;
+    if (const char *si = std::getenv("OOB_DP_SEEDINIT")) pl->seed_init = std::atoi(si) != 0;
+    if (const char *po = std::getenv("OOB_DP_PERM")) pl->perm_order = std::atoi(po) != 0;
+    if (const char *rv = std::getenv("OOB_DP_REV")) pl->rev_lanes = std::atoi(rv) != 0;
     build_tiles(pl, 4);
     build_tiles(pl, 5);
     pl->waves.assign(L + 1, WaveHost());
@@ -365,12 +380,13 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
             WaveHost wh;
             // smaller chunks (more, shorter units) until every warp slot has ~4 units
             for (int CH = 96;; CH /= 2) {
-                build_wave(pl, l, ci, 2 * 148, wh, CH);
-                if (CH <= 12 || (int64_t)wh.nunits * num_profiles * (L - l + 1) >= 4LL * 2 * 148 * (NTW / 32)) break;
+                build_wave(pl, l, ci, CTAS_PER_SM * 148, wh, CH);
+                if (CH <= 12 || (int64_t)wh.nunits * num_profiles * (L - l + 1) >= 4LL * CTAS_PER_SM * 148 * (NTW / 32))
+                    break;
             }
             // resident CTAs per SM: launch bounds 256 x 2, smem
             const int by_smem = std::max<int>(1, (int)((227 * 1024) / std::max<size_t>(wh.smem, 1)));
-            const int per_sm = std::max(1, std::min(2, by_smem));
+            const int per_sm = std::max(1, std::min(CTAS_PER_SM, by_smem));
             const double warps_per_smsp = per_sm * (NTW / 32) / 4.0;
             // issue efficiency saturates at ~4 resident warps per scheduler; TE = 5 (larger
             // code, measured slower on B200) is kept as a forced option (OOB_DP_WCFG=1)
@@ -388,7 +404,15 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
         items_total += align_up(wh.cb.size() * sizeof(int32_t), 16);
         gacc_max = std::max(gacc_max, (size_t)num_profiles * (L - l + 1) * wh.nout);
         wh.ctr_off = ctr_total;
-        ctr_total += (size_t)num_profiles * (L - l + 1);
+        ctr_total += 2 * (size_t)num_profiles * (L - l + 1);
+        // seeding pass: the balanced entries' units (~4% of the wave) fill the global
+        // accumulator first, so that the main pass's flush filter rarely passes
+        wh.seed_units = 0;
+        if (l >= 24 && pl->seed_pass) {
+            const int target = std::max(1, wh.nunits / 25);
+            for (int e = 0; e < wh.nents && wh.seed_units < target; ++e) wh.seed_units = wh.upre[e + 1];
+            if (wh.seed_units >= wh.nunits) wh.seed_units = 0;
+        }
         pl->max_smem = std::max(pl->max_smem, wh.smem);
     }
     pl->ctr_n = ctr_total;
@@ -403,6 +427,8 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     }
     // k_base + k_extract; v1: one kernel per wave; v6: k_fin(1) + (k_wave_w, k_fin) per wave
     pl->launches = 2 + (pl->kernel == 1 ? (L - 1) : 1 + 2 * (L - 1));
+    if (pl->kernel == 2)
+        for (int l = 2; l <= L; ++l) pl->launches += pl->waves[l].seed_units > 0 ? 1 : 0;
 
     size_t o = 0;
     pl->off_cells = o; o = align_up(o + sizeof(int32_t) * (L + 1), 256);
@@ -418,7 +444,7 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     pl->off_ARG = o; o = align_up(o + 4 * n, 256);
     pl->off_STK = o; o = align_up(o + 8 * (size_t)num_profiles * (n_hi - n_lo + 1) * (L + 1), 256);
     pl->gacc_n = (int64_t)gacc_max;
-    pl->off_GACC = o; o = align_up(o + 16 * gacc_max, 256);
+    pl->off_GACC = o; o = align_up(o + 2 * 16 * gacc_max, 256);   // two parity buffers
     pl->off_CTR = o; o = align_up(o + 4 * pl->ctr_n + 4, 256);
     pl->ws_bytes = o;
     pl->tpl_bytes = packed_template_bytes(L);
@@ -499,6 +525,12 @@ extern "C" oob_status oob_dp_kernel_time(oob_dp_plan *pl, double *ms_out, int64_
 }
 
 // k_fin: W winners of wave lw (lw >= 2, else none) + small cells of wave ls (0: none).
+// accumulator of wave l: two parity buffers (k_fin finalizes wave l-1 from one while it
+// seeds wave l into the other)
+static ulonglong2 *gacc_of(const oob_dp_plan *pl, ulonglong2 *gacc, int l) {
+    return gacc + (size_t)(l & 1) * (size_t)pl->gacc_n;
+}
+
 static cudaError_t launch_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglong2 *gacc, int lw, int ls,
                               cudaStream_t stream) {
     const Geometry &G = pl->g;
@@ -508,13 +540,19 @@ static cudaError_t launch_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglon
     f.nout_w = lw ? pl->waves[lw].nout : 0;
     const int64_t nw = (int64_t)pl->P * f.nranges_w * f.nout_w;
     f.nbw = (int)((nw + 255) / 256);
-    f.GACC = gacc;
+    f.GACC = gacc_of(pl, gacc, lw);
+    // seeds for wave ls (children of length <= ls-2: final before this launch)
+    f.lseed = (ls >= SEED_MIN_L && pl->seed_init) ? ls : 0;
+    f.nout_s = f.lseed ? pl->waves[ls].nout : 0;
+    const int64_t nsd = f.lseed ? (int64_t)pl->P * (G.L - ls + 1) * f.nout_s : 0;
+    f.nbseed = (int)((nsd + 255) / 256);
+    f.GSEED = gacc_of(pl, gacc, ls);
     f.ls = ls;
     f.nsmall = ls ? small_cells(G, ls) : 0;
     f.tpc = ls ? small_tpc(G, ls) : 32;
     const int64_t ns = ls ? (int64_t)pl->P * (G.L - ls + 1) * f.nsmall : 0;
     const int64_t nbs = (ns + (256 / f.tpc) - 1) / (256 / f.tpc);
-    const int64_t blocks = f.nbw + nbs;
+    const int64_t blocks = f.nbw + f.nbseed + nbs;
     if (blocks == 0) return cudaSuccess;
     k_fin<<<(unsigned)blocks, 256, 0, stream>>>(dg, f);
     return cudaGetLastError();
@@ -572,7 +610,7 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
     ulonglong2 *gacc = (ulonglong2 *)(ws + pl->off_GACC);
     if (pl->kernel == 2) {
         if (pl->gacc_ready != d_ws && pl->gacc_n > 0) {   // finalize resets what it reads
-            k_gacc_init<<<(unsigned)((pl->gacc_n + 255) / 256), 256, 0, stream>>>(gacc, pl->gacc_n);
+            k_gacc_init<<<(unsigned)((2 * pl->gacc_n + 255) / 256), 256, 0, stream>>>(gacc, 2 * pl->gacc_n);
             e = cudaGetLastError();
             if (e != cudaSuccess) return cuda_fail(e, "k_gacc_init launch");
             pl->gacc_ready = d_ws;
@@ -604,17 +642,32 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
         w.cb = (const int32_t *)(ws + pl->off_items + wh.cb_off);
         w.ctr = (int *)(ws + pl->off_CTR) + wh.ctr_off;
         w.nout = wh.nout;
-        w.GACC = gacc;
+        w.GACC = gacc_of(pl, gacc, l);
         w.tile_off = (const int32_t *)(ws + pl->off_tile_off) + (size_t)(G.L + 1) * te_index(WCFGS[wh.cfg].te);
         w.tile_cnt = (const int32_t *)(ws + pl->off_tile_cnt) + (size_t)(G.L + 1) * te_index(WCFGS[wh.cfg].te);
         w.tiles = (const int32_t *)(ws + pl->off_tiles);
         const int64_t ctas = wh.nents > 0 ? (int64_t)pl->P * w.nranges * w.cpr : 0;
         if (pl->timing) cudaEventRecord(pl->ev[pl->ev_used], stream);
         if (ctas > 0) {
-            if (WCFGS[wh.cfg].te == 4)
-                k_wave_w<4><<<(unsigned)ctas, NTW, wh.smem, stream>>>(dg, w);
-            else
-                k_wave_w<5><<<(unsigned)ctas, NTW, wh.smem, stream>>>(dg, w);
+            // pass 1 (optional): the seeding units; pass 2: the rest, from the seeded minima
+            for (int pass = wh.seed_units > 0 ? 0 : 1; pass < 2; ++pass) {
+                w.unit_lo = pass == 0 ? 0 : wh.seed_units;
+                w.unit_hi = pass == 0 ? wh.seed_units : wh.nunits;
+                w.seeded = (pass == 1 && wh.seed_units > 0) || (l >= SEED_MIN_L && pl->seed_init);
+                w.ctr = (int *)(ws + pl->off_CTR) + wh.ctr_off + (size_t)pass * pl->P * w.nranges;
+                w.perm_a = 1;
+                w.rev_lanes = pl->rev_lanes;
+                if (pl->perm_order) {   // a multiplier near n * 0.618 coprime to n
+                    const long long n = w.unit_hi - w.unit_lo;
+                    long long a = std::max<long long>(2, (long long)(n * 0.6180339887));
+                    while (n > 2 && std::gcd(a, n) != 1) ++a;
+                    w.perm_a = n > 2 ? a : 1;
+                }
+                if (WCFGS[wh.cfg].te == 4)
+                    k_wave_w<4><<<(unsigned)ctas, NTW, wh.smem, stream>>>(dg, w);
+                else
+                    k_wave_w<5><<<(unsigned)ctas, NTW, wh.smem, stream>>>(dg, w);
+            }
         }
         if (pl->timing) { cudaEventRecord(pl->ev[pl->ev_used + 1], stream); pl->ev_used += 2; }
         e = cudaGetLastError();
@@ -629,4 +682,14 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
         if (e != cudaSuccess) return cuda_fail(e, "k_extract launch");
     }
     return OOB_OK;
+}
+
+// Diagnostic (not part of the C ABI header): enable/read the flush counters of k_wave_w.
+extern "C" int oob_dbg_flush_stats(int enable, unsigned long long *out4) {
+    if (out4) {
+        if (cudaMemcpyFromSymbol(out4, oob::g_flush_stats, sizeof(unsigned long long) * 4) != cudaSuccess) return 1;
+    }
+    unsigned long long z[4] = {0, 0, 0, 0};
+    if (cudaMemcpyToSymbol(oob::g_flush_stats, z, sizeof(z)) != cudaSuccess) return 1;
+    return cudaMemcpyToSymbol(oob::g_flush_stats_on, &enable, sizeof(int)) == cudaSuccess ? 0 : 1;
 }

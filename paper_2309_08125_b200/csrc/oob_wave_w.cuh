@@ -49,7 +49,11 @@ struct WaveW {
     const int4 *ents;      // per entry: (l1, nblocks, nchunks, chunk_off)
     const int32_t *upre;   // [nents + 1] unit prefix: entry e owns units [upre[e], upre[e+1])
     const int32_t *cb;     // chunk row boundaries: rows [cb[off+c], cb[off+c+1])
-    int *ctr;              // [P][nranges] unit counters (zeroed before the launch)
+    int *ctr;              // [P][nranges] unit counters of this pass (zeroed before the launch)
+    int unit_lo, unit_hi;  // this pass processes queue units [unit_lo, unit_hi)
+    int seeded;            // 1: start from the global accumulator (an earlier pass's minima)
+    long long perm_a;      // > 1: unit order permutation multiplier (coprime to the pass's unit count)
+    int rev_lanes;         // 1: lane i holds the block's tile 31 - i (diagnostic)
     int nout;              // W-part cells of a slab of length l (W(1)..W(Q_l))
     ulonglong2 *GACC;      // global accumulator [P][nranges][nout]: {total bits, key}
     const int32_t *tile_off;   // [L+1] offset of the flat tile list of a big side of length lb
@@ -150,11 +154,22 @@ __device__ __forceinline__ int c_ipart(int M, int l) {
 // does the lane read the 16-byte entry and run the lexicographic CAS loop (entries only
 // decrease, so a stale read is an upper bound and the loop stays exact), then lower the
 // filter.  Dummy entries have filter 0 (nothing passes); +inf / NaN never pass ACC_EMPTY.
+// diagnostic counters (flush tests passed, CAS successes): compiled in with -DOOB_FLUSH_STATS
+// (scripts/flush_stats.py), enabled by oob_dbg_flush_stats
+__device__ unsigned long long g_flush_stats[4];
+__device__ int g_flush_stats_on;
+
 __device__ __forceinline__ void acc_flush(unsigned acc_s, unsigned filt_s, int idx, double b, uint32_t key) {
     const unsigned bh = (unsigned)__double2hiint(b);
     unsigned fh;
     asm("ld.shared.u32 %0, [%1];" : "=r"(fh) : "r"(filt_s + 4u * (unsigned)idx));
     if (bh <= fh) {
+#ifdef OOB_FLUSH_STATS
+        if (g_flush_stats_on) {
+            atomicAdd(&g_flush_stats[0], 1ull);
+            if (bh < fh) atomicAdd(&g_flush_stats[2], 1ull);
+        }
+#endif
         const unsigned addr = acc_s + 16u * (unsigned)idx;
         const unsigned long long bb = (unsigned long long)__double_as_longlong(b);
         unsigned long long cx, cy;
@@ -163,6 +178,9 @@ __device__ __forceinline__ void acc_flush(unsigned acc_s, unsigned filt_s, int i
             unsigned long long ox, oy;
             cas128_shared(addr, ox, oy, cx, cy, bb, (unsigned long long)key);
             if (ox == cx && oy == cy) {
+#ifdef OOB_FLUSH_STATS
+                if (g_flush_stats_on) atomicAdd(&g_flush_stats[1], 1ull);
+#endif
                 asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(filt_s + 4u * (unsigned)idx), "r"(bh) : "memory");
                 break;
             }
@@ -274,10 +292,13 @@ __global__ void __launch_bounds__(NTW, 2) k_wave_w(DevGeom g, WaveW w) {
     const int64_t pc = (int64_t)p * g.C;
     const int Ql = (l == L) ? g.n_hi : max(1, g.n_hi - 1);
 
+    const ulonglong2 *gseed = w.GACC + ((size_t)(blockIdx.x / w.cpr)) * nout;   // this range's entries
     for (int i = tid; i < nout + ndum; i += NTW) {
         const bool real = i < nout;
-        acc[i] = real ? make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull) : make_ulonglong2(0ull, 0ull);
-        filt[i] = real ? (unsigned)(ACC_EMPTY >> 32) : 0u;
+        ulonglong2 a = real ? make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull) : make_ulonglong2(0ull, 0ull);
+        if (real && w.seeded) a = __ldcg(gseed + i);
+        acc[i] = a;
+        filt[i] = real ? (unsigned)(a.x >> 32) : 0u;
     }
     for (int i = tid; i < L + 2; i += NTW) {
         sbase[i] = g.base[i];
@@ -289,16 +310,18 @@ __global__ void __launch_bounds__(NTW, 2) k_wave_w(DevGeom g, WaveW w) {
         if (i < w.nents) sents[i] = w.ents[i];
     }
     __syncthreads();
-    const int nunits = upre[w.nents];
+    const int nunits = w.unit_hi;
     const unsigned acc_s = (unsigned)__cvta_generic_to_shared(acc);
     const unsigned filt_s = (unsigned)__cvta_generic_to_shared(filt);
     int *gctr = w.ctr + pr;
 
     for (;;) {
         int un = 0;
-        if (lane == 0) un = atomicAdd(gctr, 1);
+        if (lane == 0) un = w.unit_lo + atomicAdd(gctr, 1);
         un = __shfl_sync(0xFFFFFFFFu, un, 0);
         if (un >= nunits) break;
+        if (w.perm_a > 1)    // visit the queue in a pseudo-random order (a permutation of the pass's units)
+            un = w.unit_lo + (int)(((long long)(un - w.unit_lo) * w.perm_a) % (nunits - w.unit_lo));
         int lo = 0, hi = w.nents - 1;                // entry: upre[ei] <= un < upre[ei+1]
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
@@ -306,21 +329,19 @@ __global__ void __launch_bounds__(NTW, 2) k_wave_w(DevGeom g, WaveW w) {
         }
         const int ei = lo;
         const int4 en = sents[ei];
-        const int l1 = en.x;
+        const int l1 = en.x & 0xFFFF;
         const int local = un - upre[ei];
         const int chunk = local / en.y;
         const int blk = local % en.y;
         const int r_lo = w.cb[en.w + chunk], r_hi = w.cb[en.w + chunk + 1];
         const int k = u + l1;
         const int l2 = l - l1;
-        const int Q1 = (l1 == L) ? g.n_hi : max(1, g.n_hi - 1), Q2 = (l2 == L) ? g.n_hi : max(1, g.n_hi - 1);
-        const int wc1 = c_woff(M, l1, min(Q1, l1) + 1), wc2 = c_woff(M, l2, min(Q2, l2) + 1);
-        const bool ltiled = wc1 >= wc2;                             // big side = left
+        const bool ltiled = (en.x >> 16) & 1;                     // tiled side = left child
         const int ls = ltiled ? l2 : l1;                           // small side length
         const int lb = ltiled ? l1 : l2;
         const int us = ltiled ? k : u;                             // small slab start
         const int ub = ltiled ? u : k;
-        const int ti = blk * 32 + lane;
+        const int ti = blk * 32 + (w.rev_lanes ? 31 - lane : lane);
         const bool has = ti < w.tile_cnt[lb];
         const int32_t code = has ? w.tiles[w.tile_off[lb] + ti] : 0;
         const int rowB = has ? (code >> 16) : 1;
@@ -389,7 +410,9 @@ __global__ void k_gacc_init(ulonglong2 *gacc, int64_t n) {
 struct FinArgs {
     int lw, nranges_w, nout_w;     // W finalize of wave lw (lw = 0: none)
     int nbw;                       // blocks of the W part
-    ulonglong2 *GACC;
+    ulonglong2 *GACC;              // accumulator of wave lw
+    int lseed, nout_s, nbseed;     // seeds of wave lseed (0: none): W outputs per range, blocks
+    ulonglong2 *GSEED;             // accumulator of wave lseed (the other parity buffer)
     int ls, nsmall;                // small cells of wave ls (ls = 0: none); cells per range
     int tpc;                       // threads per small cell
 };
@@ -431,12 +454,71 @@ __global__ void __launch_bounds__(256) k_fin(DevGeom g, FinArgs f) {
         d_write_winner(g, pc, Sp, u, l, aW, l1, j - 1, s);
         return;
     }
+    if ((int)blockIdx.x < f.nbw + f.nbseed) {
+        // ---------------- seeds of wave lseed: per W(q >= 2) output (S', u, u+l, W(q)), the
+        // lexicographic minimum over a few proportional splits (j ~ q/2, s ~ S' j/q,
+        // l1 ~ l s/S'), evaluated exactly as k_wave_w evaluates them (split_total), so the
+        // accumulator starts near the optimum and the flush filter rarely passes.  Children
+        // come from waves <= l-2 (2 <= l1 <= l-2), all final when this kernel runs.
+        const int l = f.lseed;
+        const int nr = g.L - l + 1;
+        const int nout = f.nout_s;
+        const int64_t t = (int64_t)(blockIdx.x - f.nbw) * blockDim.x + threadIdx.x;
+        if (t >= (int64_t)g.P * nr * nout) return;
+        const int i = (int)(t % nout);
+        const int u = (int)((t / nout) % nr);
+        const int p = (int)(t / ((int64_t)nout * nr));
+        const int M = g.M;
+        const int Ql = (l == g.L) ? g.n_hi : max(1, g.n_hi - 1);
+        int lo = 1, hi = min(Ql, l);
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (c_woff(M, l, mid) <= i) lo = mid; else hi = mid - 1;
+        }
+        const int q = lo, Sp = q + (i - c_woff(M, l, q));
+        unsigned long long bb = ACC_EMPTY;
+        uint32_t bk = 0xFFFFFFFFu;
+        if (q >= 2) {
+            const int64_t pc = (int64_t)p * g.C;
+            const int Qc = max(1, g.n_hi - 1);                 // children are shorter than L
+            for (int jj = 0; jj < 2; ++jj) {
+                const int j = jj == 0 ? q / 2 : (q + 1) / 2;
+                if (jj == 1 && j == q / 2) continue;
+                const int jr = q - j;
+                if (j < 1 || jr < 1 || j > Qc || jr > Qc) continue;
+                for (int ss = 0; ss < 2; ++ss) {
+                    const int s = ss == 0 ? (Sp * j) / q : (Sp * j + q - 1) / q;
+                    if (ss == 1 && s == (Sp * j) / q) continue;
+                    const int sr = Sp - s;
+                    if (s < j || sr < jr || s > M * j || sr > M * jr) continue;
+                    for (int kk = 0; kk < 3; ++kk) {
+                        const int l1 = (l * s) / Sp + kk - 1;
+                        const int l2 = l - l1;
+                        if (l1 < 2 || l2 < 2 || s > l1 || sr > l2 || j > l1 || jr > l2) continue;
+                        const Cell4 *lc = g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + c_ipart(M, l1) +
+                                          c_woff(M, l1, j) + (s - j);
+                        const Cell4 *rc = g.CELL + pc + g.base[l2] + (int64_t)(u + l1) * g.cells[l2] +
+                                          c_ipart(M, l2) + c_woff(M, l2, jr) + (sr - jr);
+                        const Cell4 L = d_load(lc), R = d_load(rc);
+                        const double cL = __dadd_rn(L.C1, (double)(3 * sr));
+                        const double cR = __dadd_rn(R.C1, (double)(4 * s));
+                        const double tot = split_total(L.T1, L.T3, L.TS, cL, R.T1, R.T3, R.TS, cR);
+                        const unsigned long long tb = (unsigned long long)__double_as_longlong(tot);
+                        const uint32_t key = ((uint32_t)l1 << 20) | ((uint32_t)j << 10) | (uint32_t)s;
+                        if (lex_less(tb, key, bb, bk)) { bb = tb; bk = key; }
+                    }
+                }
+            }
+        }
+        __stcg(f.GSEED + t, make_ulonglong2(bb, (unsigned long long)bk));
+        return;
+    }
     // ---------------- small cells of wave ls
     const int l = f.ls;
     const int nr = g.L - l + 1;
     const int cpb = blockDim.x / f.tpc;                      // cells per block
     const int sub = threadIdx.x / f.tpc, tl = threadIdx.x % f.tpc;
-    const int64_t cell = (int64_t)(blockIdx.x - f.nbw) * cpb + sub;
+    const int64_t cell = (int64_t)(blockIdx.x - f.nbw - f.nbseed) * cpb + sub;
     const bool active = cell < (int64_t)g.P * nr * f.nsmall;
     double best = D_INF;
     uint32_t bkey = 0xFFFFFFFFu;
