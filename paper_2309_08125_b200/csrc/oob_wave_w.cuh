@@ -510,6 +510,43 @@ __global__ void __launch_bounds__(256) k_fin(DevGeom g, FinArgs f) {
                 }
             }
         }
+        // warm start: the argmin splits (l1', j', s') of the same output (q, S') on the two
+        // length-(l-2) sub-ranges [u, u+l-2) and [u+2, u+l), shifted to [u, u+l)
+        if (q >= 2 && l >= 8) {
+            const int64_t pc = (int64_t)p * g.C;
+            const int lp = l - 2;
+            const int Qp = max(1, g.n_hi - 1);
+            if (q <= Qp && q <= lp && Sp <= min(lp, M * q)) {
+#pragma unroll 1
+                for (int side = 0; side < 2; ++side) {
+                    const int up = u + 2 * side;
+                    const uint32_t arg = g.ARG[pc + g.base[lp] + (int64_t)up * g.cells[lp] + c_ipart(M, lp) +
+                                               c_woff(M, lp, q) + (Sp - q)];
+                    if (arg >= 0xFFFFFFFEu) continue;
+                    const int l1p = (int)(arg & 1023u) + 1 + 2 * side, j = (int)((arg >> 10) & 1023u) + 1;
+                    const int s = (int)(arg >> 20);
+                    const int jr = q - j, sr = Sp - s;
+#pragma unroll 1
+                    for (int d = 0; d < 3; ++d) {
+                        const int l1 = l1p + d - side;   // shifts 0..2 (left range) / 1..3 - 1 (right)
+                        const int l2 = l - l1;
+                        if (l1 < 2 || l2 < 2 || s > l1 || sr > l2 || j > l1 || jr > l2 || jr < 1) continue;
+                        const Cell4 *lc = g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + c_ipart(M, l1) +
+                                          c_woff(M, l1, j) + (s - j);
+                        const Cell4 *rc = g.CELL + pc + g.base[l2] + (int64_t)(u + l1) * g.cells[l2] +
+                                          c_ipart(M, l2) + c_woff(M, l2, jr) + (sr - jr);
+                        if (s < j || sr < jr || s > M * j || sr > M * jr) continue;
+                        const Cell4 Lc = d_load(lc), Rc = d_load(rc);
+                        const double cL = __dadd_rn(Lc.C1, (double)(3 * sr));
+                        const double cR = __dadd_rn(Rc.C1, (double)(4 * s));
+                        const double tot = split_total(Lc.T1, Lc.T3, Lc.TS, cL, Rc.T1, Rc.T3, Rc.TS, cR);
+                        const unsigned long long tb = (unsigned long long)__double_as_longlong(tot);
+                        const uint32_t key = ((uint32_t)l1 << 20) | ((uint32_t)j << 10) | (uint32_t)s;
+                        if (lex_less(tb, key, bb, bk)) { bb = tb; bk = key; }
+                    }
+                }
+            }
+        }
         __stcg(f.GSEED + t, make_ulonglong2(bb, (unsigned long long)bk));
         return;
     }
