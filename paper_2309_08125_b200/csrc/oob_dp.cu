@@ -157,6 +157,11 @@ __global__ void k_extract(DevGeom g, unsigned char *packed, size_t tpl_bytes) {
         const int k = u + (int)(arg & 1023u) + 1;
         const int j = (int)((arg >> 10) & 1023u);
         const int s = (int)(arg >> 20);
+        if (arg >= 0xFFFFFFFDu || k <= u || k >= v || s < 1 || s >= Sp || j >= d_num_dsplits(g, a) ||
+            top + 2 > L + 1) {   // corrupt split (never for a valid table): flag the template, stop
+            h->status = 1;
+            break;
+        }
         int a1, a2;
         d_dsplit(g, a, j, a1, a2);
         const bool wsplit = d_is_whole(g, a) && d_alloc_n(g, a) >= 2;

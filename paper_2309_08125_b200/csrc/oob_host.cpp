@@ -280,7 +280,7 @@ extern "C" oob_status oob_template_set_from_packed(const void *h_packed, const o
             const size_t t = (size_t)pr * p + i;
             const PackedHeader *h = (const PackedHeader *)(base + t * info->packed_template_bytes);
             const int32_t *st = (const int32_t *)(h + 1);
-            if (h->S < 1 || h->S > info->L) {
+            if (h->S < 1 || h->S > info->L || h->status != 0) {
                 delete s;
                 return fail(OOB_E_CUDA, "corrupt packed template (profile " + std::to_string(pr) + ", i " + std::to_string(i) + ")");
             }

@@ -451,6 +451,15 @@ __global__ void __launch_bounds__(256) k_fin(DevGeom g, FinArgs f) {
         }
         const uint32_t key = (uint32_t)a.y;
         const int l1 = (int)(key >> 20), j = (int)((key >> 10) & 1023u), s = (int)(key & 1023u);
+        // bounds check of the decoded split (a corrupt key must not read outside the table)
+        const int l2 = l - l1, jr = q - j, sr = Sp - s;
+        if (l1 < 1 || l2 < 1 || j < 1 || jr < 1 || s < j || sr < jr || s > min(l1, g.M * j) ||
+            sr > min(l2, g.M * jr)) {
+            const int64_t c = pc + d_cell(g, Sp, u, l, aW);
+            g.CELL[c].T1 = __longlong_as_double(0x7ff8000000000000LL);
+            g.ARG[c] = 0xFFFFFFFDu;
+            return;
+        }
         d_write_winner(g, pc, Sp, u, l, aW, l1, j - 1, s);
         return;
     }

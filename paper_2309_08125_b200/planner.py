@@ -60,7 +60,7 @@ class Profile:
         return out.value
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib.oob_profile_free(self._h)
             self._h = None
 
@@ -104,7 +104,7 @@ class TemplateSet:
         return [self.get(profile, i) for i in range(self.count(profile))]
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib.oob_template_set_free(self._h)
             self._h = None
 
@@ -158,7 +158,7 @@ class DPPlan:
         return TemplateSet(h)
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib.oob_dp_plan_free(self._h)
             self._h = None
 
