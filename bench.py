@@ -157,6 +157,8 @@ def main():
     ap.add_argument("--profiles-per-rank", type=int, default=0,
                     help="profiles per rank (default: 1; cfg5: 1024/N)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard-profile", action="store_true",
+                    help="N > 1: all ranks plan ONE profile, wavefronts split across GPUs (strong scaling)")
     ap.add_argument("--ref-sample-sizes", type=int, default=5,
                     help="reference arm / cpu_baseline: number of template sizes in the sample")
     args = ap.parse_args()
@@ -192,9 +194,15 @@ def main():
     else:
         P = args.profiles_per_rank or 1
         from workloads import gpt_profile
-        profs = [gpt_profile(cfg, cfg.seed + 1000 * (rank * P + i)) for i in range(P)]
+        seed_rank = 0 if args.shard_profile else rank
+        profs = [gpt_profile(cfg, cfg.seed + 1000 * (seed_rank * P + i)) for i in range(P)]
 
+    shard = args.shard_profile and world > 1 and cfg.key != "cfg5"
     plan = planner.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, P)
+    comm = None
+    if shard:   # single-profile wavefront sharding: NCCL all-gather of partial argmins per wavefront
+        comm = planner.NcclComm(world, rank, local)
+        plan.set_comm(comm)
     info = plan.info
     dev = torch.device("cuda", local)
     fwd = torch.tensor(np.stack([p.fwd_ms for p in profs]), dtype=torch.float64, device=dev)
@@ -207,7 +215,7 @@ def main():
 
     def step():
         plan.run(fwd.data_ptr(), bwd.data_ptr(), ws.data_ptr(), ws.numel(), packed.data_ptr(), sptr)
-        if world > 1:   # one NCCL all-gather assembles every rank's packed template sets
+        if world > 1 and not shard:   # one NCCL all-gather assembles every rank's packed template sets
             odist.allgather_packed(packed, info.packed_bytes)
 
     for _ in range(args.warmup):
@@ -237,18 +245,23 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms, kern_ms_max = float(t[0]), float(t[1])
     ms_per_step = total_ms / args.steps
-    cells_step = info.cells_per_profile * P * world
+    units = P * (1 if shard else world)       # profiles planned per step by the whole job
+    cells_step = info.cells_per_profile * units
     # cfg5 default: the fixed 1024-profile sweep is split across ranks (strong scaling);
-    # otherwise every rank plans its own profile(s) of the workload's shape (weak scaling)
-    scaling = "strong" if (cfg.key == "cfg5" and not args.profiles_per_rank) else "weak"
-    splits_step = info.splits_per_profile * P * world
+    # --shard-profile: one profile split across ranks (strong); otherwise every rank plans
+    # its own profile(s) of the workload's shape (weak scaling)
+    scaling = "strong" if ((cfg.key == "cfg5" and not args.profiles_per_rank) or shard) else "weak"
+    splits_step = info.splits_per_profile * units
     value = cells_step / (ms_per_step / 1e3)
 
     # roofline of the dominant kernel (the wavefront DP kernel): FP64 pipe
     clocks = clk.summary()
     sm_max = clocks.get("sm_max_mhz") or _peaks().get("sm_max_mhz", 1965.0)
     kern_ms_per_step = kern_ms / args.steps
-    achieved = info.splits_per_profile * P * FP64_PER_SPLIT / (kern_ms_per_step / 1e3) / 1e12
+    # per-rank algorithmic work (sharded: ~1/world of the splits; short wavefronts are
+    # replicated, so this slightly under-counts the rank's work)
+    rank_splits = info.splits_per_profile * P / (world if shard else 1)
+    achieved = rank_splits * FP64_PER_SPLIT / (kern_ms_per_step / 1e3) / 1e12
     peak = SMS * FP64_LANES_PER_SM * sm_max * 1e6 / 1e12
     traffic = None
     try:   # DRAM bytes per launch of the dominant kernel, from the committed ncu capture
@@ -270,7 +283,15 @@ def main():
     e2e_ws = torch.empty(info.workspace_bytes + (4 << 20) + info.packed_bytes + 2 * 8 * cfg.L * cfg.M * P + (1 << 20),
                          dtype=torch.uint8, device=dev)
 
+    h_fwd = torch.from_numpy(np.stack([p.fwd_ms for p in profs])).pin_memory()
+    h_bwd = torch.from_numpy(np.stack([p.bwd_ms for p in profs])).pin_memory()
+
     def e2e_step():
+        if shard:   # public DPPlan API: pinned H2D, sharded DP, D2H + host template set
+            fwd.copy_(h_fwd, non_blocking=True)
+            bwd.copy_(h_bwd, non_blocking=True)
+            plan.run(fwd.data_ptr(), bwd.data_ptr(), ws.data_ptr(), ws.numel(), packed.data_ptr(), sptr)
+            return plan.template_set(packed.cpu().numpy())
         ts = planner.generate_templates(hprofs, nodes=cfg.N, gpus_per_node=cfg.M, f=cfg.f, n0=cfg.n0,
                                         device=local, stream=sptr, workspace=e2e_ws.data_ptr(),
                                         workspace_bytes=e2e_ws.numel())
@@ -320,8 +341,11 @@ def main():
                            "f": cfg.f, "n0": cfg.n0, "sizes": [cfg.n0, cfg.n_max], "profiles_per_rank": P,
                            "cells_per_step": cells_step, "splits_per_step": splits_step,
                            "l2": "flushed (256 MiB write) before every timed step",
-                           "parallelism": f"independent template DPs, {P} profile(s) per rank x {world} rank(s)"
-                                          + (", NCCL all-gather of packed template sets" if world > 1 else "")},
+                           "parallelism": (f"one profile, wavefronts sharded over {world} GPUs (NCCL all-gather of "
+                                           f"partial argmins per wavefront)") if shard else
+                                          f"independent template DPs, {P} profile(s) per rank x {world} rank(s)"
+                                          + (", NCCL all-gather of packed template sets" if world > 1 and not shard
+                                             else "")},
                 "splits_per_s": splits_step / (ms_per_step / 1e3),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "full_plan_latency_ms": {"templates_e2e": e2e_s * 1e3, "instantiate_N_capped_1e4": inst_ms,

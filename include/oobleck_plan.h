@@ -42,7 +42,7 @@ typedef enum {
     OOB_E_BATCH = 4,       /* B % b != 0 or B/b < pipelines; see recommended */
     OOB_E_TOO_MANY = 5,    /* Eq.5 enumeration exceeded max_enumerated (plan is best-so-far) */
     OOB_E_CUDA = 6,        /* CUDA runtime/launch failure */
-    OOB_E_NCCL = 7,        /* reserved: collective failure */
+    OOB_E_NCCL = 7,        /* collective failure (oob_nccl_*, oob_dp_run with a communicator) */
     OOB_E_NOMEM = 8        /* host allocation or workspace too small */
 } oob_status;
 
@@ -161,6 +161,26 @@ oob_status oob_dp_run(oob_dp_plan *plan, const double *d_fwd, const double *d_bw
 oob_status oob_dp_set_timing(oob_dp_plan *plan, int32_t enable);
 oob_status oob_dp_kernel_time(oob_dp_plan *plan, double *ms_out, int64_t *launches_out,
                               int32_t reset);
+/* ------------------------------------------------------------------ multi-GPU (one profile)
+ * Single-profile sharding across `world` GPUs of one box: every rank calls
+ * oob_dp_run on the same profile with the same plan geometry; the W-cell splits of every
+ * wavefront are divided across ranks (rank r takes units r, r+world, ... of each range's
+ * unit queue) and one ncclAllGather of the per-rank partial argmins per wavefront (16 bytes
+ * per output) lets every rank finalize the whole wavefront, so every rank ends with the same
+ * table and packed templates (bit-identical to world = 1).
+ *   oob_nccl_unique_id : rank 0 creates the id (OOB_NCCL_ID_BYTES bytes), the caller
+ *                        broadcasts it (e.g. torch.distributed);
+ *   oob_nccl_comm_create: every rank, on its CUDA device (`device` < 0: current);
+ *   oob_dp_set_comm    : attach the communicator to a plan (comm = NULL, world = 1: detach);
+ *                        the plan's workspace grows by world x (largest wavefront partial):
+ *                        re-read oob_dp_plan_info afterwards.  The communicator is borrowed.
+ * Errors: OOB_E_INVALID, OOB_E_NCCL, OOB_E_CUDA. */
+#define OOB_NCCL_ID_BYTES 128
+oob_status oob_nccl_unique_id(void *id_out);
+oob_status oob_nccl_comm_create(const void *id, int32_t world, int32_t rank, int32_t device, void **comm_out);
+void oob_nccl_comm_destroy(void *comm);
+oob_status oob_dp_set_comm(oob_dp_plan *plan, void *comm, int32_t world, int32_t rank);
+
 /* Build a template set from a HOST copy of the packed output (d_packed copied back). */
 oob_status oob_template_set_from_packed(const void *h_packed, const oob_dp_info *info,
                                         oob_template_set **out);

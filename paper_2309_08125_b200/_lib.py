@@ -83,6 +83,10 @@ _proto("oob_dp_run", ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_si
 _proto("oob_dp_set_timing", ctypes.c_int, [c_void_p, c_int32])
 _proto("oob_dp_kernel_time", ctypes.c_int, [c_void_p, P(c_double), P(c_int64), c_int32])
 _proto("oob_template_set_from_packed", ctypes.c_int, [c_void_p, P(OobDpInfo), P(c_void_p)])
+_proto("oob_nccl_unique_id", ctypes.c_int, [c_void_p])
+_proto("oob_nccl_comm_create", ctypes.c_int, [c_void_p, c_int32, c_int32, c_int32, P(c_void_p)])
+_proto("oob_nccl_comm_destroy", None, [c_void_p])
+_proto("oob_dp_set_comm", ctypes.c_int, [c_void_p, c_void_p, c_int32, c_int32])
 _proto("oob_instantiate", ctypes.c_int, [c_void_p, c_int32, c_int32, c_int32, c_int64, c_int32, c_int64,
                                          c_void_p, c_void_p, c_int32, P(c_int32), P(c_double), P(c_double),
                                          P(c_int64), P(c_int64)])
@@ -98,8 +102,10 @@ EXPORTED = [
     "oob_template_get", "oob_template_set_free", "oob_dp_plan_create", "oob_dp_plan_free",
     "oob_dp_plan_info", "oob_dp_run", "oob_dp_set_timing", "oob_dp_kernel_time",
     "oob_template_set_from_packed", "oob_instantiate", "oob_count_sets", "oob_distribute_batch",
-    "oob_recommend_batch",
+    "oob_recommend_batch", "oob_nccl_unique_id", "oob_nccl_comm_create", "oob_nccl_comm_destroy",
+    "oob_dp_set_comm",
 ]
+NCCL_ID_BYTES = 128
 
 
 class OobError(RuntimeError):

@@ -18,8 +18,22 @@ LIB = os.path.join(PKG, "liboobleck_plan.so")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
+
+def _nccl_dir() -> str:
+    """NCCL shipped with the torch wheel (site-packages/nvidia/nccl): headers + libnccl.so.2."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (list(spec.submodule_search_locations) if spec else []):
+        d = os.path.join(base, "nccl")
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    raise RuntimeError("NCCL headers not found (site-packages/nvidia/nccl)")
+
+
+NCCL = _nccl_dir()
+
 CU_SOURCES = ["oob_dp.cu"]
-CPP_SOURCES = ["oob_host.cpp", "oob_geometry.cpp", "oob_instantiate.cpp"]
+CPP_SOURCES = ["oob_host.cpp", "oob_geometry.cpp", "oob_instantiate.cpp", "oob_dist.cpp"]
 HEADERS = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".h", ".cuh"))] + \
     [os.path.join(INC, "oobleck_plan.h")]
 
@@ -28,7 +42,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 if os.environ.get("OOB_FLUSH_STATS"):          # diagnostic build (scripts/flush_stats.py)
     NVCC_FLAGS += ["-DOOB_FLUSH_STATS"]
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall",
-             "-I", INC, "-I", CSRC, "-I", os.path.join(CUDA, "include")]
+             "-I", INC, "-I", CSRC, "-I", os.path.join(CUDA, "include"), "-I", os.path.join(NCCL, "include")]
 
 
 def _stale(obj: str, src: str) -> bool:
@@ -64,8 +78,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
             _run(["g++"] + CXX_FLAGS + ["-c", s, "-o", o], log)
         objs.append(o)
     if force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        _run([NVCC, "-shared", "-o", LIB] + objs + ["-cudart", "static", "-gencode",
-                                                     "arch=compute_100a,code=sm_100a"], log)
+        nlib = os.path.join(NCCL, "lib")
+        _run([NVCC, "-shared", "-o", LIB] + objs + ["-cudart", "static", "-gencode", "arch=compute_100a,code=sm_100a",
+                                                     "-L", nlib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + nlib], log)
     if verbose:
         print("\n".join(x for x in log if x.strip()))
     return LIB

@@ -186,6 +186,7 @@ namespace {
 // k_wave_w launch configurations: (TE cells per lane tile, threads per CTA)
 struct WCfg { int te, nt; };
 constexpr WCfg WCFGS[] = {{4, NTW}, {5, NTW}};
+constexpr double SHARD_MIN_SPLITS = 2e7;   // wavefronts sharded across ranks (oob_dp_set_comm)
 constexpr int SEED_MIN_L = 6;      // waves seeded with proportional splits (k_fin)
 constexpr int CTAS_PER_SM = 512 / NTW;   // k_wave_w: 16 resident warps per SM (register bound: 128 regs)
 constexpr int NWCFG = 2;
@@ -232,6 +233,10 @@ struct oob_dp_plan {
            off_items = 0;
     size_t off_CELL = 0, off_ARG = 0, off_STK = 0, off_GACC = 0, off_CTR = 0;
     int64_t gacc_n = 0;
+    void *comm = nullptr;                // ncclComm_t (single-profile sharding), world > 1
+    int rank = 0, world = 1;
+    size_t off_GPART = 0;                // [world][wave partial] gathered partial accumulators
+    size_t ws_bytes_base = 0;
     size_t ctr_n = 0;
     std::vector<int32_t> tiles;          // all TE's tables concatenated
     TileTab tab[2];                      // TE = 4, TE = 5
@@ -451,6 +456,7 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     pl->gacc_n = (int64_t)gacc_max;
     pl->off_GACC = o; o = align_up(o + 2 * 16 * gacc_max, 256);   // two parity buffers
     pl->off_CTR = o; o = align_up(o + 4 * pl->ctr_n + 4, 256);
+    pl->ws_bytes_base = o;
     pl->ws_bytes = o;
     pl->tpl_bytes = packed_template_bytes(L);
     pl->geom_blob.assign(pl->geom_bytes, 0);
@@ -498,6 +504,19 @@ extern "C" oob_status oob_dp_plan_info(const oob_dp_plan *pl, oob_dp_info *out) 
     return OOB_OK;
 }
 
+extern "C" oob_status oob_dp_set_comm(oob_dp_plan *pl, void *comm, int32_t world, int32_t rank) {
+    if (!pl || world < 1 || rank < 0 || rank >= world || (world > 1 && !comm))
+        return fail(OOB_E_INVALID, "oob_dp_set_comm: bad argument");
+    if (world > 1 && pl->kernel != 2)
+        return fail(OOB_E_INVALID, "oob_dp_set_comm: sharding needs the W-kernel path");
+    pl->comm = world > 1 ? comm : nullptr;
+    pl->world = world;
+    pl->rank = world > 1 ? rank : 0;
+    pl->off_GPART = pl->ws_bytes_base;
+    pl->ws_bytes = pl->ws_bytes_base + (world > 1 ? align_up(16 * (size_t)world * pl->gacc_n, 256) : 0);
+    return OOB_OK;
+}
+
 extern "C" oob_status oob_dp_set_timing(oob_dp_plan *pl, int32_t enable) {
     if (!pl) return fail(OOB_E_INVALID, "oob_dp_set_timing: NULL plan");
     pl->timing = enable ? 1 : 0;
@@ -537,7 +556,7 @@ static ulonglong2 *gacc_of(const oob_dp_plan *pl, ulonglong2 *gacc, int l) {
 }
 
 static cudaError_t launch_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglong2 *gacc, int lw, int ls,
-                              cudaStream_t stream) {
+                              cudaStream_t stream, bool sharded = false) {
     const Geometry &G = pl->g;
     FinArgs f;
     f.lw = lw;
@@ -546,6 +565,9 @@ static cudaError_t launch_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglon
     const int64_t nw = (int64_t)pl->P * f.nranges_w * f.nout_w;
     f.nbw = (int)((nw + 255) / 256);
     f.GACC = gacc_of(pl, gacc, lw);
+    f.world = sharded ? pl->world : 1;
+    f.part_stride = (int64_t)pl->P * f.nranges_w * f.nout_w;   // all-gather: rank r at r x (wave partial)
+    f.GPART = (const ulonglong2 *)((const unsigned char *)dg.CELL - pl->off_CELL + pl->off_GPART);
     // seeds for wave ls (children of length <= ls-2: final before this launch)
     f.lseed = (ls >= SEED_MIN_L && pl->seed_init) ? ls : 0;
     f.nout_s = f.lseed ? pl->waves[ls].nout : 0;
@@ -651,6 +673,11 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
         w.tile_off = (const int32_t *)(ws + pl->off_tile_off) + (size_t)(G.L + 1) * te_index(WCFGS[wh.cfg].te);
         w.tile_cnt = (const int32_t *)(ws + pl->off_tile_cnt) + (size_t)(G.L + 1) * te_index(WCFGS[wh.cfg].te);
         w.tiles = (const int32_t *)(ws + pl->off_tiles);
+        // shard only wavefronts whose work outweighs the all-gather (~10-20 us on NVLink);
+        // short wavefronts run redundantly on every rank (identical results, no exchange)
+        const bool shard = pl->world > 1 && (double)G.wave_splits[l] * pl->P >= SHARD_MIN_SPLITS;
+        w.rank = shard ? pl->rank : 0;
+        w.world = shard ? pl->world : 1;
         const int64_t ctas = wh.nents > 0 ? (int64_t)pl->P * w.nranges * w.cpr : 0;
         if (pl->timing) cudaEventRecord(pl->ev[pl->ev_used], stream);
         if (ctas > 0) {
@@ -677,7 +704,13 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
         if (pl->timing) { cudaEventRecord(pl->ev[pl->ev_used + 1], stream); pl->ev_used += 2; }
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "k_wave_w launch");
-        if ((e = launch_fin(pl, dg, gacc, l, l < G.L ? l + 1 : 0, stream)) != cudaSuccess)
+        if (shard) {   // one all-gather of the wave's partial argmins (every rank finalizes all)
+            const size_t bytes = 16 * (size_t)pl->P * w.nranges * w.nout;
+            oob_status st = nccl_allgather_bytes(pl->comm, gacc_of(pl, gacc, l), ws + pl->off_GPART,
+                                                 bytes, 16 * (size_t)pl->gacc_n, pl->world, stream);
+            if (st != OOB_OK) return st;
+        }
+        if ((e = launch_fin(pl, dg, gacc, l, l < G.L ? l + 1 : 0, stream, shard)) != cudaSuccess)
             return cuda_fail(e, "k_fin launch");
     }
     {

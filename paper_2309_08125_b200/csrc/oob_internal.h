@@ -48,6 +48,10 @@ struct Geometry {
 // Builds the geometry; returns false (and sets the error) on bad arguments.
 bool build_geometry(int L, int M, int n_lo, int n_hi, Geometry &g);
 
+// ncclAllGather of `bytes` per rank (oob_dist.cpp)
+oob_status nccl_allgather_bytes(void *comm, const void *send, void *recv, size_t bytes, size_t recv_cap,
+                                int world, void *stream);
+
 // ---------------------------------------------------------------- packed templates
 // Device output record, see oob_dp_run in oobleck_plan.h.
 struct PackedHeader {

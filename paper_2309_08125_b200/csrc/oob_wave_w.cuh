@@ -54,6 +54,7 @@ struct WaveW {
     int seeded;            // 1: start from the global accumulator (an earlier pass's minima)
     long long perm_a;      // > 1: unit order permutation multiplier (coprime to the pass's unit count)
     int rev_lanes;         // 1: lane i holds the block's tile 31 - i (diagnostic)
+    int rank, world;       // single-profile sharding: this rank takes units rank, rank+world, ...
     int nout;              // W-part cells of a slab of length l (W(1)..W(Q_l))
     ulonglong2 *GACC;      // global accumulator [P][nranges][nout]: {total bits, key}
     const int32_t *tile_off;   // [L+1] offset of the flat tile list of a big side of length lb
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(NTW, 2) k_wave_w(DevGeom g, WaveW w) {
 
     for (;;) {
         int un = 0;
-        if (lane == 0) un = w.unit_lo + atomicAdd(gctr, 1);
+        if (lane == 0) un = w.unit_lo + w.rank + w.world * atomicAdd(gctr, 1);
         un = __shfl_sync(0xFFFFFFFFu, un, 0);
         if (un >= nunits) break;
         if (w.perm_a > 1)    // visit the queue in a pseudo-random order (a permutation of the pass's units)
@@ -410,7 +411,10 @@ __global__ void k_gacc_init(ulonglong2 *gacc, int64_t n) {
 struct FinArgs {
     int lw, nranges_w, nout_w;     // W finalize of wave lw (lw = 0: none)
     int nbw;                       // blocks of the W part
-    ulonglong2 *GACC;              // accumulator of wave lw
+    ulonglong2 *GACC;              // accumulator of wave lw (this rank's)
+    const ulonglong2 *GPART;       // world > 1: all ranks' partial accumulators [world][entries]
+    int64_t part_stride;           // entries per rank in GPART
+    int world;
     int lseed, nout_s, nbseed;     // seeds of wave lseed (0: none): W outputs per range, blocks
     ulonglong2 *GSEED;             // accumulator of wave lseed (the other parity buffer)
     int ls, nsmall;                // small cells of wave ls (ls = 0: none); cells per range
@@ -439,8 +443,12 @@ __global__ void __launch_bounds__(256) k_fin(DevGeom g, FinArgs f) {
         const int q = lo, Sp = q + (i - c_woff(g.M, l, q));
         if (q < 2) return;        // W(1) cell (computed with the small cells)
         ulonglong2 *ga = f.GACC + t;
-        const ulonglong2 a = __ldcg(ga);
+        ulonglong2 a = __ldcg(ga);
         __stcg(ga, make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull));
+        for (int r = 0; r < f.world && f.world > 1; ++r) {   // lexicographic min over the ranks
+            const ulonglong2 b = __ldcg(f.GPART + (int64_t)r * f.part_stride + t);
+            if (lex_less(b.x, (uint32_t)b.y, a.x, (uint32_t)a.y)) a = b;
+        }
         const int64_t pc = (int64_t)p * g.C;
         const int aW = (g.M - 1) + q - 1;
         if (a.x >= ACC_EMPTY) {   // no split found: impossible for a valid cell; poison it

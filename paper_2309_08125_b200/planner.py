@@ -141,6 +141,16 @@ class DPPlan:
             stream: int = 0) -> None:
         check(lib.oob_dp_run(self._h, d_fwd, d_bwd, d_workspace, workspace_bytes, d_packed, stream or None))
 
+    def set_comm(self, comm: "NcclComm | None") -> None:
+        """oob_dp_set_comm: shard this plan's wavefronts across the communicator's ranks
+        (every rank runs the same profile); refreshes `info` (the workspace grows)."""
+        if comm is None:
+            check(lib.oob_dp_set_comm(self._h, None, 1, 0))
+        else:
+            check(lib.oob_dp_set_comm(self._h, comm.handle, comm.world, comm.rank))
+            self._comm = comm
+        check(lib.oob_dp_plan_info(self._h, ctypes.byref(self.info)))
+
     def set_timing(self, enable: bool) -> None:
         check(lib.oob_dp_set_timing(self._h, 1 if enable else 0))
 
@@ -161,6 +171,36 @@ class DPPlan:
         if getattr(self, "_h", None) and lib is not None:
             lib.oob_dp_plan_free(self._h)
             self._h = None
+
+
+class NcclComm:
+    """An NCCL communicator owned by the library (oob_nccl_comm_create); the unique id is
+    created by rank 0 and broadcast over an existing torch.distributed process group."""
+
+    def __init__(self, world: int, rank: int, device: int, group=None):
+        import torch
+        import torch.distributed as dist
+        buf = torch.zeros(_lib.NCCL_ID_BYTES, dtype=torch.uint8)
+        if rank == 0:
+            idb = (ctypes.c_uint8 * _lib.NCCL_ID_BYTES)()
+            check(lib.oob_nccl_unique_id(idb))
+            buf = torch.tensor(list(idb), dtype=torch.uint8)
+        if world > 1:
+            if dist.get_backend(group) == "nccl":
+                dev_buf = buf.cuda(device)
+                dist.broadcast(dev_buf, 0, group=group)
+                buf = dev_buf.cpu()
+            else:
+                dist.broadcast(buf, 0, group=group)
+        idb = (ctypes.c_uint8 * _lib.NCCL_ID_BYTES)(*buf.tolist())
+        h = ctypes.c_void_p()
+        check(lib.oob_nccl_comm_create(idb, world, rank, device, ctypes.byref(h)))
+        self.handle, self.world, self.rank = h, world, rank
+
+    def __del__(self):
+        if getattr(self, "handle", None) and lib is not None:
+            lib.oob_nccl_comm_destroy(self.handle)
+            self.handle = None
 
 
 def dp_info(L: int, M: int, n_lo: int, n_hi: int, num_profiles: int = 1) -> OobDpInfo:

@@ -193,3 +193,54 @@ def test_cfg5_full_sweep_sampled(planner):
         p = profs[i]
         want, _ = coracle.template_set(p.fwd_ms, p.bwd_ms, cfg.M, cfg.n0, cfg.n0 + 3)
         _assert_same(ts.templates(i)[:4], want, f"cfg5 profile {i} sizes 1..4")
+
+
+def _shard_worker(rank, world, port, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        from paper_2309_08125_b200 import planner as pl
+        cfg = CONFIGS["cfg3"]
+        prof = config_profiles(cfg, "real")[0]
+        comm = pl.NcclComm(world, rank, rank)
+        plan = pl.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, 1)
+        plan.set_comm(comm)
+        info = plan.info
+        fwd = torch.tensor(prof.fwd_ms[None], dtype=torch.float64, device="cuda")
+        bwd = torch.tensor(prof.bwd_ms[None], dtype=torch.float64, device="cuda")
+        ws = torch.empty(info.workspace_bytes, dtype=torch.uint8, device="cuda")
+        packed = torch.zeros(info.packed_bytes, dtype=torch.uint8, device="cuda")
+        plan.run(fwd.data_ptr(), bwd.data_ptr(), ws.data_ptr(), ws.numel(), packed.data_ptr(),
+                 torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        got = plan.template_set(packed.cpu().numpy()).templates(0)
+        want, _ = coracle.template_set(prof.fwd_ms, prof.bwd_ms, cfg.M, cfg.n0, cfg.n_max)
+        q.put((rank, got == want))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_single_profile_sharding_two_gpus(planner):
+    """oob_dp_set_comm: one profile split across 2 GPUs (NCCL all-gather of partial argmins
+    per wavefront) gives the oracle's template set on both ranks (needs >= 2 GPUs)."""
+    import socket
+    import torch
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    res = sorted(q.get() for _ in range(2))
+    assert res == [(0, True), (1, True)]
