@@ -41,6 +41,8 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
               "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-I", INC, "-I", CSRC]
 if os.environ.get("OOB_FLUSH_STATS"):          # diagnostic build (scripts/flush_stats.py)
     NVCC_FLAGS += ["-DOOB_FLUSH_STATS"]
+for _d in os.environ.get("OOB_NVCC_DEFS", "").split():   # diagnostic builds: OOB_NVCC_DEFS="X=1 Y"
+    NVCC_FLAGS += ["-D" + _d]
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall",
              "-I", INC, "-I", CSRC, "-I", os.path.join(CUDA, "include"), "-I", os.path.join(NCCL, "include")]
 

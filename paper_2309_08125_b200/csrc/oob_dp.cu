@@ -185,11 +185,11 @@ namespace {
 
 // k_wave_w launch configurations: (TE cells per lane tile, threads per CTA)
 struct WCfg { int te, nt; };
-constexpr WCfg WCFGS[] = {{4, NTW}, {5, NTW}};
+constexpr WCfg WCFGS[] = {{4, NTW}, {5, NTW}, {3, NTW}, {2, NTW}};
 constexpr double SHARD_MIN_SPLITS = 2e7;   // wavefronts sharded across ranks (oob_dp_set_comm)
 constexpr int SEED_MIN_L = 6;      // waves seeded with proportional splits (k_fin)
 constexpr int CTAS_PER_SM = 512 / NTW;   // k_wave_w: 16 resident warps per SM (register bound: 128 regs)
-constexpr int NWCFG = 2;
+constexpr int NWCFG = 4;
 
 struct WaveHost {
     int cfg = 0;                   // index into WCFGS
@@ -223,8 +223,11 @@ struct oob_dp_plan {
     int32_t P = 1;
     int kernel = 2;                      // 1 = v1 (thread per cell), 2 = tiled W kernel
     int force_cfg = -1;
+    int units_per_cta = 0;               // OOB_DP_UPC: minimum queue units per CTA (chunk size)
+    int auto_cfgs = 2;                   // OOB_DP_AUTOCFGS: WCFGS entries the wave model chooses from
     int seed_pass = 0;                   // OOB_DP_SEED=1 enables the seeding pass
     int seed_init = 1;                   // OOB_DP_SEEDINIT=0: no proportional-split seeds
+    int small_pairs = 1;                 // OOB_DP_SMALLPAIRS: layer splits per thread of a small cell
     int perm_order = 0;                  // OOB_DP_PERM=1: pseudo-random unit order
     int rev_lanes = 0;                   // OOB_DP_REV=1: reversed lane <-> tile order
     size_t geom_bytes = 0, ws_bytes = 0, tpl_bytes = 0;
@@ -239,7 +242,7 @@ struct oob_dp_plan {
     size_t ws_bytes_base = 0;
     size_t ctr_n = 0;
     std::vector<int32_t> tiles;          // all TE's tables concatenated
-    TileTab tab[2];                      // TE = 4, TE = 5
+    TileTab tab[NWCFG];                  // per WCFGS entry (TE = 4, 5, 3, 2)
     std::vector<WaveHost> waves;         // [L+1]
     size_t max_smem = 0;
     int64_t launches = 0;
@@ -258,7 +261,7 @@ static oob_status cuda_fail(cudaError_t e, const char *what) {
     return fail(OOB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-static int te_index(int te) { return te == 4 ? 0 : 1; }
+static int te_index(int te) { return te == 4 ? 0 : te == 5 ? 1 : te == 3 ? 2 : 3; }
 
 // Flat tile lists: for a big side of length lb, its W rows j = 1..min(Q, lb) cut into
 // ceil(len/TE) tiles of TE consecutive cells, in row order; 32 consecutive tiles form one
@@ -343,7 +346,7 @@ static void build_wave(oob_dp_plan *pl, int l, int ci, int slots, WaveHost &wh, 
     const size_t nent = (size_t)(wh.nout + g.L + 2 * TE + 2);
     const size_t before_ring = nent * 16 + (nent + 3) / 4 * 16 + (size_t)wh.nents * 16 + (size_t)(g.L + 2) * 8 +
                                (size_t)(g.L + 1) * 4 + (size_t)(g.L + 2) * 4 + (size_t)(g.L + 4) * 4;
-    wh.smem = before_ring + 16;
+    wh.smem = before_ring + 32 + (size_t)(NTW / 32) * XR_BYTES;   // + per-warp streamed-side rings
     wh.cost = total * ranges;
 }
 
@@ -354,11 +357,10 @@ static int small_cells(const Geometry &g, int l) {
     return per;
 }
 
-// threads per small cell: ~4 (k, m) pairs per thread, 32..256
-static int small_tpc(const Geometry &g, int l) {
-    const int pairs = (l - 1) * std::max(1, g.M - 1);
-    int t = 32;
-    while (t < 256 && t * 4 < pairs) t *= 2;
+// threads per small cell: about `per` layer splits l1 per thread, 1..32 (one warp segment)
+static int small_tpc(const Geometry &g, int l, int per) {
+    int t = 1;
+    while (t < 32 && t * per < l - 1) t *= 2;
     return t;
 }
 
@@ -374,24 +376,28 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     const char *kv = std::getenv("OOB_DP_KERNEL");
     pl->kernel = (kv && std::string(kv) == "v1") ? 1 : 2;
     if (const char *fc = std::getenv("OOB_DP_WCFG")) pl->force_cfg = std::atoi(fc);
+    if (const char *up = std::getenv("OOB_DP_UPC")) pl->units_per_cta = std::max(0, std::atoi(up));
+    if (const char *ac = std::getenv("OOB_DP_AUTOCFGS")) pl->auto_cfgs = std::max(1, std::min(NWCFG, std::atoi(ac)));
     if (const char *sp = std::getenv("OOB_DP_SEED")) pl->seed_pass = std::atoi(sp) != 0;
     if (const char *si = std::getenv("OOB_DP_SEEDINIT")) pl->seed_init = std::atoi(si) != 0;
+    if (const char *sp2 = std::getenv("OOB_DP_SMALLPAIRS")) pl->small_pairs = std::max(1, std::atoi(sp2));
     if (const char *po = std::getenv("OOB_DP_PERM")) pl->perm_order = std::atoi(po) != 0;
     if (const char *rv = std::getenv("OOB_DP_REV")) pl->rev_lanes = std::atoi(rv) != 0;
-    build_tiles(pl, 4);
-    build_tiles(pl, 5);
+    for (int ci = 0; ci < NWCFG; ++ci) build_tiles(pl, WCFGS[ci].te);
     pl->waves.assign(L + 1, WaveHost());
     size_t items_total = 0, gacc_max = 0, ctr_total = 0;
     for (int l = 2; l <= L; ++l) {
         WaveHost best;
         double best_t = 1e300;
         for (int ci = 0; ci < NWCFG; ++ci) {
-            if (pl->force_cfg >= 0 && ci != pl->force_cfg) continue;
+            if (pl->force_cfg >= 0 ? ci != pl->force_cfg : ci >= pl->auto_cfgs) continue;
             WaveHost wh;
-            // smaller chunks (more, shorter units) until every warp slot has ~4 units
+            // smaller chunks (more, shorter units) until every warp slot has ~4 units and every
+            // CTA has >= units_per_cta units of its range's queue (short tails per CTA)
             for (int CH = 96;; CH /= 2) {
                 build_wave(pl, l, ci, CTAS_PER_SM * 148, wh, CH);
-                if (CH <= 12 || (int64_t)wh.nunits * num_profiles * (L - l + 1) >= 4LL * CTAS_PER_SM * 148 * (NTW / 32))
+                if (CH <= 12 || ((int64_t)wh.nunits * num_profiles * (L - l + 1) >= 4LL * CTAS_PER_SM * 148 * (NTW / 32) &&
+                                 wh.nunits >= pl->units_per_cta * wh.cpr))
                     break;
             }
             // resident CTAs per SM: launch bounds 256 x 2, smem
@@ -445,12 +451,12 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     pl->off_base = o;  o = align_up(o + sizeof(int64_t) * (L + 2), 256);
     pl->off_off = o;   o = align_up(o + sizeof(int32_t) * (size_t)(L + 1) * g.A, 256);
     pl->off_tiles = o; o = align_up(o + sizeof(int32_t) * pl->tiles.size(), 256);
-    pl->off_tile_off = o; o = align_up(o + sizeof(int32_t) * (L + 1) * 2, 256);
-    pl->off_tile_cnt = o; o = align_up(o + sizeof(int32_t) * (L + 1) * 2, 256);
+    pl->off_tile_off = o; o = align_up(o + sizeof(int32_t) * (L + 1) * NWCFG, 256);
+    pl->off_tile_cnt = o; o = align_up(o + sizeof(int32_t) * (L + 1) * NWCFG, 256);
     pl->off_items = o;    o = align_up(o + items_total, 256);
     pl->geom_bytes = o;
     const size_t n = (size_t)g.total_cells * num_profiles;
-    pl->off_CELL = o; o = align_up(o + 32 * (n + 16), 256);   // + padding: row streams read ahead
+    pl->off_CELL = o; o = align_up(o + 32 * (n + 16 + XR_CELLS), 256);   // + padding: row streams read ahead
     pl->off_ARG = o; o = align_up(o + 4 * n, 256);
     pl->off_STK = o; o = align_up(o + 8 * (size_t)num_profiles * (n_hi - n_lo + 1) * (L + 1), 256);
     pl->gacc_n = (int64_t)gacc_max;
@@ -465,7 +471,7 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     std::memcpy(b + pl->off_base, g.base.data(), sizeof(int64_t) * (L + 2));
     std::memcpy(b + pl->off_off, g.off.data(), sizeof(int32_t) * (size_t)(L + 1) * g.A);
     if (!pl->tiles.empty()) std::memcpy(b + pl->off_tiles, pl->tiles.data(), sizeof(int32_t) * pl->tiles.size());
-    for (int ti = 0; ti < 2; ++ti) {
+    for (int ti = 0; ti < NWCFG; ++ti) {
         std::memcpy(b + pl->off_tile_off + sizeof(int32_t) * (L + 1) * ti, pl->tab[ti].off.data(), sizeof(int32_t) * (L + 1));
         std::memcpy(b + pl->off_tile_cnt + sizeof(int32_t) * (L + 1) * ti, pl->tab[ti].cnt.data(), sizeof(int32_t) * (L + 1));
     }
@@ -576,7 +582,7 @@ static cudaError_t launch_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglon
     f.GSEED = gacc_of(pl, gacc, ls);
     f.ls = ls;
     f.nsmall = ls ? small_cells(G, ls) : 0;
-    f.tpc = ls ? small_tpc(G, ls) : 32;
+    f.tpc = ls ? small_tpc(G, ls, pl->small_pairs) : 32;
     const int64_t ns = ls ? (int64_t)pl->P * (G.L - ls + 1) * f.nsmall : 0;
     const int64_t nbs = (ns + (256 / f.tpc) - 1) / (256 / f.tpc);
     const int64_t blocks = f.nbw + f.nbseed + nbs;
@@ -605,6 +611,10 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
             e = cudaFuncSetAttribute(k_wave_w<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
             if (e == cudaSuccess)
                 e = cudaFuncSetAttribute(k_wave_w<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(k_wave_w<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(k_wave_w<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
             if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(k_wave_w)");
         }
     }
@@ -695,10 +705,12 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
                     while (n > 2 && std::gcd(a, n) != 1) ++a;
                     w.perm_a = n > 2 ? a : 1;
                 }
-                if (WCFGS[wh.cfg].te == 4)
-                    k_wave_w<4><<<(unsigned)ctas, NTW, wh.smem, stream>>>(dg, w);
-                else
-                    k_wave_w<5><<<(unsigned)ctas, NTW, wh.smem, stream>>>(dg, w);
+                switch (WCFGS[wh.cfg].te) {
+                    case 2: k_wave_w<2><<<(unsigned)ctas, NTW, wh.smem, stream>>>(dg, w); break;
+                    case 3: k_wave_w<3><<<(unsigned)ctas, NTW, wh.smem, stream>>>(dg, w); break;
+                    case 4: k_wave_w<4><<<(unsigned)ctas, NTW, wh.smem, stream>>>(dg, w); break;
+                    default: k_wave_w<5><<<(unsigned)ctas, NTW, wh.smem, stream>>>(dg, w); break;
+                }
             }
         }
         if (pl->timing) { cudaEventRecord(pl->ev[pl->ev_used + 1], stream); pl->ev_used += 2; }

@@ -191,6 +191,71 @@ __device__ __forceinline__ void acc_flush(unsigned acc_s, unsigned filt_s, int i
     }
 }
 
+// Streamed side staging: a per-warp ring of XR_CELLS cells in shared memory, filled with
+// cp.async in batches of XR_BATCH cells (512 B: one 16-byte copy per lane) issued
+// XR_AHEAD batches ahead of the step loop, so the steps read the streamed cell from shared
+// memory (broadcast LDS) instead of waiting on L1/L2.  The first XR_MIRROR cells of the
+// ring are mirrored after its end, so the TE+1 cells a block of steps reads are contiguous
+// (one base address per block, immediate offsets).  Copies are unguarded: a chunk's last
+// batches may read past the slab (the CELL allocation is padded by XR_CELLS cells).
+constexpr int XR_CELLS = 64;
+constexpr int XR_BATCH = 16;
+constexpr int XR_AHEAD = 2;
+constexpr int XR_MIRROR = 8;
+constexpr int XR_BYTES = (XR_CELLS + XR_MIRROR) * 32;   // per warp
+
+struct XRing {
+    const double2 *ring;                  // this warp's ring (shared memory, 2 x double2 per cell)
+    unsigned ring_s;                      // its shared-space address + lane * 16
+    const char *src;                      // chunk start (global) + lane * 16
+    int nb_iss, nb_ok;                    // batches issued / complete
+    bool mirror;                          // this lane also writes the mirror cells
+};
+
+__device__ __forceinline__ void xr_issue(XRing &r) {
+#ifdef OOB_XR_SYNC
+    __syncwarp();
+#endif
+    const int b = r.nb_iss++;
+    const unsigned pos = (unsigned)((b * XR_BATCH) & (XR_CELLS - 1)) * 32u;
+    const char *g = r.src + (size_t)b * (XR_BATCH * 32);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(r.ring_s + pos), "l"(g) : "memory");
+    if (pos == 0 && r.mirror)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(r.ring_s + XR_CELLS * 32u), "l"(g) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void xr_start(XRing &r, const double2 *ring, const Cell4 *src, int lane) {
+    r.ring = ring;
+    r.ring_s = (unsigned)__cvta_generic_to_shared(ring) + lane * 16;
+    r.src = reinterpret_cast<const char *>(src) + lane * 16;
+    r.mirror = lane < 2 * XR_MIRROR;
+    r.nb_iss = 0;
+    r.nb_ok = 0;
+#pragma unroll
+    for (int i = 0; i <= XR_AHEAD; ++i) xr_issue(r);
+}
+// make cells <= j available (warp-uniform; j grows by <= XR_BATCH between calls)
+__device__ __forceinline__ void xr_ensure(XRing &r, int j) {
+    if (j / XR_BATCH >= r.nb_ok) {
+        xr_issue(r);
+#ifdef OOB_XR_WAIT0
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+#else
+        asm volatile("cp.async.wait_group %0;" ::"n"(XR_AHEAD) : "memory");
+#endif
+        __syncwarp();                     // the other lanes' copies are visible
+        r.nb_ok = r.nb_iss - XR_AHEAD;
+    }
+}
+// cells c .. c + XR_MIRROR of the ring as one contiguous run
+__device__ __forceinline__ const double2 *xr_at(const XRing &r, int c) { return r.ring + 2 * (c & (XR_CELLS - 1)); }
+__device__ __forceinline__ Cell4 xr_cell(const double2 *q, int i) {
+    const double2 a = q[2 * i], b = q[2 * i + 1];
+    Cell4 x;
+    x.T1 = a.x; x.T3 = a.y; x.TS = b.x; x.C1 = b.y;
+    return x;
+}
+
 // The small-side rows r_lo..r_hi-1 of one unit against this lane's register tile.
 //  LT = true : tile = LEFT child (row rowB = j, s_t = S0 + t), stream = RIGHT child (row
 //              rs = j', S_R = rs + e).  cL = C1_L[t] + 3 S_R, cR = C1_R(e) + 4 s_t.
@@ -201,15 +266,16 @@ __device__ __forceinline__ void acc_flush(unsigned acc_s, unsigned filt_s, int i
 //              Ties: arrivals with increasing s -> "<".  key = l1<<20 | rs<<10 | (rs + e).
 // Output E' = e + t (index relative to the tile's first output) lives in ring slot
 // E' mod TE; its first contribution (t = TE-1) assigns the slot, t = 0 completes it (flush).
-// Each row runs in blocks of TE steps (static slots) plus a guarded tail.
+// Each row runs in blocks of TE steps (static slots) plus a guarded tail.  The streamed
+// cells (rows r_lo..r_hi-1 are contiguous in the slab) come through the warp's XRing.
 template <int TE, bool LT>
-__device__ __forceinline__ void run_rows(const Cell4 *__restrict__ sp, int M, int ls, int r_lo, int r_hi,
+__device__ __forceinline__ void run_rows(XRing &xr, int M, int ls, int r_lo, int r_hi,
                                          const double (&RT1)[TE], const double (&RT3)[TE], const double (&RTS)[TE],
                                          const double (&RC1)[TE], int rowB, int e0, int l1, int L,
                                          const int *outOff, int nout, unsigned acc_s, unsigned filt_s) {
     const int S0 = rowB + e0;
     const double xadd = (double)((LT ? 4 : 3) * S0);
-    const Cell4 *rp = sp + c_woff(M, ls, r_lo);          // rows of a slab are contiguous
+    int rb = 0;                                           // chunk cell of the row's first cell
     for (int rs = r_lo; rs < r_hi; ++rs) {
         const int rl = c_wlen(M, ls, rs);
         const int q = rowB + rs;
@@ -222,11 +288,13 @@ __device__ __forceinline__ void run_rows(const Cell4 *__restrict__ sp, int M, in
         int widx[TE];
 #pragma unroll
         for (int t = 0; t < TE; ++t) { best[t] = D_INF; widx[t] = 0; }
-        Cell4 x = d_load(rp);
+        xr_ensure(xr, rb + TE);
+        Cell4 x = xr_cell(xr_at(xr, rb), 0);
         int blk = 0;
+        const double2 *xq = xr_at(xr, rb);
 #define OOB_STEP(I)                                                                             \
     {                                                                                           \
-        const Cell4 nx = d_load(rp + blk + (I) + 1);                                            \
+        const Cell4 nx = xr_cell(xq, (I) + 1);                                                  \
         const double xc = __dadd_rn(x.C1, xadd);                                                \
         _Pragma("unroll") for (int t = 0; t < TE; ++t) {                                        \
             const int sl = ((I) + t) % TE;                                                      \
@@ -248,15 +316,16 @@ __device__ __forceinline__ void run_rows(const Cell4 *__restrict__ sp, int M, in
                   LT ? kb + (uint32_t)widx[(I)] : kb + (uint32_t)(blk + (I) - widx[(I)]));      \
         x = nx;                                                                                 \
     }
+        // blocks of TE steps; the last one stops at the row end (one copy of the step code
+        // keeps the kernel inside the instruction cache)
 #pragma unroll 1
-        for (; blk + TE <= rl; blk += TE) {
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + blk + 3 * TE));
+        for (; blk < rl; blk += TE) {
+            xr_ensure(xr, rb + blk + TE);
+            xq = xr_at(xr, rb + blk);
 #pragma unroll
-            for (int I = 0; I < TE; ++I) OOB_STEP(I)
+            for (int I = 0; I < TE; ++I)
+                if (I == 0 || blk + I < rl) OOB_STEP(I)
         }
-#pragma unroll
-        for (int I = 0; I < TE - 1; ++I)
-            if (blk + I < rl) OOB_STEP(I)
 #undef OOB_STEP
         // pending: slot sl holds E' = rl + ((sl - rl) mod TE); E' = rl + TE - 1 is the slot of
         // E' = rl - 1, already flushed
@@ -267,8 +336,10 @@ __device__ __forceinline__ void run_rows(const Cell4 *__restrict__ sp, int M, in
                 acc_flush(acc_s, filt_s, idx0 + Ep, best[sl],
                           LT ? kb + (uint32_t)widx[sl] : kb + (uint32_t)(Ep - widx[sl]));
         }
-        rp += rl;
+        rb += rl;
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");   // no copy of this chunk outlives the unit
+    __syncwarp();
 }
 
 template <int TE>
@@ -285,6 +356,9 @@ __global__ void __launch_bounds__(NTW, 2) k_wave_w(DevGeom g, WaveW w) {
     int *scells = reinterpret_cast<int *>(sbase + L + 2);        // [L+1]
     int *outOff = scells + (L + 1);                              // [L+2] W(q) offsets (nout: none)
     int *upre = outOff + (L + 2);                                // [nents + 1]
+    // per-warp streamed-side rings (16 B aligned) after upre
+    const size_t ring_off = ((size_t)(reinterpret_cast<unsigned char *>(upre + w.nents + 1) - smem) + 15) & ~(size_t)15;
+    double2 *rings = reinterpret_cast<double2 *>(smem + ring_off);
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int pr = blockIdx.x / w.cpr;
@@ -363,11 +437,13 @@ __global__ void __launch_bounds__(NTW, 2) k_wave_w(DevGeom g, WaveW w) {
             }
         }
         const Cell4 *sp = g.CELL + pc + sbase[ls] + (int64_t)us * scells[ls] + c_ipart(M, ls);
+        XRing xr;                                            // rows r_lo.. are contiguous
+        xr_start(xr, rings + (size_t)(tid >> 5) * (XR_BYTES / 16), sp + c_woff(M, ls, r_lo), lane);
         if (ltiled)
-            run_rows<TE, true>(sp, M, ls, r_lo, r_hi, RT1, RT3, RTS, RC1, rowB, e0, l1, L, outOff, nout, acc_s,
+            run_rows<TE, true>(xr, M, ls, r_lo, r_hi, RT1, RT3, RTS, RC1, rowB, e0, l1, L, outOff, nout, acc_s,
                                filt_s);
         else
-            run_rows<TE, false>(sp, M, ls, r_lo, r_hi, RT1, RT3, RTS, RC1, rowB, e0, l1, L, outOff, nout, acc_s,
+            run_rows<TE, false>(xr, M, ls, r_lo, r_hi, RT1, RT3, RTS, RC1, rowB, e0, l1, L, outOff, nout, acc_s,
                                 filt_s);
     }
     __syncthreads();
@@ -591,27 +667,34 @@ __global__ void __launch_bounds__(256) k_fin(DevGeom g, FinArgs f) {
         const double dSp3 = (double)(3 * Sp - 1);
         const int r = d_is_whole(g, a) ? g.M : d_alloc_n(g, a);  // GPUs of the cell's node part
         const int nd = r - 1;                                    // device splits (I(m), I(r-m))
-        const int npairs = (l - 1) * nd;
-        for (int fp = tl; fp < npairs; fp += f.tpc) {
-            const int l1 = 1 + fp / nd, m = 1 + fp % nd;
+        // a thread takes layer splits l1 = 1 + tl, 1 + tl + tpc, ... and, for each, every
+        // device split m and stage split s (ascending, strict "<": the first minimum in
+        // (k, m, s) order).  I(m) of a slab of length l' starts at c_ipart(m, l') (I(1..m-1)
+        // before it; W(1) plays "I(M)" right after I(M-1)).
+        const Cell4 *CP = g.CELL + pc;
+        for (int l1 = 1 + tl; l1 < l; l1 += f.tpc) {
             const int k = u + l1, l2 = l - l1;
-            const int s_lo = max(1, Sp - min(l2, r - m));
-            const int s_hi = min(Sp - 1, min(l1, m));
-            const Cell4 *lb = g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + g.off[l1 * g.A + (m - 1)] - 1;
-            const Cell4 *rb = g.CELL + pc + g.base[l2] + (int64_t)k * g.cells[l2] + g.off[l2 * g.A + (r - m - 1)] - 1;
-            for (int s = s_lo; s <= s_hi; ++s) {
-                const Cell4 Lc = d_load(lb + s);
-                const Cell4 Rc = d_load(rb + (Sp - s));
-                const double T1 = __dadd_rn(Lc.T1, Rc.T1);
-                const bool left = Lc.TS >= Rc.TS;
-                const double T3 = left ? __dadd_rn(Lc.T3, Rc.T1) : Rc.T3;
-                const double TS = left ? Lc.TS : Rc.TS;
-                const double KD = left ? d_kd(Lc.C1, s) : __dadd_rn((double)s, d_kd(Rc.C1, Sp - s));
-                const double T2 = __dmul_rn(__dadd_rn(KD, dSp3), TS);
-                const double tot = __dadd_rn(__dadd_rn(T1, T2), T3);
-                if (tot < best) {
-                    best = tot;
-                    bkey = ((uint32_t)l1 << 20) | ((uint32_t)(m - 1) << 10) | (uint32_t)s;
+            const Cell4 *lrow = CP + g.base[l1] + (int64_t)u * g.cells[l1] - 1;
+            const Cell4 *rrow = CP + g.base[l2] + (int64_t)k * g.cells[l2] - 1;
+            for (int m = 1; m <= nd; ++m) {
+                const int s_lo = max(1, Sp - min(l2, r - m));
+                const int s_hi = min(Sp - 1, min(l1, m));
+                const Cell4 *lb = lrow + c_ipart(m, l1);
+                const Cell4 *rb = rrow + c_ipart(r - m, l2) + Sp;
+                for (int s = s_lo; s <= s_hi; ++s) {
+                    const Cell4 Lc = d_load(lb + s);
+                    const Cell4 Rc = d_load(rb - s);
+                    const double T1 = __dadd_rn(Lc.T1, Rc.T1);
+                    const bool left = Lc.TS >= Rc.TS;
+                    const double T3 = left ? __dadd_rn(Lc.T3, Rc.T1) : Rc.T3;
+                    const double TS = left ? Lc.TS : Rc.TS;
+                    const double KD = left ? d_kd(Lc.C1, s) : __dadd_rn((double)s, d_kd(Rc.C1, Sp - s));
+                    const double T2 = __dmul_rn(__dadd_rn(KD, dSp3), TS);
+                    const double tot = __dadd_rn(__dadd_rn(T1, T2), T3);
+                    if (tot < best) {
+                        best = tot;
+                        bkey = ((uint32_t)l1 << 20) | ((uint32_t)(m - 1) << 10) | (uint32_t)s;
+                    }
                 }
             }
         }
