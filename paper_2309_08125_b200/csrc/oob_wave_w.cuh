@@ -289,12 +289,11 @@ __device__ __forceinline__ void run_rows(XRing &xr, int M, int ls, int r_lo, int
 #pragma unroll
         for (int t = 0; t < TE; ++t) { best[t] = D_INF; widx[t] = 0; }
         xr_ensure(xr, rb + TE);
-        Cell4 x = xr_cell(xr_at(xr, rb), 0);
         int blk = 0;
         const double2 *xq = xr_at(xr, rb);
 #define OOB_STEP(I)                                                                             \
     {                                                                                           \
-        const Cell4 nx = xr_cell(xq, (I) + 1);                                                  \
+        const Cell4 x = xr_cell(xq, (I));                                                       \
         const double xc = __dadd_rn(x.C1, xadd);                                                \
         _Pragma("unroll") for (int t = 0; t < TE; ++t) {                                        \
             const int sl = ((I) + t) % TE;                                                      \
@@ -314,7 +313,6 @@ __device__ __forceinline__ void run_rows(XRing &xr, int M, int ls, int r_lo, int
         cst = __dadd_rn(cst, LT ? 3.0 : 4.0);                                                   \
         acc_flush(acc_s, filt_s, idx0 + blk + (I), best[(I)],                                   \
                   LT ? kb + (uint32_t)widx[(I)] : kb + (uint32_t)(blk + (I) - widx[(I)]));      \
-        x = nx;                                                                                 \
     }
         // blocks of TE steps; the last one stops at the row end (one copy of the step code
         // keeps the kernel inside the instruction cache)
