@@ -200,8 +200,10 @@ struct WaveHost {
     std::vector<int32_t> cb;       // chunk row boundaries
     size_t smem = 0;
     size_t ctr_off = 0;            // first unit counter of this wave (ints; two passes)
+    size_t done_off = 0;           // per-range finished-CTA counters (fused finalize)
     int seed_units = 0;            // units of the seeding pass (balanced splits), 0 = one pass
     int nsmall = 0;                // cells inside one node with S' >= 2 per range
+    bool seed = false;             // accumulator seeded by k_fin (proportional + warm-start splits)
     double cost = 0.0;             // modelled issue cycles of the wave (all ranges, profiles)
 };
 
@@ -227,7 +229,9 @@ struct oob_dp_plan {
     int auto_cfgs = 2;                   // OOB_DP_AUTOCFGS: WCFGS entries the wave model chooses from
     int seed_pass = 0;                   // OOB_DP_SEED=1 enables the seeding pass
     int seed_init = 1;                   // OOB_DP_SEEDINIT=0: no proportional-split seeds
+    double seed_spo = 1000.0;            // OOB_DP_SEEDSPO: seed waves with >= this many splits per W output
     int small_pairs = 1;                 // OOB_DP_SMALLPAIRS: layer splits per thread of a small cell
+    int fuse_fin = 1;                    // OOB_DP_FUSE=0: separate k_fin launch per wave
     int perm_order = 0;                  // OOB_DP_PERM=1: pseudo-random unit order
     int rev_lanes = 0;                   // OOB_DP_REV=1: reversed lane <-> tile order
     size_t geom_bytes = 0, ws_bytes = 0, tpl_bytes = 0;
@@ -380,7 +384,9 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     if (const char *ac = std::getenv("OOB_DP_AUTOCFGS")) pl->auto_cfgs = std::max(1, std::min(NWCFG, std::atoi(ac)));
     if (const char *sp = std::getenv("OOB_DP_SEED")) pl->seed_pass = std::atoi(sp) != 0;
     if (const char *si = std::getenv("OOB_DP_SEEDINIT")) pl->seed_init = std::atoi(si) != 0;
+    if (const char *ss = std::getenv("OOB_DP_SEEDSPO")) pl->seed_spo = std::atof(ss);
     if (const char *sp2 = std::getenv("OOB_DP_SMALLPAIRS")) pl->small_pairs = std::max(1, std::atoi(sp2));
+    if (const char *fu = std::getenv("OOB_DP_FUSE")) pl->fuse_fin = std::atoi(fu) != 0;
     if (const char *po = std::getenv("OOB_DP_PERM")) pl->perm_order = std::atoi(po) != 0;
     if (const char *rv = std::getenv("OOB_DP_REV")) pl->rev_lanes = std::atoi(rv) != 0;
     for (int ci = 0; ci < NWCFG; ++ci) build_tiles(pl, WCFGS[ci].te);
@@ -419,8 +425,18 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
         wh.cb_off = items_total;
         items_total += align_up(wh.cb.size() * sizeof(int32_t), 16);
         gacc_max = std::max(gacc_max, (size_t)num_profiles * (L - l + 1) * wh.nout);
+        // seeds cost ~18 scattered split evaluations per W output; they pay off where an output
+        // has many splits (long rows: many flushes the seeded filter rejects)
+        {
+            int64_t wout = 0;
+            for (int q = 2; q <= std::min(Q_of(g, l), l); ++q) wout += wlen_h(g, l, q);
+            const double spo = wout ? (double)g.wave_splits[l] / ((double)(L - l + 1) * wout) : 0.0;
+            wh.seed = pl->seed_init && l >= SEED_MIN_L && spo >= pl->seed_spo;
+        }
         wh.ctr_off = ctr_total;
         ctr_total += 2 * (size_t)num_profiles * (L - l + 1);
+        wh.done_off = ctr_total;
+        ctr_total += (size_t)num_profiles * (L - l + 1);
         // seeding pass: the balanced entries' units (~4% of the wave) fill the global
         // accumulator first, so that the main pass's flush filter rarely passes
         wh.seed_units = 0;
@@ -441,10 +457,6 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
                          (long long)wh.cpr * (L - l + 1) * num_profiles, wh.smem, wh.cost);
         }
     }
-    // k_base + k_extract; v1: one kernel per wave; v6: k_fin(1) + (k_wave_w, k_fin) per wave
-    pl->launches = 2 + (pl->kernel == 1 ? (L - 1) : 1 + 2 * (L - 1));
-    if (pl->kernel == 2)
-        for (int l = 2; l <= L; ++l) pl->launches += pl->waves[l].seed_units > 0 ? 1 : 0;
 
     size_t o = 0;
     pl->off_cells = o; o = align_up(o + sizeof(int32_t) * (L + 1), 256);
@@ -494,6 +506,23 @@ extern "C" void oob_dp_plan_free(oob_dp_plan *pl) {
     delete pl;
 }
 
+// Kernels one oob_dp_run enqueues (k_gacc_init only on a workspace's first run): k_base,
+// k_fin(in-node cells of wave 2), per wave k_wave_w (+ seeding pass) and, unless fused,
+// k_fin; k_extract.  v1: k_base, one kernel per wave, k_extract.
+static int64_t count_launches(const oob_dp_plan *pl) {
+    const Geometry &G = pl->g;
+    if (pl->kernel == 1) return 2 + (G.L - 1);
+    int64_t n = 3;
+    for (int l = 2; l <= G.L; ++l) {
+        const WaveHost &wh = pl->waves[l];
+        const bool shard = pl->world > 1 && (double)G.wave_splits[l] * pl->P >= SHARD_MIN_SPLITS;
+        const bool has = wh.nents > 0;
+        n += has ? (wh.seed_units > 0 ? 2 : 1) : 0;
+        n += (pl->fuse_fin && has && !shard && wh.seed_units == 0) ? 0 : 1;
+    }
+    return n;
+}
+
 extern "C" oob_status oob_dp_plan_info(const oob_dp_plan *pl, oob_dp_info *out) {
     if (!pl || !out) return fail(OOB_E_INVALID, "oob_dp_plan_info: NULL argument");
     const Geometry &g = pl->g;
@@ -502,7 +531,7 @@ extern "C" oob_status oob_dp_plan_info(const oob_dp_plan *pl, oob_dp_info *out) 
     out->wavefronts = g.L - 1;
     out->cells_per_profile = g.total_cells;
     out->splits_per_profile = g.total_splits;
-    out->kernel_launches = pl->launches;
+    out->kernel_launches = count_launches(pl);
     out->workspace_bytes = pl->ws_bytes;
     out->packed_template_bytes = pl->tpl_bytes;
     out->packed_profile_bytes = pl->tpl_bytes * (size_t)(g.n_hi - g.n_lo + 1);
@@ -561,8 +590,10 @@ static ulonglong2 *gacc_of(const oob_dp_plan *pl, ulonglong2 *gacc, int l) {
     return gacc + (size_t)(l & 1) * (size_t)pl->gacc_n;
 }
 
-static cudaError_t launch_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglong2 *gacc, int lw, int ls,
-                              cudaStream_t stream, bool sharded = false) {
+// Finalize arguments for wave lw (0: none) and in-node cells + seeds of wave ls (0: none);
+// *nbsmall receives the blocks of the small-cell part.
+static FinArgs make_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglong2 *gacc, int lw, int ls, bool sharded,
+                        int64_t *nbsmall) {
     const Geometry &G = pl->g;
     FinArgs f;
     f.lw = lw;
@@ -575,7 +606,7 @@ static cudaError_t launch_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglon
     f.part_stride = (int64_t)pl->P * f.nranges_w * f.nout_w;   // all-gather: rank r at r x (wave partial)
     f.GPART = (const ulonglong2 *)((const unsigned char *)dg.CELL - pl->off_CELL + pl->off_GPART);
     // seeds for wave ls (children of length <= ls-2: final before this launch)
-    f.lseed = (ls >= SEED_MIN_L && pl->seed_init) ? ls : 0;
+    f.lseed = (ls >= 2 && pl->waves[ls].seed) ? ls : 0;
     f.nout_s = f.lseed ? pl->waves[ls].nout : 0;
     const int64_t nsd = f.lseed ? (int64_t)pl->P * (G.L - ls + 1) * f.nout_s : 0;
     f.nbseed = (int)((nsd + 255) / 256);
@@ -584,7 +615,14 @@ static cudaError_t launch_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglon
     f.nsmall = ls ? small_cells(G, ls) : 0;
     f.tpc = ls ? small_tpc(G, ls, pl->small_pairs) : 32;
     const int64_t ns = ls ? (int64_t)pl->P * (G.L - ls + 1) * f.nsmall : 0;
-    const int64_t nbs = (ns + (256 / f.tpc) - 1) / (256 / f.tpc);
+    *nbsmall = (ns + (256 / f.tpc) - 1) / (256 / f.tpc);
+    return f;
+}
+
+static cudaError_t launch_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglong2 *gacc, int lw, int ls,
+                              cudaStream_t stream, bool sharded = false) {
+    int64_t nbs = 0;
+    const FinArgs f = make_fin(pl, dg, gacc, lw, ls, sharded, &nbs);
     const int64_t blocks = f.nbw + f.nbseed + nbs;
     if (blocks == 0) return cudaSuccess;
     k_fin<<<(unsigned)blocks, 256, 0, stream>>>(dg, f);
@@ -689,13 +727,26 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
         w.rank = shard ? pl->rank : 0;
         w.world = shard ? pl->world : 1;
         const int64_t ctas = wh.nents > 0 ? (int64_t)pl->P * w.nranges * w.cpr : 0;
+        // fused finalize (OOB_DP_FUSE=1): unsharded, single-pass waves finalize in k_wave_w's
+        // last CTAs and run the next wave's in-node cells and seeds in extra blocks
+        const bool fused = pl->fuse_fin && ctas > 0 && !shard && wh.seed_units == 0;
+        int64_t aux = 0;
+        w.nbmain = (int)ctas;
+        w.fin_inline = fused ? 1 : 0;
+        w.rdone = (int *)(ws + pl->off_CTR) + wh.done_off;
+        if (fused) {
+            int64_t nbs = 0, nbw = 0;
+            w.fa = make_fin(pl, dg, gacc, 0, l < G.L ? l + 1 : 0, false, &nbs);
+            w.fw = make_fin(pl, dg, gacc, l, 0, false, &nbw);
+            aux = w.fa.nbseed + nbs;
+        }
         if (pl->timing) cudaEventRecord(pl->ev[pl->ev_used], stream);
         if (ctas > 0) {
             // pass 1 (optional): the seeding units; pass 2: the rest, from the seeded minima
             for (int pass = wh.seed_units > 0 ? 0 : 1; pass < 2; ++pass) {
                 w.unit_lo = pass == 0 ? 0 : wh.seed_units;
                 w.unit_hi = pass == 0 ? wh.seed_units : wh.nunits;
-                w.seeded = (pass == 1 && wh.seed_units > 0) || (l >= SEED_MIN_L && pl->seed_init);
+                w.seeded = (pass == 1 && wh.seed_units > 0) || wh.seed;
                 w.ctr = (int *)(ws + pl->off_CTR) + wh.ctr_off + (size_t)pass * pl->P * w.nranges;
                 w.perm_a = 1;
                 w.rev_lanes = pl->rev_lanes;
@@ -705,11 +756,12 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
                     while (n > 2 && std::gcd(a, n) != 1) ++a;
                     w.perm_a = n > 2 ? a : 1;
                 }
+                const unsigned grid = (unsigned)(ctas + aux);
                 switch (WCFGS[wh.cfg].te) {
-                    case 2: k_wave_w<2><<<(unsigned)ctas, NTW, wh.smem, stream>>>(dg, w); break;
-                    case 3: k_wave_w<3><<<(unsigned)ctas, NTW, wh.smem, stream>>>(dg, w); break;
-                    case 4: k_wave_w<4><<<(unsigned)ctas, NTW, wh.smem, stream>>>(dg, w); break;
-                    default: k_wave_w<5><<<(unsigned)ctas, NTW, wh.smem, stream>>>(dg, w); break;
+                    case 2: k_wave_w<2><<<grid, NTW, wh.smem, stream>>>(dg, w); break;
+                    case 3: k_wave_w<3><<<grid, NTW, wh.smem, stream>>>(dg, w); break;
+                    case 4: k_wave_w<4><<<grid, NTW, wh.smem, stream>>>(dg, w); break;
+                    default: k_wave_w<5><<<grid, NTW, wh.smem, stream>>>(dg, w); break;
                 }
             }
         }
@@ -722,7 +774,7 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
                                                  bytes, 16 * (size_t)pl->gacc_n, pl->world, stream);
             if (st != OOB_OK) return st;
         }
-        if ((e = launch_fin(pl, dg, gacc, l, l < G.L ? l + 1 : 0, stream, shard)) != cudaSuccess)
+        if (!fused && (e = launch_fin(pl, dg, gacc, l, l < G.L ? l + 1 : 0, stream, shard)) != cudaSuccess)
             return cuda_fail(e, "k_fin launch");
     }
     {

@@ -41,6 +41,20 @@ constexpr int NTW = 256;                                          // threads per
 constexpr unsigned long long ACC_EMPTY = 0x7FEFFFFFFFFFFFFFull;   // DBL_MAX: "no split yet"
 constexpr double D_INF = __builtin_huge_val();
 
+// Finalize / in-node work of one wavefront (k_fin, or k_wave_w's extra blocks and last CTAs).
+struct FinArgs {
+    int lw, nranges_w, nout_w;     // W finalize of wave lw (lw = 0: none)
+    int nbw;                       // blocks of the W part
+    ulonglong2 *GACC;              // accumulator of wave lw (this rank's)
+    const ulonglong2 *GPART;       // world > 1: all ranks' partial accumulators [world][entries]
+    int64_t part_stride;           // entries per rank in GPART
+    int world;
+    int lseed, nout_s, nbseed;     // seeds of wave lseed (0: none): W outputs per range, blocks
+    ulonglong2 *GSEED;             // accumulator of wave lseed (the other parity buffer)
+    int ls, nsmall;                // small cells of wave ls (ls = 0: none); cells per range
+    int tpc;                       // threads per small cell
+};
+
 struct WaveW {
     int l;                 // wavefront length
     int nranges;           // L - l + 1
@@ -60,6 +74,13 @@ struct WaveW {
     const int32_t *tile_off;   // [L+1] offset of the flat tile list of a big side of length lb
     const int32_t *tile_cnt;   // [L+1] number of tiles
     const int32_t *tiles;      // packed (row << 16 | e0)
+    // fused finalize (unsharded waves): blocks >= nbmain run the in-node cells and seeds of
+    // the next wave (fa: nbw = 0; independent of this wave, they fill its tail); the last CTA
+    // of each range (rdone counter) finalizes the range's W outputs of this wave (fw: lw = l)
+    int nbmain;
+    int fin_inline;
+    int *rdone;                // [P][nranges] CTAs of the range that have merged
+    FinArgs fa, fw;
 };
 
 __device__ __forceinline__ int d_wcells(const DevGeom &g, int l) {
@@ -340,9 +361,329 @@ __device__ __forceinline__ void run_rows(XRing &xr, int M, int ls, int r_lo, int
     __syncwarp();
 }
 
+// Per-wave finalize + small cells.  Blocks [0, nbw): one thread per (profile, range, W-part
+// cell) of wave lw (lw >= 2): read + reset the global accumulator, recompute the winner.
+// Blocks [nbw, ...): cells inside one node (I(r), W(1), S' >= 2) of wave ls (2 <= ls <= L):
+// `tpc` threads per cell (1..32, power of two) split the layer splits of the cell, scan
+// (m, s), keep the first strictly smaller total, then a lexicographic (total, key) reduction.
+
+__device__ __forceinline__ void fin_w_one(const DevGeom &g, const FinArgs &f, int64_t t) {
+    const int l = f.lw;
+    const int nout = f.nout_w;
+    const int i = (int)(t % nout);
+    const int u = (int)((t / nout) % f.nranges_w);
+    const int p = (int)(t / ((int64_t)nout * f.nranges_w));
+    const int Ql = (l == g.L) ? g.n_hi : max(1, g.n_hi - 1);
+    // row q of the W-part cell i: largest q with c_woff(q) <= i (binary search, closed form)
+    int lo = 1, hi = min(Ql, l);
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (c_woff(g.M, l, mid) <= i) lo = mid; else hi = mid - 1;
+    }
+    const int q = lo, Sp = q + (i - c_woff(g.M, l, q));
+    if (q < 2) return;        // W(1) cell (computed with the small cells)
+    ulonglong2 *ga = f.GACC + t;
+    ulonglong2 a = __ldcg(ga);
+    __stcg(ga, make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull));
+    for (int r = 0; r < f.world && f.world > 1; ++r) {   // lexicographic min over the ranks
+        const ulonglong2 b = __ldcg(f.GPART + (int64_t)r * f.part_stride + t);
+        if (lex_less(b.x, (uint32_t)b.y, a.x, (uint32_t)a.y)) a = b;
+    }
+    const int64_t pc = (int64_t)p * g.C;
+    const int aW = (g.M - 1) + q - 1;
+    if (a.x >= ACC_EMPTY) {   // no split found: impossible for a valid cell; poison it
+        const int64_t c = pc + d_cell(g, Sp, u, l, aW);
+        g.CELL[c].T1 = __longlong_as_double(0x7ff8000000000000LL);
+        g.ARG[c] = 0xFFFFFFFEu;
+        return;
+    }
+    const uint32_t key = (uint32_t)a.y;
+    const int l1 = (int)(key >> 20), j = (int)((key >> 10) & 1023u), s = (int)(key & 1023u);
+    // bounds check of the decoded split (a corrupt key must not read outside the table)
+    const int l2 = l - l1, jr = q - j, sr = Sp - s;
+    if (l1 < 1 || l2 < 1 || j < 1 || jr < 1 || s < j || sr < jr || s > min(l1, g.M * j) ||
+        sr > min(l2, g.M * jr)) {
+        const int64_t c = pc + d_cell(g, Sp, u, l, aW);
+        g.CELL[c].T1 = __longlong_as_double(0x7ff8000000000000LL);
+        g.ARG[c] = 0xFFFFFFFDu;
+        return;
+    }
+    d_write_winner(g, pc, Sp, u, l, aW, l1, j - 1, s);
+    return;
+}
+
+// The W finalize of one range (profile-range index pr) of wave f.lw by one CTA (k_wave_w's
+// last CTA of the range): fin_w_one's steps in three phases over FB outputs per thread
+// (accumulator loads; child loads; recompute + store) so their memory latencies overlap.
+template <int NT>
+__device__ __forceinline__ void fin_w_range(const DevGeom &g, const FinArgs &f, int pr, int tid) {
+    constexpr int FB = 4;
+    const int l = f.lw, nout = f.nout_w, M = g.M;
+    const int u = pr % f.nranges_w, p = pr / f.nranges_w;
+    const int64_t pc = (int64_t)p * g.C;
+    const int Ql = (l == g.L) ? g.n_hi : max(1, g.n_hi - 1);
+    for (int i0 = tid; i0 < nout; i0 += FB * NT) {
+        int q[FB], Sp[FB];
+        ulonglong2 a[FB];
+#pragma unroll
+        for (int j = 0; j < FB; ++j) {
+            const int i = i0 + j * NT;
+            q[j] = 0;
+            Sp[j] = 0;
+            a[j] = make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull);
+            if (i >= nout) continue;
+            int lo = 1, hi = min(Ql, l);
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (c_woff(M, l, mid) <= i) lo = mid; else hi = mid - 1;
+            }
+            q[j] = lo;
+            Sp[j] = lo + (i - c_woff(M, l, lo));
+            if (lo < 2) continue;
+            ulonglong2 *ga = f.GACC + (int64_t)pr * nout + i;
+            a[j] = __ldcg(ga);
+            __stcg(ga, make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull));
+        }
+        Cell4 Lc[FB], Rc[FB];
+        int l1v[FB], sv[FB], ok[FB];
+#pragma unroll
+        for (int j = 0; j < FB; ++j) {
+            ok[j] = 0;
+            l1v[j] = 0;
+            sv[j] = 0;
+            if (q[j] < 2) continue;
+            const int aW = (M - 1) + q[j] - 1;
+            if (a[j].x >= ACC_EMPTY) {       // no split found: impossible for a valid cell; poison it
+                const int64_t c = pc + d_cell(g, Sp[j], u, l, aW);
+                g.CELL[c].T1 = __longlong_as_double(0x7ff8000000000000LL);
+                g.ARG[c] = 0xFFFFFFFEu;
+                continue;
+            }
+            const uint32_t key = (uint32_t)a[j].y;
+            const int l1 = (int)(key >> 20), jj = (int)((key >> 10) & 1023u), s = (int)(key & 1023u);
+            const int l2 = l - l1, jr = q[j] - jj, sr = Sp[j] - s;
+            if (l1 < 1 || l2 < 1 || jj < 1 || jr < 1 || s < jj || sr < jr || s > min(l1, M * jj) ||
+                sr > min(l2, M * jr)) {      // corrupt key: flag, never read outside the table
+                const int64_t c = pc + d_cell(g, Sp[j], u, l, aW);
+                g.CELL[c].T1 = __longlong_as_double(0x7ff8000000000000LL);
+                g.ARG[c] = 0xFFFFFFFDu;
+                continue;
+            }
+            // children W(jj) of (u, u+l1) and W(jr) of (u+l1, u+l)
+            Lc[j] = d_load(g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + c_ipart(M, l1) + c_woff(M, l1, jj) +
+                           (s - jj));
+            Rc[j] = d_load(g.CELL + pc + g.base[l2] + (int64_t)(u + l1) * g.cells[l2] + c_ipart(M, l2) +
+                           c_woff(M, l2, jr) + (sr - jr));
+            l1v[j] = l1;
+            sv[j] = s | (jj << 16);
+            ok[j] = 1;
+        }
+#pragma unroll
+        for (int j = 0; j < FB; ++j) {
+            if (!ok[j]) continue;
+            const int s = sv[j] & 0xFFFF, jj = sv[j] >> 16;
+            const bool left = Lc[j].TS >= Rc[j].TS;
+            const double kd = left ? d_kd(Lc[j].C1, s) : __dadd_rn((double)s, d_kd(Rc[j].C1, Sp[j] - s));
+            const int64_t c = pc + d_cell(g, Sp[j], u, l, (M - 1) + q[j] - 1);
+            d_store(g.CELL + c, __dadd_rn(Lc[j].T1, Rc[j].T1), left ? __dadd_rn(Lc[j].T3, Rc[j].T1) : Rc[j].T3,
+                    left ? Lc[j].TS : Rc[j].TS, d_c1(kd, Sp[j]));
+            g.ARG[c] = (uint32_t)(l1v[j] - 1) | ((uint32_t)(jj - 1) << 10) | ((uint32_t)s << 20);
+        }
+    }
+}
+
+__device__ __forceinline__ void fin_seed_one(const DevGeom &g, const FinArgs &f, int64_t t) {
+    // ---------------- seeds of wave lseed: per W(q >= 2) output (S', u, u+l, W(q)), the
+    // lexicographic minimum over a few proportional splits (j ~ q/2, s ~ S' j/q,
+    // l1 ~ l s/S'), evaluated exactly as k_wave_w evaluates them (split_total), so the
+    // accumulator starts near the optimum and the flush filter rarely passes.  Children
+    // come from waves <= l-2 (2 <= l1 <= l-2), all final when this kernel runs.
+    const int l = f.lseed;
+    const int nr = g.L - l + 1;
+    const int nout = f.nout_s;
+    if (t >= (int64_t)g.P * nr * nout) return;
+    const int i = (int)(t % nout);
+    const int u = (int)((t / nout) % nr);
+    const int p = (int)(t / ((int64_t)nout * nr));
+    const int M = g.M;
+    const int Ql = (l == g.L) ? g.n_hi : max(1, g.n_hi - 1);
+    int lo = 1, hi = min(Ql, l);
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (c_woff(M, l, mid) <= i) lo = mid; else hi = mid - 1;
+    }
+    const int q = lo, Sp = q + (i - c_woff(M, l, q));
+    unsigned long long bb = ACC_EMPTY;
+    uint32_t bk = 0xFFFFFFFFu;
+    if (q >= 2) {
+        const int64_t pc = (int64_t)p * g.C;
+        const int Qc = max(1, g.n_hi - 1);                 // children are shorter than L
+        for (int jj = 0; jj < 2; ++jj) {
+            const int j = jj == 0 ? q / 2 : (q + 1) / 2;
+            if (jj == 1 && j == q / 2) continue;
+            const int jr = q - j;
+            if (j < 1 || jr < 1 || j > Qc || jr > Qc) continue;
+            for (int ss = 0; ss < 2; ++ss) {
+                const int s = ss == 0 ? (Sp * j) / q : (Sp * j + q - 1) / q;
+                if (ss == 1 && s == (Sp * j) / q) continue;
+                const int sr = Sp - s;
+                if (s < j || sr < jr || s > M * j || sr > M * jr) continue;
+                for (int kk = 0; kk < 3; ++kk) {
+                    const int l1 = (l * s) / Sp + kk - 1;
+                    const int l2 = l - l1;
+                    if (l1 < 2 || l2 < 2 || s > l1 || sr > l2 || j > l1 || jr > l2) continue;
+                    const Cell4 *lc = g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + c_ipart(M, l1) +
+                                      c_woff(M, l1, j) + (s - j);
+                    const Cell4 *rc = g.CELL + pc + g.base[l2] + (int64_t)(u + l1) * g.cells[l2] +
+                                      c_ipart(M, l2) + c_woff(M, l2, jr) + (sr - jr);
+                    const Cell4 L = d_load(lc), R = d_load(rc);
+                    const double cL = __dadd_rn(L.C1, (double)(3 * sr));
+                    const double cR = __dadd_rn(R.C1, (double)(4 * s));
+                    const double tot = split_total(L.T1, L.T3, L.TS, cL, R.T1, R.T3, R.TS, cR);
+                    const unsigned long long tb = (unsigned long long)__double_as_longlong(tot);
+                    const uint32_t key = ((uint32_t)l1 << 20) | ((uint32_t)j << 10) | (uint32_t)s;
+                    if (lex_less(tb, key, bb, bk)) { bb = tb; bk = key; }
+                }
+            }
+        }
+    }
+    // warm start: the argmin splits (l1', j', s') of the same output (q, S') on the two
+    // length-(l-2) sub-ranges [u, u+l-2) and [u+2, u+l), shifted to [u, u+l)
+    if (q >= 2 && l >= 8) {
+        const int64_t pc = (int64_t)p * g.C;
+        const int lp = l - 2;
+        const int Qp = max(1, g.n_hi - 1);
+        if (q <= Qp && q <= lp && Sp <= min(lp, M * q)) {
+#pragma unroll 1
+            for (int side = 0; side < 2; ++side) {
+                const int up = u + 2 * side;
+                const uint32_t arg = g.ARG[pc + g.base[lp] + (int64_t)up * g.cells[lp] + c_ipart(M, lp) +
+                                           c_woff(M, lp, q) + (Sp - q)];
+                if (arg >= 0xFFFFFFFEu) continue;
+                const int l1p = (int)(arg & 1023u) + 1 + 2 * side, j = (int)((arg >> 10) & 1023u) + 1;
+                const int s = (int)(arg >> 20);
+                const int jr = q - j, sr = Sp - s;
+#pragma unroll 1
+                for (int d = 0; d < 3; ++d) {
+                    const int l1 = l1p + d - side;   // shifts 0..2 (left range) / 1..3 - 1 (right)
+                    const int l2 = l - l1;
+                    if (l1 < 2 || l2 < 2 || s > l1 || sr > l2 || j > l1 || jr > l2 || jr < 1) continue;
+                    const Cell4 *lc = g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + c_ipart(M, l1) +
+                                      c_woff(M, l1, j) + (s - j);
+                    const Cell4 *rc = g.CELL + pc + g.base[l2] + (int64_t)(u + l1) * g.cells[l2] +
+                                      c_ipart(M, l2) + c_woff(M, l2, jr) + (sr - jr);
+                    if (s < j || sr < jr || s > M * j || sr > M * jr) continue;
+                    const Cell4 Lc = d_load(lc), Rc = d_load(rc);
+                    const double cL = __dadd_rn(Lc.C1, (double)(3 * sr));
+                    const double cR = __dadd_rn(Rc.C1, (double)(4 * s));
+                    const double tot = split_total(Lc.T1, Lc.T3, Lc.TS, cL, Rc.T1, Rc.T3, Rc.TS, cR);
+                    const unsigned long long tb = (unsigned long long)__double_as_longlong(tot);
+                    const uint32_t key = ((uint32_t)l1 << 20) | ((uint32_t)j << 10) | (uint32_t)s;
+                    if (lex_less(tb, key, bb, bk)) { bb = tb; bk = key; }
+                }
+            }
+        }
+    }
+    __stcg(f.GSEED + t, make_ulonglong2(bb, (unsigned long long)bk));
+    return;
+}
+
+// Small cells of wave f.ls: block `bid` of the small part (256 threads, f.tpc <= 32 threads per cell).
+__device__ __forceinline__ void fin_small_block(const DevGeom &g, const FinArgs &f, int64_t bid) {
+    const int l = f.ls;
+    const int nr = g.L - l + 1;
+    const int cpb = blockDim.x / f.tpc;                      // cells per block
+    const int sub = threadIdx.x / f.tpc, tl = threadIdx.x % f.tpc;
+    const int64_t cell = bid * cpb + sub;
+    const bool active = cell < (int64_t)g.P * nr * f.nsmall;
+    double best = D_INF;
+    uint32_t bkey = 0xFFFFFFFFu;
+    int u = 0, p = 0, a = 0, Sp = 0;
+    if (active) {
+        int rem = (int)(cell % f.nsmall);
+        u = (int)((cell / f.nsmall) % nr);
+        p = (int)(cell / ((int64_t)f.nsmall * nr));
+        const int nsm = min(g.A, g.M);                       // alloc indices 0..M-1: I(1..M-1), W(1)
+        for (int aa = 0; aa < nsm; ++aa) {
+            const int c = max(0, d_hi(g, aa, l) - 1);
+            if (rem < c) { a = aa; Sp = 2 + rem; break; }
+            rem -= c;
+        }
+        const int64_t pc = (int64_t)p * g.C;
+        const double dSp3 = (double)(3 * Sp - 1);
+        const int r = d_is_whole(g, a) ? g.M : d_alloc_n(g, a);  // GPUs of the cell's node part
+        const int nd = r - 1;                                    // device splits (I(m), I(r-m))
+        // a thread takes layer splits l1 = 1 + tl, 1 + tl + tpc, ... and, for each, every
+        // device split m and stage split s (ascending, strict "<": the first minimum in
+        // (k, m, s) order).  I(m) of a slab of length l' starts at c_ipart(m, l') (I(1..m-1)
+        // before it; W(1) plays "I(M)" right after I(M-1)).
+        const Cell4 *CP = g.CELL + pc;
+        for (int l1 = 1 + tl; l1 < l; l1 += f.tpc) {
+            const int k = u + l1, l2 = l - l1;
+            const Cell4 *lrow = CP + g.base[l1] + (int64_t)u * g.cells[l1] - 1;
+            const Cell4 *rrow = CP + g.base[l2] + (int64_t)k * g.cells[l2] - 1;
+            for (int m = 1; m <= nd; ++m) {
+                const int s_lo = max(1, Sp - min(l2, r - m));
+                const int s_hi = min(Sp - 1, min(l1, m));
+                const Cell4 *lb = lrow + c_ipart(m, l1);
+                const Cell4 *rb = rrow + c_ipart(r - m, l2) + Sp;
+                for (int s = s_lo; s <= s_hi; ++s) {
+                    const Cell4 Lc = d_load(lb + s);
+                    const Cell4 Rc = d_load(rb - s);
+                    const double T1 = __dadd_rn(Lc.T1, Rc.T1);
+                    const bool left = Lc.TS >= Rc.TS;
+                    const double T3 = left ? __dadd_rn(Lc.T3, Rc.T1) : Rc.T3;
+                    const double TS = left ? Lc.TS : Rc.TS;
+                    const double KD = left ? d_kd(Lc.C1, s) : __dadd_rn((double)s, d_kd(Rc.C1, Sp - s));
+                    const double T2 = __dmul_rn(__dadd_rn(KD, dSp3), TS);
+                    const double tot = __dadd_rn(__dadd_rn(T1, T2), T3);
+                    if (tot < best) {
+                        best = tot;
+                        bkey = ((uint32_t)l1 << 20) | ((uint32_t)(m - 1) << 10) | (uint32_t)s;
+                    }
+                }
+            }
+        }
+    }
+    // lexicographic (total, key) reduction over the tpc threads of the cell (segments of
+    // width tpc <= 32 inside a warp)
+    const int wd = min(f.tpc, 32);
+    for (int d = wd >> 1; d >= 1; d >>= 1) {
+        const double ob = __shfl_down_sync(0xFFFFFFFFu, best, d, wd);
+        const uint32_t ok = __shfl_down_sync(0xFFFFFFFFu, bkey, d, wd);
+        if (ob < best || (ob == best && ok < bkey)) { best = ob; bkey = ok; }
+    }
+    if (tl != 0) return;
+    if (!active) return;
+    d_write_winner(g, (int64_t)p * g.C, Sp, u, l, a, (int)(bkey >> 20), (int)((bkey >> 10) & 1023u),
+                   (int)(bkey & 1023u));
+}
+
+__global__ void __launch_bounds__(256) k_fin(DevGeom g, FinArgs f) {
+    if ((int)blockIdx.x < f.nbw) {
+        const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if (t < (int64_t)g.P * f.nranges_w * f.nout_w) fin_w_one(g, f, t);
+        return;
+    }
+    if ((int)blockIdx.x < f.nbw + f.nbseed) {
+        fin_seed_one(g, f, (int64_t)(blockIdx.x - f.nbw) * blockDim.x + threadIdx.x);
+        return;
+    }
+    fin_small_block(g, f, (int64_t)blockIdx.x - f.nbw - f.nbseed);
+}
+
 template <int TE>
 __global__ void __launch_bounds__(NTW, 2) k_wave_w(DevGeom g, WaveW w) {
     extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_last;
+    if ((int)blockIdx.x >= w.nbmain) {        // next wave's seeds and in-node cells
+        const int ab = (int)blockIdx.x - w.nbmain;
+        if (ab < w.fa.nbseed)
+            fin_seed_one(g, w.fa, (int64_t)ab * NTW + threadIdx.x);
+        else
+            fin_small_block(g, w.fa, (int64_t)ab - w.fa.nbseed);
+        return;
+    }
     const int l = w.l;
     const int nout = w.nout;
     const int L = g.L, M = g.M;
@@ -470,254 +811,21 @@ __global__ void __launch_bounds__(NTW, 2) k_wave_w(DevGeom g, WaveW w) {
             }
         }
     }
+    if (w.fin_inline) {                        // the range's last CTA finalizes its W outputs
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) s_last = atomicAdd(w.rdone + pr, 1) == w.cpr - 1;
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            fin_w_range<NTW>(g, w.fw, pr, tid);
+        }
+    }
 }
 
 __global__ void k_gacc_init(ulonglong2 *gacc, int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) gacc[i] = make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull);
-}
-
-// Per-wave finalize + small cells.  Blocks [0, nbw): one thread per (profile, range, W-part
-// cell) of wave lw (lw >= 2): read + reset the global accumulator, recompute the winner.
-// Blocks [nbw, ...): cells inside one node (I(r), W(1), S' >= 2) of wave ls (2 <= ls <= L):
-// `tpc` threads per cell (32..256, power of two) split the (k, m) pairs of the cell, scan
-// s, keep the first strictly smaller total, then a lexicographic (total, key) reduction.
-struct FinArgs {
-    int lw, nranges_w, nout_w;     // W finalize of wave lw (lw = 0: none)
-    int nbw;                       // blocks of the W part
-    ulonglong2 *GACC;              // accumulator of wave lw (this rank's)
-    const ulonglong2 *GPART;       // world > 1: all ranks' partial accumulators [world][entries]
-    int64_t part_stride;           // entries per rank in GPART
-    int world;
-    int lseed, nout_s, nbseed;     // seeds of wave lseed (0: none): W outputs per range, blocks
-    ulonglong2 *GSEED;             // accumulator of wave lseed (the other parity buffer)
-    int ls, nsmall;                // small cells of wave ls (ls = 0: none); cells per range
-    int tpc;                       // threads per small cell
-};
-
-__global__ void __launch_bounds__(256) k_fin(DevGeom g, FinArgs f) {
-    __shared__ double red_b[8];
-    __shared__ uint32_t red_k[8];
-    if ((int)blockIdx.x < f.nbw) {
-        const int l = f.lw;
-        const int nout = f.nout_w;
-        const int64_t n = (int64_t)g.P * f.nranges_w * nout;
-        const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-        if (t >= n) return;
-        const int i = (int)(t % nout);
-        const int u = (int)((t / nout) % f.nranges_w);
-        const int p = (int)(t / ((int64_t)nout * f.nranges_w));
-        const int Ql = (l == g.L) ? g.n_hi : max(1, g.n_hi - 1);
-        // row q of the W-part cell i: largest q with c_woff(q) <= i (binary search, closed form)
-        int lo = 1, hi = min(Ql, l);
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (c_woff(g.M, l, mid) <= i) lo = mid; else hi = mid - 1;
-        }
-        const int q = lo, Sp = q + (i - c_woff(g.M, l, q));
-        if (q < 2) return;        // W(1) cell (computed with the small cells)
-        ulonglong2 *ga = f.GACC + t;
-        ulonglong2 a = __ldcg(ga);
-        __stcg(ga, make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull));
-        for (int r = 0; r < f.world && f.world > 1; ++r) {   // lexicographic min over the ranks
-            const ulonglong2 b = __ldcg(f.GPART + (int64_t)r * f.part_stride + t);
-            if (lex_less(b.x, (uint32_t)b.y, a.x, (uint32_t)a.y)) a = b;
-        }
-        const int64_t pc = (int64_t)p * g.C;
-        const int aW = (g.M - 1) + q - 1;
-        if (a.x >= ACC_EMPTY) {   // no split found: impossible for a valid cell; poison it
-            const int64_t c = pc + d_cell(g, Sp, u, l, aW);
-            g.CELL[c].T1 = __longlong_as_double(0x7ff8000000000000LL);
-            g.ARG[c] = 0xFFFFFFFEu;
-            return;
-        }
-        const uint32_t key = (uint32_t)a.y;
-        const int l1 = (int)(key >> 20), j = (int)((key >> 10) & 1023u), s = (int)(key & 1023u);
-        // bounds check of the decoded split (a corrupt key must not read outside the table)
-        const int l2 = l - l1, jr = q - j, sr = Sp - s;
-        if (l1 < 1 || l2 < 1 || j < 1 || jr < 1 || s < j || sr < jr || s > min(l1, g.M * j) ||
-            sr > min(l2, g.M * jr)) {
-            const int64_t c = pc + d_cell(g, Sp, u, l, aW);
-            g.CELL[c].T1 = __longlong_as_double(0x7ff8000000000000LL);
-            g.ARG[c] = 0xFFFFFFFDu;
-            return;
-        }
-        d_write_winner(g, pc, Sp, u, l, aW, l1, j - 1, s);
-        return;
-    }
-    if ((int)blockIdx.x < f.nbw + f.nbseed) {
-        // ---------------- seeds of wave lseed: per W(q >= 2) output (S', u, u+l, W(q)), the
-        // lexicographic minimum over a few proportional splits (j ~ q/2, s ~ S' j/q,
-        // l1 ~ l s/S'), evaluated exactly as k_wave_w evaluates them (split_total), so the
-        // accumulator starts near the optimum and the flush filter rarely passes.  Children
-        // come from waves <= l-2 (2 <= l1 <= l-2), all final when this kernel runs.
-        const int l = f.lseed;
-        const int nr = g.L - l + 1;
-        const int nout = f.nout_s;
-        const int64_t t = (int64_t)(blockIdx.x - f.nbw) * blockDim.x + threadIdx.x;
-        if (t >= (int64_t)g.P * nr * nout) return;
-        const int i = (int)(t % nout);
-        const int u = (int)((t / nout) % nr);
-        const int p = (int)(t / ((int64_t)nout * nr));
-        const int M = g.M;
-        const int Ql = (l == g.L) ? g.n_hi : max(1, g.n_hi - 1);
-        int lo = 1, hi = min(Ql, l);
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (c_woff(M, l, mid) <= i) lo = mid; else hi = mid - 1;
-        }
-        const int q = lo, Sp = q + (i - c_woff(M, l, q));
-        unsigned long long bb = ACC_EMPTY;
-        uint32_t bk = 0xFFFFFFFFu;
-        if (q >= 2) {
-            const int64_t pc = (int64_t)p * g.C;
-            const int Qc = max(1, g.n_hi - 1);                 // children are shorter than L
-            for (int jj = 0; jj < 2; ++jj) {
-                const int j = jj == 0 ? q / 2 : (q + 1) / 2;
-                if (jj == 1 && j == q / 2) continue;
-                const int jr = q - j;
-                if (j < 1 || jr < 1 || j > Qc || jr > Qc) continue;
-                for (int ss = 0; ss < 2; ++ss) {
-                    const int s = ss == 0 ? (Sp * j) / q : (Sp * j + q - 1) / q;
-                    if (ss == 1 && s == (Sp * j) / q) continue;
-                    const int sr = Sp - s;
-                    if (s < j || sr < jr || s > M * j || sr > M * jr) continue;
-                    for (int kk = 0; kk < 3; ++kk) {
-                        const int l1 = (l * s) / Sp + kk - 1;
-                        const int l2 = l - l1;
-                        if (l1 < 2 || l2 < 2 || s > l1 || sr > l2 || j > l1 || jr > l2) continue;
-                        const Cell4 *lc = g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + c_ipart(M, l1) +
-                                          c_woff(M, l1, j) + (s - j);
-                        const Cell4 *rc = g.CELL + pc + g.base[l2] + (int64_t)(u + l1) * g.cells[l2] +
-                                          c_ipart(M, l2) + c_woff(M, l2, jr) + (sr - jr);
-                        const Cell4 L = d_load(lc), R = d_load(rc);
-                        const double cL = __dadd_rn(L.C1, (double)(3 * sr));
-                        const double cR = __dadd_rn(R.C1, (double)(4 * s));
-                        const double tot = split_total(L.T1, L.T3, L.TS, cL, R.T1, R.T3, R.TS, cR);
-                        const unsigned long long tb = (unsigned long long)__double_as_longlong(tot);
-                        const uint32_t key = ((uint32_t)l1 << 20) | ((uint32_t)j << 10) | (uint32_t)s;
-                        if (lex_less(tb, key, bb, bk)) { bb = tb; bk = key; }
-                    }
-                }
-            }
-        }
-        // warm start: the argmin splits (l1', j', s') of the same output (q, S') on the two
-        // length-(l-2) sub-ranges [u, u+l-2) and [u+2, u+l), shifted to [u, u+l)
-        if (q >= 2 && l >= 8) {
-            const int64_t pc = (int64_t)p * g.C;
-            const int lp = l - 2;
-            const int Qp = max(1, g.n_hi - 1);
-            if (q <= Qp && q <= lp && Sp <= min(lp, M * q)) {
-#pragma unroll 1
-                for (int side = 0; side < 2; ++side) {
-                    const int up = u + 2 * side;
-                    const uint32_t arg = g.ARG[pc + g.base[lp] + (int64_t)up * g.cells[lp] + c_ipart(M, lp) +
-                                               c_woff(M, lp, q) + (Sp - q)];
-                    if (arg >= 0xFFFFFFFEu) continue;
-                    const int l1p = (int)(arg & 1023u) + 1 + 2 * side, j = (int)((arg >> 10) & 1023u) + 1;
-                    const int s = (int)(arg >> 20);
-                    const int jr = q - j, sr = Sp - s;
-#pragma unroll 1
-                    for (int d = 0; d < 3; ++d) {
-                        const int l1 = l1p + d - side;   // shifts 0..2 (left range) / 1..3 - 1 (right)
-                        const int l2 = l - l1;
-                        if (l1 < 2 || l2 < 2 || s > l1 || sr > l2 || j > l1 || jr > l2 || jr < 1) continue;
-                        const Cell4 *lc = g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + c_ipart(M, l1) +
-                                          c_woff(M, l1, j) + (s - j);
-                        const Cell4 *rc = g.CELL + pc + g.base[l2] + (int64_t)(u + l1) * g.cells[l2] +
-                                          c_ipart(M, l2) + c_woff(M, l2, jr) + (sr - jr);
-                        if (s < j || sr < jr || s > M * j || sr > M * jr) continue;
-                        const Cell4 Lc = d_load(lc), Rc = d_load(rc);
-                        const double cL = __dadd_rn(Lc.C1, (double)(3 * sr));
-                        const double cR = __dadd_rn(Rc.C1, (double)(4 * s));
-                        const double tot = split_total(Lc.T1, Lc.T3, Lc.TS, cL, Rc.T1, Rc.T3, Rc.TS, cR);
-                        const unsigned long long tb = (unsigned long long)__double_as_longlong(tot);
-                        const uint32_t key = ((uint32_t)l1 << 20) | ((uint32_t)j << 10) | (uint32_t)s;
-                        if (lex_less(tb, key, bb, bk)) { bb = tb; bk = key; }
-                    }
-                }
-            }
-        }
-        __stcg(f.GSEED + t, make_ulonglong2(bb, (unsigned long long)bk));
-        return;
-    }
-    // ---------------- small cells of wave ls
-    const int l = f.ls;
-    const int nr = g.L - l + 1;
-    const int cpb = blockDim.x / f.tpc;                      // cells per block
-    const int sub = threadIdx.x / f.tpc, tl = threadIdx.x % f.tpc;
-    const int64_t cell = (int64_t)(blockIdx.x - f.nbw - f.nbseed) * cpb + sub;
-    const bool active = cell < (int64_t)g.P * nr * f.nsmall;
-    double best = D_INF;
-    uint32_t bkey = 0xFFFFFFFFu;
-    int u = 0, p = 0, a = 0, Sp = 0;
-    if (active) {
-        int rem = (int)(cell % f.nsmall);
-        u = (int)((cell / f.nsmall) % nr);
-        p = (int)(cell / ((int64_t)f.nsmall * nr));
-        const int nsm = min(g.A, g.M);                       // alloc indices 0..M-1: I(1..M-1), W(1)
-        for (int aa = 0; aa < nsm; ++aa) {
-            const int c = max(0, d_hi(g, aa, l) - 1);
-            if (rem < c) { a = aa; Sp = 2 + rem; break; }
-            rem -= c;
-        }
-        const int64_t pc = (int64_t)p * g.C;
-        const double dSp3 = (double)(3 * Sp - 1);
-        const int r = d_is_whole(g, a) ? g.M : d_alloc_n(g, a);  // GPUs of the cell's node part
-        const int nd = r - 1;                                    // device splits (I(m), I(r-m))
-        // a thread takes layer splits l1 = 1 + tl, 1 + tl + tpc, ... and, for each, every
-        // device split m and stage split s (ascending, strict "<": the first minimum in
-        // (k, m, s) order).  I(m) of a slab of length l' starts at c_ipart(m, l') (I(1..m-1)
-        // before it; W(1) plays "I(M)" right after I(M-1)).
-        const Cell4 *CP = g.CELL + pc;
-        for (int l1 = 1 + tl; l1 < l; l1 += f.tpc) {
-            const int k = u + l1, l2 = l - l1;
-            const Cell4 *lrow = CP + g.base[l1] + (int64_t)u * g.cells[l1] - 1;
-            const Cell4 *rrow = CP + g.base[l2] + (int64_t)k * g.cells[l2] - 1;
-            for (int m = 1; m <= nd; ++m) {
-                const int s_lo = max(1, Sp - min(l2, r - m));
-                const int s_hi = min(Sp - 1, min(l1, m));
-                const Cell4 *lb = lrow + c_ipart(m, l1);
-                const Cell4 *rb = rrow + c_ipart(r - m, l2) + Sp;
-                for (int s = s_lo; s <= s_hi; ++s) {
-                    const Cell4 Lc = d_load(lb + s);
-                    const Cell4 Rc = d_load(rb - s);
-                    const double T1 = __dadd_rn(Lc.T1, Rc.T1);
-                    const bool left = Lc.TS >= Rc.TS;
-                    const double T3 = left ? __dadd_rn(Lc.T3, Rc.T1) : Rc.T3;
-                    const double TS = left ? Lc.TS : Rc.TS;
-                    const double KD = left ? d_kd(Lc.C1, s) : __dadd_rn((double)s, d_kd(Rc.C1, Sp - s));
-                    const double T2 = __dmul_rn(__dadd_rn(KD, dSp3), TS);
-                    const double tot = __dadd_rn(__dadd_rn(T1, T2), T3);
-                    if (tot < best) {
-                        best = tot;
-                        bkey = ((uint32_t)l1 << 20) | ((uint32_t)(m - 1) << 10) | (uint32_t)s;
-                    }
-                }
-            }
-        }
-    }
-    // lexicographic (total, key) reduction over the tpc threads of the cell (segments of
-    // width min(tpc, 32) inside a warp, then across the cell's warps)
-    const int wd = min(f.tpc, 32);
-    for (int d = wd >> 1; d >= 1; d >>= 1) {
-        const double ob = __shfl_down_sync(0xFFFFFFFFu, best, d, wd);
-        const uint32_t ok = __shfl_down_sync(0xFFFFFFFFu, bkey, d, wd);
-        if (ob < best || (ob == best && ok < bkey)) { best = ob; bkey = ok; }
-    }
-    if (f.tpc > 32) {
-        const int wid = threadIdx.x >> 5;
-        if ((threadIdx.x & 31) == 0) { red_b[wid] = best; red_k[wid] = bkey; }
-        __syncthreads();
-        if ((threadIdx.x & 31) != 0 || tl != 0) return;
-        for (int w2 = wid + 1; w2 < wid + f.tpc / 32; ++w2)
-            if (red_b[w2] < best || (red_b[w2] == best && red_k[w2] < bkey)) { best = red_b[w2]; bkey = red_k[w2]; }
-    } else if (tl != 0) {
-        return;
-    }
-    if (!active) return;
-    d_write_winner(g, (int64_t)p * g.C, Sp, u, l, a, (int)(bkey >> 20), (int)((bkey >> 10) & 1023u),
-                   (int)(bkey & 1023u));
 }
 
 }  // namespace oob

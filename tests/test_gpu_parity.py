@@ -82,10 +82,14 @@ def test_batched_profiles_vs_oracle(planner):
         _assert_same(ts.templates(i), want, f"cfg5 profile {i}")
 
 
+@pytest.mark.parametrize("fuse", ["default", "0", "1"])
 @pytest.mark.parametrize("mode", ["real", "dyadic"])
-def test_cfg4_full_vs_golden(planner, mode):
+def test_cfg4_full_vs_golden(planner, mode, fuse, monkeypatch):
     """Full template set of the north-star config (96 layers, 512 x 8 GPUs, f=4, n0=3)
-    vs the C oracle's output stored by scripts/make_golden.py."""
+    vs the C oracle's output stored by scripts/make_golden.py; with the finalize fused into
+    k_wave_w (OOB_DP_FUSE=1) and as separate k_fin launches (0)."""
+    if fuse != "default":
+        monkeypatch.setenv("OOB_DP_FUSE", fuse)
     rec = load_golden("cfg4", mode)
     if rec is None:
         pytest.skip(f"tests/golden/cfg4_{mode}.json not generated")
@@ -156,15 +160,31 @@ def test_v1_kernel_still_matches(planner, key, monkeypatch):
     _assert_same(ts.templates(0), want, key + " v1")
 
 
+VARIANTS = [
+    {"OOB_DP_WCFG": "1"},            # TE = 5 register tile
+    {"OOB_DP_WCFG": "2"},            # TE = 3
+    {"OOB_DP_WCFG": "3"},            # TE = 2
+    {"OOB_DP_FUSE": "0"},            # separate k_fin launches
+    {"OOB_DP_FUSE": "1"},            # finalize + next wave's in-node cells inside k_wave_w
+    {"OOB_DP_SEEDSPO": "0"},         # every wave >= 6 seeded
+    {"OOB_DP_SEEDINIT": "0"},        # no seeds
+    {"OOB_DP_SMALLPAIRS": "4"},      # fewer threads per in-node cell
+]
+
+
+@pytest.mark.parametrize("env", VARIANTS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 @pytest.mark.parametrize("key", ["cfg2", "cfg3"])
-def test_te5_kernel_config_matches(planner, key, monkeypatch):
-    """The alternative W-kernel configuration (TE = 5 register tile, OOB_DP_WCFG=1)."""
-    monkeypatch.setenv("OOB_DP_WCFG", "1")
+def test_kernel_variants_match(planner, key, env, monkeypatch):
+    """Alternative W-kernel configurations and finalize / seeding modes (plan-time switches)
+    all give the oracle's template sets."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     cfg = CONFIGS[key]
-    prof = config_profiles(cfg, "real")[0]
-    ts = _gpu_set(planner, [prof], (cfg.L, cfg.M, cfg.N, cfg.f, cfg.n0))
-    want, _ = coracle.template_set(prof.fwd_ms, prof.bwd_ms, cfg.M, cfg.n0, cfg.n_max)
-    _assert_same(ts.templates(0), want, key + " TE5")
+    for mode in ("real", "dyadic"):
+        prof = config_profiles(cfg, mode)[0]
+        ts = _gpu_set(planner, [prof], (cfg.L, cfg.M, cfg.N, cfg.f, cfg.n0))
+        want, _ = coracle.template_set(prof.fwd_ms, prof.bwd_ms, cfg.M, cfg.n0, cfg.n_max)
+        _assert_same(ts.templates(0), want, f"{key} {mode} {env}")
 
 
 def test_cfg5_full_sweep_sampled(planner):
