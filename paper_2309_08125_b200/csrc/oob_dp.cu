@@ -247,6 +247,7 @@ struct oob_dp_plan {
     size_t ctr_n = 0;
     std::vector<int32_t> tiles;          // all TE's tables concatenated
     TileTab tab[NWCFG];                  // per WCFGS entry (TE = 4, 5, 3, 2)
+    std::vector<double> stream_steps;    // [L+1] cost-model steps of streaming a slab of length ls
     std::vector<WaveHost> waves;         // [L+1]
     size_t max_smem = 0;
     int64_t launches = 0;
@@ -290,12 +291,9 @@ static void build_tiles(oob_dp_plan *pl, int TE) {
 // (32 lanes) walks its rows; a step costs TE splits (~20 instructions each) plus the load
 // and the merge (~24).
 static double k_cost(const oob_dp_plan *pl, int TE, int l, int l1, bool lt) {
-    const Geometry &g = pl->g;
     const int l2 = l - l1;
     const int ls = lt ? l2 : l1, lb = lt ? l1 : l2;       // streamed side, tiled side
-    const int JS = std::min(Q_of(g, ls), ls);
-    double steps = 0.0;
-    for (int r = 1; r <= JS; ++r) steps += wlen_h(g, ls, r) + 6.0;   // + per-row tail/flush/setup
+    const double steps = pl->stream_steps[ls];             // rows + per-row tail/flush/setup
     const double units = (pl->tab[te_index(TE)].cnt[lb] + 31) / 32;
     return units * (steps * (TE * 20.0 + 24.0) + 400.0);
 }
@@ -390,6 +388,11 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     if (const char *po = std::getenv("OOB_DP_PERM")) pl->perm_order = std::atoi(po) != 0;
     if (const char *rv = std::getenv("OOB_DP_REV")) pl->rev_lanes = std::atoi(rv) != 0;
     for (int ci = 0; ci < NWCFG; ++ci) build_tiles(pl, WCFGS[ci].te);
+    pl->stream_steps.assign(L + 1, 0.0);
+    for (int ls = 1; ls <= L; ++ls) {
+        const int JS = std::min(Q_of(pl->g, ls), ls);
+        for (int r = 1; r <= JS; ++r) pl->stream_steps[ls] += wlen_h(pl->g, ls, r) + 6.0;
+    }
     pl->waves.assign(L + 1, WaveHost());
     size_t items_total = 0, gacc_max = 0, ctr_total = 0;
     for (int l = 2; l <= L; ++l) {
@@ -498,6 +501,11 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     }
     *out = pl;
     return OOB_OK;
+}
+
+void oob::dp_plan_invalidate(oob_dp_plan *pl) {
+    pl->uploaded_to = nullptr;
+    pl->gacc_ready = nullptr;
 }
 
 extern "C" void oob_dp_plan_free(oob_dp_plan *pl) {

@@ -61,13 +61,16 @@ bool build_geometry(int L, int M, int n_lo, int n_hi, Geometry &g) {
     auto LW = [&](int l, int q) { return lenW[(size_t)l * (n_hi + 1) + q]; };
     auto LI = [&](int l, int r) { return lenI[(size_t)l * (M + 1) + r]; };
     g.total_splits = 0;
+    std::vector<int64_t> pre((size_t)n_hi + 1, 0);
     for (int l = 2; l <= L; ++l) {
         int64_t per_range = 0;
+        const int Q = g.Q[l];
         for (int l1 = 1; l1 < l; ++l1) {
             int l2 = l - l1;
-            // W(q >= 2) -> (W(j), W(q-j))
-            for (int q = 2; q <= g.Q[l]; ++q)
-                for (int j = 1; j < q; ++j) per_range += LW(l1, j) * LW(l2, q - j);
+            // W(q >= 2) -> (W(j), W(q-j)): sum over 2 <= q <= Q, 1 <= j < q of
+            // LW(l1, j) LW(l2, q-j) = sum_j LW(l1, j) * (LW(l2, 1) + ... + LW(l2, Q-j))
+            for (int m = 1; m <= Q; ++m) pre[m] = pre[m - 1] + LW(l2, m);
+            for (int j = 1; j < Q; ++j) per_range += LW(l1, j) * pre[Q - j];
             // W(1) -> (I(m), I(M-m))
             for (int m = 1; m < M; ++m) per_range += LI(l1, m) * LI(l2, M - m);
             // I(r) -> (I(m), I(r-m))

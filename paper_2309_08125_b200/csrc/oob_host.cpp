@@ -13,6 +13,7 @@
 #include <fstream>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <sstream>
 #include <string>
@@ -318,6 +319,52 @@ extern "C" oob_status oob_template_get(const oob_template_set *s, int32_t profil
 }
 extern "C" void oob_template_set_free(oob_template_set *s) { delete s; }
 
+// Plans (host geometry + unit queues, a few ms to build at cfg4) are cached across
+// oob_generate_templates calls, keyed by shape, device and the OOB_DP_* plan switches; a
+// plan is taken out of the cache while in use, so concurrent calls never share one.
+namespace {
+struct PlanCache {
+    std::mutex mu;
+    std::vector<std::pair<std::string, oob_dp_plan *>> plans;   // most recent last
+};
+PlanCache &plan_cache() {
+    static PlanCache *c = new PlanCache();   // never destroyed: no CUDA calls at exit
+    return *c;
+}
+std::string plan_key(int L, int M, int n_lo, int n_hi, int P, int dev) {
+    std::string k = std::to_string(L) + "," + std::to_string(M) + "," + std::to_string(n_lo) + "," +
+                    std::to_string(n_hi) + "," + std::to_string(P) + "," + std::to_string(dev);
+    static const char *knobs[] = {"OOB_DP_KERNEL", "OOB_DP_WCFG", "OOB_DP_AUTOCFGS", "OOB_DP_UPC", "OOB_DP_SEED",
+                                  "OOB_DP_SEEDINIT", "OOB_DP_SEEDSPO", "OOB_DP_SMALLPAIRS", "OOB_DP_FUSE",
+                                  "OOB_DP_PERM", "OOB_DP_REV"};
+    for (const char *n : knobs) {
+        const char *v = std::getenv(n);
+        k += std::string("|") + (v ? v : "");
+    }
+    return k;
+}
+oob_dp_plan *take_plan(const std::string &key) {
+    PlanCache &c = plan_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    for (size_t i = c.plans.size(); i-- > 0;)
+        if (c.plans[i].first == key) {
+            oob_dp_plan *p = c.plans[i].second;
+            c.plans.erase(c.plans.begin() + (long)i);
+            return p;
+        }
+    return nullptr;
+}
+void give_plan(const std::string &key, oob_dp_plan *p) {
+    PlanCache &c = plan_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.plans.emplace_back(key, p);
+    while (c.plans.size() > 4) {
+        oob_dp_plan_free(c.plans.front().second);
+        c.plans.erase(c.plans.begin());
+    }
+}
+}  // namespace
+
 extern "C" oob_status oob_generate_templates(const oob_profile *const *profiles, int32_t num_profiles,
                                              const oob_plan_opts *opts, oob_template_set **out) {
     if (!profiles || !opts || !out || num_profiles < 1)
@@ -352,10 +399,21 @@ extern "C" oob_status oob_generate_templates(const oob_profile *const *profiles,
         if (e != cudaSuccess) return fail(OOB_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
     }
     cudaStream_t stream = (cudaStream_t)opts->stream;
-    oob_dp_plan *plan = nullptr;
-    st = oob_dp_plan_create(L, M, n_lo, n_hi, num_profiles, &plan);
-    if (st != OOB_OK) return st;
-    std::unique_ptr<oob_dp_plan, void (*)(oob_dp_plan *)> plan_guard(plan, oob_dp_plan_free);
+    int dev = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess)
+        return fail(OOB_E_CUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
+    const std::string key = plan_key(L, M, n_lo, n_hi, num_profiles, dev);
+    oob_dp_plan *plan = take_plan(key);
+    if (!plan) {
+        st = oob_dp_plan_create(L, M, n_lo, n_hi, num_profiles, &plan);
+        if (st != OOB_OK) return st;
+    }
+    dp_plan_invalidate(plan);   // the workspace may be new memory at an old address
+    struct Return {
+        std::string key;
+        oob_dp_plan *p;
+        ~Return() { give_plan(key, p); }
+    } plan_guard{key, plan};
     oob_dp_info info;
     oob_dp_plan_info(plan, &info);
 
