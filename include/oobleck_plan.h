@@ -198,8 +198,10 @@ oob_status oob_template_set_from_packed(const void *h_packed, const oob_dp_info 
  *  num_feasible_out: number of feasible X (saturates at INT64_MAX)
  * max_enumerated <= 0 means 1e6.  Errors: OOB_E_INFEASIBLE (N' < (f+1) n0 or no X),
  * OOB_E_BATCH (no X can be distributed; *recommended_batch_out is set), OOB_E_TOO_MANY
- * (more than max_enumerated X: outputs hold the best of the first max_enumerated),
- * OOB_E_NOMEM (max_pipelines too small). */
+ * (more than max_enumerated X, e.g. 2.2e19 at 512 nodes: not enumerated; the outputs hold
+ * the best, scored exactly as above, of the knapsack candidates — for each fill/drain
+ * overhead threshold, the X of maximum total microbatch rate sum x_i / t*_i among the
+ * templates under it — a heuristic, reading R20), OOB_E_NOMEM (max_pipelines too small). */
 oob_status oob_instantiate(const oob_template_set *set, int32_t profile, int32_t nodes,
                            int32_t f, int64_t global_batch, int32_t microbatch,
                            int64_t max_enumerated, int32_t *counts_out, int64_t *nb_out,

@@ -225,6 +225,136 @@ void dfs(InstCtx &c, int i, int rem) {
     c.x[i] = 0;
 }
 
+// Candidates when Eq.5's list is too long to enumerate (cfg4: 2.2e19 sets).  With the
+// batch balanced, a plan's iteration time is about K / R + overhead, R = sum_i x_i / t*_i
+// (the pipelines' total microbatch rate) and overhead = max over used templates of the
+// fill/drain term T1 + T3 - (S - k* + 1) t*.  Unbounded knapsacks over nodes (exactly N
+// used) maximise R:
+//   (1) for every overhead threshold (templates sorted by it), among the templates under
+//       it, with >= f+1 pipelines (saturating pipeline-count bucket 0..f+1);
+//   (2) among all templates, for every exact pipeline count c = f+1 .. min(K, N/n0) (few
+//       microbatches per pipeline make the integer split matter; c <= K keeps the batch
+//       distributable).
+// Every candidate is then scored exactly (Eq.6 + iteration time) like an enumerated set.
+std::vector<std::vector<int32_t>> knapsack_candidates(const oob_template *tpl, int p, int n_lo, int N, int f,
+                                                      int64_t K) {
+    std::vector<int> order(p);
+    std::vector<double> over(p), rate(p);
+    for (int i = 0; i < p; ++i) {
+        order[i] = i;
+        rate[i] = 1.0 / tpl[i].tstar_ms;
+        over[i] = tpl[i].t1_ms + tpl[i].t3_ms - (double)(tpl[i].num_stages - tpl[i].kstar + 1) * tpl[i].tstar_ms;
+    }
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return over[a] < over[b]; });
+    const double NEG = -std::numeric_limits<double>::infinity();
+    std::vector<double> dp;
+    std::vector<int32_t> from;
+    std::vector<std::vector<int32_t>> out;
+    // knapsack over the allowed templates with C count buckets (saturating or exact)
+    auto run = [&](const std::vector<char> &allowed, int C, bool saturate) {
+        dp.assign((size_t)(N + 1) * C, NEG);
+        from.assign((size_t)(N + 1) * C, 0);
+        dp[0] = 0.0;
+        for (int t = 1; t <= N; ++t)
+            for (int i = 0; i < p; ++i) {
+                if (!allowed[i]) continue;
+                const int n = n_lo + i;
+                if (n > t) break;
+                for (int c = 0; c < C; ++c) {
+                    const double v = dp[(size_t)(t - n) * C + c];
+                    if (v == NEG) continue;
+                    const int c2 = saturate ? std::min(c + 1, C - 1) : c + 1;
+                    if (c2 >= C) continue;
+                    const double w = v + rate[i];
+                    double &d = dp[(size_t)t * C + c2];
+                    if (w > d) { d = w; from[(size_t)t * C + c2] = i | (c << 16); }
+                }
+            }
+    };
+    auto add = [&](int C, int c) {
+        if (dp[(size_t)N * C + c] == NEG) return;
+        std::vector<int32_t> x(p, 0);
+        int t = N;
+        while (t > 0) {
+            const int32_t fr = from[(size_t)t * C + c];
+            const int i = fr & 0xFFFF;
+            x[i]++;
+            t -= n_lo + i;
+            c = fr >> 16;
+        }
+        if (std::find(out.begin(), out.end(), x) == out.end()) out.push_back(x);
+    };
+    std::vector<char> allowed(p, 0);
+    for (int th = 0; th < p; ++th) {                       // (1)
+        allowed[order[th]] = 1;
+        if (th + 1 < p && over[order[th + 1]] == over[order[th]]) continue;
+        run(allowed, f + 2, true);
+        add(f + 2, f + 1);
+    }
+    // (3) (near-)homogeneous sets: q or q-1, q-2 pipelines of one template plus at most one
+    // pipeline of the size that uses the remaining nodes (equal pipelines balance exactly)
+    for (int i = 0; i < p; ++i) {
+        const int n = n_lo + i, q = N / n;
+        for (int k = 0; k <= 2 && q - k >= 1; ++k) {
+            const int R = N - (q - k) * n;
+            if (R != 0 && (R < n_lo || R >= n_lo + p)) continue;
+            if ((q - k) + (R ? 1 : 0) < f + 1) continue;
+            std::vector<int32_t> x(p, 0);
+            x[i] += q - k;
+            if (R) x[R - n_lo] += 1;
+            if (std::find(out.begin(), out.end(), x) == out.end()) out.push_back(x);
+        }
+    }
+    // (2) with the KB best rates per (nodes, count) state, so near-optimal sets whose
+    // integer batch split is better also get scored
+    const int64_t cmax = std::min<int64_t>(K, N / n_lo);
+    if (cmax >= f + 1) {
+        constexpr int KB = 4;
+        const int C = (int)cmax + 1;
+        struct E { double v; int32_t i, c, r; };      // value, template, previous count, previous rank
+        std::vector<E> kb((size_t)(N + 1) * C * KB, E{NEG, -1, 0, 0});
+        auto at = [&](int t, int c, int r) -> E & { return kb[((size_t)t * C + c) * KB + r]; };
+        at(0, 0, 0).v = 0.0;
+        for (int t = 1; t <= N; ++t)
+            for (int c = 1; c < C; ++c) {
+                E best[KB];
+                for (int r = 0; r < KB; ++r) best[r] = E{NEG, -1, 0, 0};
+                for (int i = 0; i < p; ++i) {
+                    const int n = n_lo + i;
+                    if (n > t) break;
+                    for (int r = 0; r < KB; ++r) {
+                        const E &prev = at(t - n, c - 1, r);
+                        if (prev.v == NEG) break;
+                        const E cand{prev.v + rate[i], i, c - 1, r};
+                        if (cand.v <= best[KB - 1].v) continue;
+                        bool dup = false;                // the same multiset reached in another order
+                        for (int k = 0; k < KB; ++k) dup = dup || best[k].v == cand.v;
+                        if (dup) continue;
+                        int k = KB - 1;
+                        while (k > 0 && best[k - 1].v < cand.v) { best[k] = best[k - 1]; --k; }
+                        best[k] = cand;
+                    }
+                }
+                for (int r = 0; r < KB; ++r) at(t, c, r) = best[r];
+            }
+        for (int c = f + 1; c < C; ++c)
+            for (int r0 = 0; r0 < KB; ++r0) {
+                if (at(N, c, r0).v == NEG) break;
+                std::vector<int32_t> x(p, 0);
+                int t = N, cc = c, r = r0;
+                while (t > 0) {
+                    const E &e = at(t, cc, r);
+                    x[e.i]++;
+                    t -= n_lo + e.i;
+                    cc = e.c;
+                    r = e.r;
+                }
+                if (std::find(out.begin(), out.end(), x) == out.end()) out.push_back(x);
+            }
+    }
+    return out;
+}
+
 }  // namespace
 
 extern "C" oob_status oob_count_sets(int32_t n_lo, int32_t n_hi, int32_t N, int32_t f, int64_t *out) {
@@ -252,7 +382,15 @@ extern "C" oob_status oob_instantiate(const oob_template_set *set, int32_t profi
     const int64_t total = count_sets(set->n_lo, set->n_hi, N, f);
     if (num_feasible_out) *num_feasible_out = total;
     if (total == 0) return fail(OOB_E_INFEASIBLE, "no feasible pipeline set for this node count");
-    dfs(c, p - 1, N);
+    if (total <= c.max_enum) {
+        dfs(c, p - 1, N);                  // exact: every feasible X (Eq.5)
+    } else {
+        c.capped = true;                   // too many: knapsack candidates, scored exactly
+        for (const auto &x : knapsack_candidates(c.tpl, p, c.n_lo, N, f, B / b)) {
+            c.x = x;
+            evaluate(c);
+        }
+    }
     if (c.best_thr < 0) {
         if (rec_out) *rec_out = oob_recommend_batch(c.min_pipes_fail == INT32_MAX ? f + 1 : c.min_pipes_fail, b, B);
         return fail(OOB_E_BATCH, "no feasible set can distribute the global batch");
@@ -264,6 +402,6 @@ extern "C" oob_status oob_instantiate(const oob_template_set *set, int32_t profi
     if (thr_out) *thr_out = c.best_thr;
     if (iter_out) *iter_out = c.best_iter;
     if (rec_out) *rec_out = B;
-    if (c.capped) return fail(OOB_E_TOO_MANY, "more than max_enumerated feasible sets; plan is the best of the first max_enumerated");
+    if (c.capped) return fail(OOB_E_TOO_MANY, "more than max_enumerated feasible sets; plan is the best knapsack candidate");
     return OOB_OK;
 }

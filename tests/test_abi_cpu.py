@@ -153,6 +153,52 @@ def test_instantiate_vs_brute(planner):
     assert checked > 20
 
 
+def _set_handle(pl, tpls, L, M, sizes):
+    packed, info = pack_templates([tpls], L, M, sizes[0], sizes[-1])
+    dinfo = pl.OobDpInfo(**info, wavefronts=0, cells_per_profile=0, splits_per_profile=0,
+                         kernel_launches=0, workspace_bytes=0)
+    h = ctypes.c_void_p()
+    pl.check(pl.lib.oob_template_set_from_packed(packed.ctypes.data, ctypes.byref(dinfo), ctypes.byref(h)))
+    return pl.TemplateSet(h)
+
+
+def test_instantiate_capped_candidates(planner):
+    """Above max_enumerated (cfg4: 2.2e19 sets) oob_instantiate scores knapsack candidates
+    (reading R20): on enumerable random cases the plan is valid, never better than the
+    exhaustive optimum, within 10% of it, and equal to it in >= 90% of the cases."""
+    from oracle import coracle
+    from paper_2309_08125_b200 import planner as pl
+    rng = random.Random(123)
+    cases = exact = 0
+    for it in range(120):
+        L, M = rng.randint(6, 24), rng.choice([1, 2, 4, 8])
+        N, f, n0 = rng.randint(8, 40), rng.randint(0, 3), rng.randint(1, 2)
+        if N < (f + 1) * n0 or n0 > L:
+            continue
+        sizes = oracle_node_sizes(N, f, n0, L)
+        prof = random_profile(100 + it, L, M, rng.choice(["uniform", "lognormal", "spiky", "integer"]))
+        tpls = coracle.template_set(prof.fwd_ms, prof.bwd_ms, M, sizes[0], sizes[-1])[0]
+        ts = _set_handle(pl, tpls, L, M, sizes)
+        b = rng.choice([1, 2, 4])
+        B = b * rng.randint(max(1, N // 4), 3 * N)
+        Np = rng.randint((f + 1) * n0, N)
+        try:
+            ex = planner.instantiate(ts, 0, Np, f, B, b, max_enumerated=10 ** 8)
+        except pl.OobError:
+            continue
+        if not 1 < ex["num_feasible"] <= 3e5:
+            continue
+        ca = planner.instantiate(ts, 0, Np, f, B, b, max_enumerated=1)
+        assert ca["capped"] and not ex["capped"]
+        assert sum(c * (sizes[0] + i) for i, c in enumerate(ca["counts"])) == Np
+        assert sum(ca["counts"]) >= f + 1 and sum(ca["nb"]) * b == B
+        assert ca["throughput"] <= ex["throughput"] * (1 + 1e-12)
+        assert ca["throughput"] >= 0.9 * ex["throughput"], (it, ca, ex)
+        cases += 1
+        exact += ca["throughput"] >= ex["throughput"] * (1 - 1e-12)
+    assert cases >= 60 and exact >= 0.9 * cases, (cases, exact)
+
+
 def test_load_profile_json(planner, tmp_path):
     from paper_2309_08125_b200._lib import OOB_E_INVALID, OOB_E_PARSE, OobError
     prof = random_profile(5, 6, 2, "lognormal")
