@@ -50,7 +50,7 @@ __global__ void k_base(DevGeom g, const double *__restrict__ fwd, const double *
     double s = 0.0;
     for (int k = u; k < u + l; ++k) s = __dadd_rn(s, __dadd_rn(F[k * g.M + d - 1], B[k * g.M + d - 1]));
     const int64_t c = (int64_t)p * g.C + d_cell(g, 1, u, l, a);
-    d_store(g.CELL + c, s, s, s, 2.0);    // T1 = T3 = t* = t; C1 = 3*1 - 1 + k*(=0)
+    d_store(g, c, s, s, s, 2.0);    // T1 = T3 = t* = t; C1 = 3*1 - 1 + k*(=0)
     g.ARG[c] = 0xFFFFFFFFu;
 }
 
@@ -238,7 +238,7 @@ struct oob_dp_plan {
     std::vector<unsigned char> geom_blob;   // host image of the geometry region
     size_t off_cells = 0, off_base = 0, off_off = 0, off_tiles = 0, off_tile_off = 0, off_tile_cnt = 0,
            off_items = 0;
-    size_t off_CELL = 0, off_ARG = 0, off_STK = 0, off_GACC = 0, off_CTR = 0;
+    size_t off_CELL = 0, off_SH = 0, off_ARG = 0, off_STK = 0, off_GACC = 0, off_GFILT = 0, off_CTR = 0;
     int64_t gacc_n = 0;
     void *comm = nullptr;                // ncclComm_t (single-profile sharding), world > 1
     int rank = 0, world = 1;
@@ -348,7 +348,7 @@ static void build_wave(oob_dp_plan *pl, int l, int ci, int slots, WaveHost &wh, 
     const size_t nent = (size_t)(wh.nout + g.L + 2 * TE + 2);
     const size_t before_ring = nent * 16 + (nent + 3) / 4 * 16 + (size_t)wh.nents * 16 + (size_t)(g.L + 2) * 8 +
                                (size_t)(g.L + 1) * 4 + (size_t)(g.L + 2) * 4 + (size_t)(g.L + 4) * 4;
-    wh.smem = before_ring + 32 + (size_t)(NTW / 32) * XR_BYTES;   // + per-warp streamed-side rings
+    wh.smem = before_ring + 32 + (size_t)(NTW / 32) * (XR_BYTES + XQ_BYTES);   // + per-warp rings and queues
     wh.cost = total * ranges;
 }
 
@@ -472,10 +472,12 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     pl->geom_bytes = o;
     const size_t n = (size_t)g.total_cells * num_profiles;
     pl->off_CELL = o; o = align_up(o + 32 * (n + 16 + XR_CELLS), 256);   // + padding: row streams read ahead
+    pl->off_SH = o; o = align_up(o + 16 * (n + 16 + XR_CELLS), 256);     // shadow lower bounds (+ padding)
     pl->off_ARG = o; o = align_up(o + 4 * n, 256);
     pl->off_STK = o; o = align_up(o + 8 * (size_t)num_profiles * (n_hi - n_lo + 1) * (L + 1), 256);
     pl->gacc_n = (int64_t)gacc_max;
     pl->off_GACC = o; o = align_up(o + 2 * 16 * gacc_max, 256);   // two parity buffers
+    pl->off_GFILT = o; o = align_up(o + 2 * 4 * gacc_max, 256);   // their filters
     pl->off_CTR = o; o = align_up(o + 4 * pl->ctr_n + 4, 256);
     pl->ws_bytes_base = o;
     pl->ws_bytes = o;
@@ -597,6 +599,10 @@ extern "C" oob_status oob_dp_kernel_time(oob_dp_plan *pl, double *ms_out, int64_
 static ulonglong2 *gacc_of(const oob_dp_plan *pl, ulonglong2 *gacc, int l) {
     return gacc + (size_t)(l & 1) * (size_t)pl->gacc_n;
 }
+// global filter of wave l's accumulator (same parity and index)
+static unsigned *gfilt_of(const oob_dp_plan *pl, ulonglong2 *gacc, int l) {
+    return (unsigned *)((unsigned char *)gacc - pl->off_GACC + pl->off_GFILT) + (size_t)(l & 1) * (size_t)pl->gacc_n;
+}
 
 // Finalize arguments for wave lw (0: none) and in-node cells + seeds of wave ls (0: none);
 // *nbsmall receives the blocks of the small-cell part.
@@ -610,6 +616,7 @@ static FinArgs make_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglong2 *ga
     const int64_t nw = (int64_t)pl->P * f.nranges_w * f.nout_w;
     f.nbw = (int)((nw + 255) / 256);
     f.GACC = gacc_of(pl, gacc, lw);
+    f.GFW = gfilt_of(pl, gacc, lw);
     f.world = sharded ? pl->world : 1;
     f.part_stride = (int64_t)pl->P * f.nranges_w * f.nout_w;   // all-gather: rank r at r x (wave partial)
     f.GPART = (const ulonglong2 *)((const unsigned char *)dg.CELL - pl->off_CELL + pl->off_GPART);
@@ -619,6 +626,7 @@ static FinArgs make_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglong2 *ga
     const int64_t nsd = f.lseed ? (int64_t)pl->P * (G.L - ls + 1) * f.nout_s : 0;
     f.nbseed = (int)((nsd + 255) / 256);
     f.GSEED = gacc_of(pl, gacc, ls);
+    f.GFS = gfilt_of(pl, gacc, ls);
     f.ls = ls;
     f.nsmall = ls ? small_cells(G, ls) : 0;
     f.tpc = ls ? small_tpc(G, ls, pl->small_pairs) : 32;
@@ -671,6 +679,7 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
     dg.base = (const int64_t *)(ws + pl->off_base);
     dg.off = (const int32_t *)(ws + pl->off_off);
     dg.CELL = (Cell4 *)(ws + pl->off_CELL);
+    dg.SH = (float4 *)(ws + pl->off_SH);
     dg.ARG = (uint32_t *)(ws + pl->off_ARG);
     dg.STK = (uint64_t *)(ws + pl->off_STK);
 
@@ -693,7 +702,8 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
     ulonglong2 *gacc = (ulonglong2 *)(ws + pl->off_GACC);
     if (pl->kernel == 2) {
         if (pl->gacc_ready != d_ws && pl->gacc_n > 0) {   // finalize resets what it reads
-            k_gacc_init<<<(unsigned)((2 * pl->gacc_n + 255) / 256), 256, 0, stream>>>(gacc, 2 * pl->gacc_n);
+            k_gacc_init<<<(unsigned)((2 * pl->gacc_n + 255) / 256), 256, 0, stream>>>(gacc, gfilt_of(pl, gacc, 0),
+                                                                                     2 * pl->gacc_n);
             e = cudaGetLastError();
             if (e != cudaSuccess) return cuda_fail(e, "k_gacc_init launch");
             pl->gacc_ready = d_ws;
@@ -726,6 +736,7 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
         w.ctr = (int *)(ws + pl->off_CTR) + wh.ctr_off;
         w.nout = wh.nout;
         w.GACC = gacc_of(pl, gacc, l);
+        w.GFILT = gfilt_of(pl, gacc, l);
         w.tile_off = (const int32_t *)(ws + pl->off_tile_off) + (size_t)(G.L + 1) * te_index(WCFGS[wh.cfg].te);
         w.tile_cnt = (const int32_t *)(ws + pl->off_tile_cnt) + (size_t)(G.L + 1) * te_index(WCFGS[wh.cfg].te);
         w.tiles = (const int32_t *)(ws + pl->off_tiles);
@@ -803,3 +814,25 @@ extern "C" int oob_dbg_flush_stats(int enable, unsigned long long *out4) {
     if (cudaMemcpyToSymbol(oob::g_flush_stats, z, sizeof(z)) != cudaSuccess) return 1;
     return cudaMemcpyToSymbol(oob::g_flush_stats_on, &enable, sizeof(int)) == cudaSuccess ? 0 : 1;
 }
+
+// Diagnostic (not part of the C ABI header): byte offsets of the cell, shadow and argmin
+// tables inside a plan's workspace (scripts/dbg_table.py).
+extern "C" int oob_dbg_offsets(const oob_dp_plan *pl, unsigned long long *out5) {   // [7]
+    if (!pl || !out5) return 1;
+    out5[0] = pl->off_CELL;
+    out5[1] = pl->off_SH;
+    out5[2] = pl->off_ARG;
+    out5[3] = pl->off_base;
+    out5[4] = pl->off_cells;
+    out5[5] = pl->off_off;
+    out5[6] = (unsigned long long)pl->g.A;
+    return 0;
+}
+
+#ifdef OOB_DBG_FILTER
+extern "C" int oob_dbg_filter(unsigned long long *out64) {
+    if (cudaMemcpyFromSymbol(out64, oob::g_dbg, sizeof(unsigned long long) * 256) != cudaSuccess) return 1;
+    unsigned long long z[256] = {0};
+    return cudaMemcpyToSymbol(oob::g_dbg, z, sizeof(z)) == cudaSuccess ? 0 : 1;
+}
+#endif

@@ -6,6 +6,10 @@
 //        P:405) — an exact small integer in binary64, so T2 = C1 * t* and
 //        k* = C1 - (3S'-1) exactly;
 //   ARG: argmin split packed (l1-1) | m << 10 | s << 20 (0xFFFFFFFF for S' = 1).
+// Shadow table SH (per cell, float4, written with every cell): binary32 LOWER BOUNDS of
+//   {A = T1 + T3 + C1 t*, T1, t*, 2 T1} (fp64 ops rounded down, then rounded down to fp32),
+//   used only by k_wave_w's filter (a split whose lower bound cannot reach the output's
+//   current minimum is skipped; every candidate is re-evaluated exactly in binary64).
 // Cell index: base[l] + u*cells[l] + off[l*A + a] + (S' - lo(a)).
 #pragma once
 
@@ -24,6 +28,7 @@ struct DevGeom {
     const int64_t *base;      // [L+2]
     const int32_t *off;       // [(L+1)*A]
     Cell4 *CELL;              // [P*C]
+    float4 *SH;               // [P*C] shadow lower bounds (filter only)
     uint32_t *ARG;            // [P*C]
     uint64_t *STK;            // [P*p*(L+1)] backtrack stacks
 };
@@ -65,9 +70,25 @@ __device__ __forceinline__ Cell4 d_load(const Cell4 *p) {
     c.T1 = a.x; c.T3 = a.y; c.TS = b.x; c.C1 = b.y;
     return c;
 }
-__device__ __forceinline__ void d_store(Cell4 *p, double T1, double T3, double TS, double C1) {
-    reinterpret_cast<double2 *>(p)[0] = make_double2(T1, T3);
-    reinterpret_cast<double2 *>(p)[1] = make_double2(TS, C1);
+// Shadow of a cell: every component rounds toward -inf, so each is <= the real value of
+// the expression on the stored binary64 values (all positive).
+__device__ __forceinline__ float4 d_shadow(double T1, double T3, double TS, double C1) {
+    const double A = __dadd_rd(__dadd_rd(T1, T3), __dmul_rd(C1, TS));
+    const float t1 = __double2float_rd(T1);
+    return make_float4(__double2float_rd(A), t1, __double2float_rd(TS), __fmul_rd(2.0f, t1));
+}
+// Store cell c (table index incl. the profile offset) and its shadow.
+__device__ __forceinline__ void d_store(const DevGeom &g, int64_t c, double T1, double T3, double TS, double C1) {
+    reinterpret_cast<double2 *>(g.CELL + c)[0] = make_double2(T1, T3);
+    reinterpret_cast<double2 *>(g.CELL + c)[1] = make_double2(TS, C1);
+    g.SH[c] = d_shadow(T1, T3, TS, C1);
+}
+// Poison cell c (no valid split found / corrupt key): NaN value, never passes the filter.
+__device__ __forceinline__ void d_poison(const DevGeom &g, int64_t c, uint32_t code) {
+    g.CELL[c].T1 = __longlong_as_double(0x7ff8000000000000LL);
+    g.SH[c] = make_float4(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000),
+                          __int_as_float(0x7fc00000));
+    g.ARG[c] = code;
 }
 
 // Recompute the value of the cell (Sp, u, u+l, a) for its winning split (l1, j, s) from its
@@ -83,7 +104,7 @@ __device__ __forceinline__ void d_write_winner(const DevGeom &g, int64_t pc, int
     const bool left = Lc.TS >= Rc.TS;
     const double kd = left ? d_kd(Lc.C1, s) : __dadd_rn((double)s, d_kd(Rc.C1, Sp - s));
     const int64_t c = pc + d_cell(g, Sp, u, l, a);
-    d_store(g.CELL + c, __dadd_rn(Lc.T1, Rc.T1), left ? __dadd_rn(Lc.T3, Rc.T1) : Rc.T3,
+    d_store(g, c, __dadd_rn(Lc.T1, Rc.T1), left ? __dadd_rn(Lc.T3, Rc.T1) : Rc.T3,
             left ? Lc.TS : Rc.TS, d_c1(kd, Sp));
     g.ARG[c] = (uint32_t)(l1 - 1) | ((uint32_t)j << 10) | ((uint32_t)s << 20);
 }

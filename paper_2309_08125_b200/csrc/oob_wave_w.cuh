@@ -51,6 +51,7 @@ struct FinArgs {
     int world;
     int lseed, nout_s, nbseed;     // seeds of wave lseed (0: none): W outputs per range, blocks
     ulonglong2 *GSEED;             // accumulator of wave lseed (the other parity buffer)
+    unsigned *GFW, *GFS;           // global filters (binary32 bits of F(min)) of waves lw / lseed
     int ls, nsmall;                // small cells of wave ls (ls = 0: none); cells per range
     int tpc;                       // threads per small cell
 };
@@ -71,6 +72,7 @@ struct WaveW {
     int rank, world;       // single-profile sharding: this rank takes units rank, rank+world, ...
     int nout;              // W-part cells of a slab of length l (W(1)..W(Q_l))
     ulonglong2 *GACC;      // global accumulator [P][nranges][nout]: {total bits, key}
+    unsigned *GFILT;       // global filter [P][nranges][nout]: F(min) over every CTA's improvements
     const int32_t *tile_off;   // [L+1] offset of the flat tile list of a big side of length lb
     const int32_t *tile_cnt;   // [L+1] number of tiles
     const int32_t *tiles;      // packed (row << 16 | e0)
@@ -169,87 +171,67 @@ __device__ __forceinline__ int c_ipart(int M, int l) {
     return l >= M - 1 ? (M - 1) * M / 2 : l * (l + 1) / 2 + (M - 1 - l) * l;
 }
 
-// Flush one completed ring slot (exact minimum `b` of its TE contributions, split key
-// `key`) into accumulator entry `idx`.  Fast path: compare the high word of `b` with the
-// entry's filter word (u32, at most the high word of the entry's total; TE odd makes the
-// lanes' filter words — TE entries apart — hit distinct banks).  Only if it can win or tie
-// does the lane read the 16-byte entry and run the lexicographic CAS loop (entries only
-// decrease, so a stale read is an upper bound and the loop stays exact), then lower the
-// filter.  Dummy entries have filter 0 (nothing passes); +inf / NaN never pass ACC_EMPTY.
-// diagnostic counters (flush tests passed, CAS successes): compiled in with -DOOB_FLUSH_STATS
-// (scripts/flush_stats.py), enabled by oob_dbg_flush_stats
+// diagnostic counters (outputs whose bound passed the filter, CAS successes): compiled in
+// with -DOOB_FLUSH_STATS (scripts/flush_stats.py), enabled by oob_dbg_flush_stats
 __device__ unsigned long long g_flush_stats[4];
 __device__ int g_flush_stats_on;
 
-__device__ __forceinline__ void acc_flush(unsigned acc_s, unsigned filt_s, int idx, double b, uint32_t key) {
-    const unsigned bh = (unsigned)__double2hiint(b);
-    unsigned fh;
-    asm("ld.shared.u32 %0, [%1];" : "=r"(fh) : "r"(filt_s + 4u * (unsigned)idx));
-    if (bh <= fh) {
-#ifdef OOB_FLUSH_STATS
-        if (g_flush_stats_on) {
-            atomicAdd(&g_flush_stats[0], 1ull);
-            if (bh < fh) atomicAdd(&g_flush_stats[2], 1ull);
-        }
-#endif
-        const unsigned addr = acc_s + 16u * (unsigned)idx;
-        const unsigned long long bb = (unsigned long long)__double_as_longlong(b);
-        unsigned long long cx, cy;
-        asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(cx), "=l"(cy) : "r"(addr) : "memory");
-        while (lex_less(bb, key, cx, (uint32_t)cy)) {
-            unsigned long long ox, oy;
-            cas128_shared(addr, ox, oy, cx, cy, bb, (unsigned long long)key);
-            if (ox == cx && oy == cy) {
-#ifdef OOB_FLUSH_STATS
-                if (g_flush_stats_on) atomicAdd(&g_flush_stats[1], 1ull);
-#endif
-                asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(filt_s + 4u * (unsigned)idx), "r"(bh) : "memory");
-                break;
-            }
-            cx = ox;
-            cy = oy;
-        }
-    }
+// ---------------------------------------------------------------- exact filter (fast path)
+// A split's binary64 total is bounded from below by a binary32 expression of the children's
+// shadows (oob_dp_common.cuh d_shadow; every operation rounds toward -inf):
+//   left child X, right child Y, s = stages of X, S_Y = stages of Y,
+//   totL = A_X + 3 S_Y X.t* + 2 Y.T1   (= the total when X holds the slowest stage)
+//   totR = A_Y + 4 s Y.t* + X.T1       (= the total when Y holds it)
+//   lb   = (X.t*_f >= Y.t*_f) ? totL : totR
+// (expand Eqs.1-3 with C1 = 3S'-1+k*: T1 + (C1_X + 3 S_Y) X.t* + X.T3 + Y.T1, resp.
+// T1 + (C1_Y + 4 s) Y.t* + Y.T3).  Rounding t* down is monotone, so the binary32 compare
+// can only misjudge an exact tie of the rounded t*'s, where X.t* < Y.t* and lb takes totL:
+// then totL <= totR + 2^-44 totR, because X.T3 sums s - k*_X stages <= X.t* and
+// Y.T1 - Y.T3 sums k*_Y stages <= Y.t* (up to the binary64 rounding of those sums, <= 192 ulp).
+// The binary64 total is >= (1 - 3u) times the real expression, so a split can reach a
+// current minimum m (its total <= m) only if lb <= m (1 + 2^-43).  The filter therefore
+// compares lb with F(m) = float_ru(m (1 + 2^-40)) and never drops a winner or a tie.
+constexpr unsigned FILT_EMPTY = 0x7F7FFFFFu;   // FLT_MAX: nothing known yet
+__device__ __forceinline__ float filt_of(unsigned long long bits) {
+    if (bits >= 0x7FEFFFFFFFFFFFFFull) return 3.402823466e38f;   // empty entry: FLT_MAX
+    return __double2float_ru(__dmul_ru(__longlong_as_double((long long)bits), 1.0 + 0x1p-40));
 }
 
-// Streamed side staging: a per-warp ring of XR_CELLS cells in shared memory, filled with
-// cp.async in batches of XR_BATCH cells (512 B: one 16-byte copy per lane) issued
-// XR_AHEAD batches ahead of the step loop, so the steps read the streamed cell from shared
-// memory (broadcast LDS) instead of waiting on L1/L2.  The first XR_MIRROR cells of the
-// ring are mirrored after its end, so the TE+1 cells a block of steps reads are contiguous
-// (one base address per block, immediate offsets).  Copies are unguarded: a chunk's last
-// batches may read past the slab (the CELL allocation is padded by XR_CELLS cells).
-constexpr int XR_CELLS = 64;
-constexpr int XR_BATCH = 16;
+// Streamed side staging: a per-warp ring of XR_CELLS shadow cells (float4) in shared memory,
+// filled with cp.async in batches of XR_BATCH cells (512 B: one 16-byte copy per lane)
+// issued XR_AHEAD batches ahead of the step loop, so the steps read the streamed shadow
+// from shared memory (broadcast LDS.128).  The first XR_MIRROR cells of the ring are
+// mirrored after its end, so the TE cells a block of steps reads are contiguous (one base
+// address per block, immediate offsets).  Copies are unguarded: a chunk's last batches may
+// read past the slab (the SH allocation is padded by XR_CELLS cells).
+constexpr int XR_CELLS = 128;
+constexpr int XR_BATCH = 32;
 constexpr int XR_AHEAD = 2;
 constexpr int XR_MIRROR = 8;
-constexpr int XR_BYTES = (XR_CELLS + XR_MIRROR) * 32;   // per warp
+constexpr int XR_BYTES = (XR_CELLS + XR_MIRROR) * 16;   // per warp
 
 struct XRing {
-    const double2 *ring;                  // this warp's ring (shared memory, 2 x double2 per cell)
+    const float4 *ring;                   // this warp's ring (shared memory)
     unsigned ring_s;                      // its shared-space address + lane * 16
-    const char *src;                      // chunk start (global) + lane * 16
+    const char *src;                      // chunk start (global shadow) + lane * 16
     int nb_iss, nb_ok;                    // batches issued / complete
-    bool mirror;                          // this lane also writes the mirror cells
+    bool mirror;                          // this lane also writes a mirror cell
 };
 
 __device__ __forceinline__ void xr_issue(XRing &r) {
-#ifdef OOB_XR_SYNC
-    __syncwarp();
-#endif
     const int b = r.nb_iss++;
-    const unsigned pos = (unsigned)((b * XR_BATCH) & (XR_CELLS - 1)) * 32u;
-    const char *g = r.src + (size_t)b * (XR_BATCH * 32);
+    const unsigned pos = (unsigned)((b * XR_BATCH) & (XR_CELLS - 1)) * 16u;
+    const char *g = r.src + (size_t)b * (XR_BATCH * 16);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(r.ring_s + pos), "l"(g) : "memory");
     if (pos == 0 && r.mirror)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(r.ring_s + XR_CELLS * 32u), "l"(g) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(r.ring_s + XR_CELLS * 16u), "l"(g) : "memory");
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
-__device__ __forceinline__ void xr_start(XRing &r, const double2 *ring, const Cell4 *src, int lane) {
+__device__ __forceinline__ void xr_start(XRing &r, const float4 *ring, const float4 *src, int lane) {
     r.ring = ring;
     r.ring_s = (unsigned)__cvta_generic_to_shared(ring) + lane * 16;
     r.src = reinterpret_cast<const char *>(src) + lane * 16;
-    r.mirror = lane < 2 * XR_MIRROR;
+    r.mirror = lane < XR_MIRROR;
     r.nb_iss = 0;
     r.nb_ok = 0;
 #pragma unroll
@@ -258,105 +240,299 @@ __device__ __forceinline__ void xr_start(XRing &r, const double2 *ring, const Ce
 // make cells <= j available (warp-uniform; j grows by <= XR_BATCH between calls)
 __device__ __forceinline__ void xr_ensure(XRing &r, int j) {
     if (j / XR_BATCH >= r.nb_ok) {
+        // lanes diverge on the exact path: none may still read the region this copy
+        // overwrites (write-after-read across lanes)
+        __syncwarp();
         xr_issue(r);
-#ifdef OOB_XR_WAIT0
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-#else
         asm volatile("cp.async.wait_group %0;" ::"n"(XR_AHEAD) : "memory");
-#endif
         __syncwarp();                     // the other lanes' copies are visible
         r.nb_ok = r.nb_iss - XR_AHEAD;
     }
 }
 // cells c .. c + XR_MIRROR of the ring as one contiguous run
-__device__ __forceinline__ const double2 *xr_at(const XRing &r, int c) { return r.ring + 2 * (c & (XR_CELLS - 1)); }
-__device__ __forceinline__ Cell4 xr_cell(const double2 *q, int i) {
-    const double2 a = q[2 * i], b = q[2 * i + 1];
-    Cell4 x;
-    x.T1 = a.x; x.T3 = a.y; x.TS = b.x; x.C1 = b.y;
-    return x;
+__device__ __forceinline__ const float4 *xr_at(const XRing &r, int c) { return r.ring + (c & (XR_CELLS - 1)); }
+
+// Lower bound of one split from the tile shadow (TA/TB/TS/TC, lane constants) and the
+// streamed shadow x (see the filter derivation above); fst = LT ? 3 S_R : 4 s.
+template <bool LT>
+__device__ __forceinline__ float split_lb(float TA, float TB, float TS, float TC, const float4 x, float fst) {
+    if (LT) {   // tile X: TA = A_X, TB = X.T1, TS = X.t*, TC = 4 s; x = Y
+        const float tl = __fadd_rd(__fmaf_rd(fst, TS, TA), x.w);
+        const float tr = __fmaf_rd(TC, x.z, __fadd_rd(x.x, TB));
+        return TS >= x.z ? tl : tr;
+    } else {    // tile Y: TA = A_Y, TB = 2 Y.T1, TS = Y.t*, TC = 3 S_Y; x = X
+        const float tl = __fadd_rd(__fmaf_rd(TC, x.z, x.x), TB);
+        const float tr = __fmaf_rd(fst, TS, __fadd_rd(TA, x.y));
+        return x.z >= TS ? tl : tr;
+    }
 }
 
-// The small-side rows r_lo..r_hi-1 of one unit against this lane's register tile.
-//  LT = true : tile = LEFT child (row rowB = j, s_t = S0 + t), stream = RIGHT child (row
-//              rs = j', S_R = rs + e).  cL = C1_L[t] + 3 S_R, cR = C1_R(e) + 4 s_t.
-//              Ties: contributions to one output arrive with decreasing s -> "<=".
-//              key = l1<<20 | rowB<<10 | (S0 + t).
-//  LT = false: tile = RIGHT child (row rowB = j', S_R,t = S0 + t), stream = LEFT child (row
-//              rs = j, s = rs + e).  cL = C1_L(e) + 3 S_R,t, cR = C1_R[t] + 4 s.
-//              Ties: arrivals with increasing s -> "<".  key = l1<<20 | rs<<10 | (rs + e).
-// Output E' = e + t (index relative to the tile's first output) lives in ring slot
-// E' mod TE; its first contribution (t = TE-1) assigns the slot, t = 0 completes it (flush).
-// Each row runs in blocks of TE steps (static slots) plus a guarded tail.  The streamed
-// cells (rows r_lo..r_hi-1 are contiguous in the slab) come through the warp's XRing.
+// Candidate queue: the splits whose lower bound passes the filter are not evaluated in place
+// (divergent, global-latency bound) but appended to a per-warp queue in shared memory and
+// evaluated by the whole warp, one split per lane, when the queue is full and at the end of
+// each unit.  An entry (16 B): the two children's table indices, the split key, and
+// idx | addL << 13 | addR << 22 | LT << 31 (accumulator entry, the exact integers added to
+// the left / right child's C1 for the parent's coefficient, tile = left child).
+constexpr int XQ_CAP = 32;
+constexpr int XQ_BYTES = XQ_CAP * 16;     // per warp
+
+// Exact evaluation of the queued splits (warp-collective; lane i takes entry i) in binary64
+// in the oracle's operation order; each result is merged as the lexicographic minimum of
+// (total, key) with the 128-bit CAS into the CTA's accumulator entry (entries only
+// decrease: a stale read is an upper bound, the loop stays exact), then the CTA's and the
+// range's global filters are lowered.
+__device__ __forceinline__ void xq_flush(const uint4 *q, int &count, const Cell4 *CELL, unsigned acc_s,
+                                         unsigned filt_s, unsigned *gfr) {
+    __syncwarp();
+    const int lane = threadIdx.x & 31;
+    if (lane < count) {
+        const uint4 en = q[lane];
+        const bool lt = en.w >> 31;
+        const int idx = (int)(en.w & 8191u);
+        const Cell4 tc = d_load(CELL + en.x), sc = d_load(CELL + en.y);
+        const Cell4 &Lc = lt ? tc : sc, &Rc = lt ? sc : tc;
+        const double cL = __dadd_rn(Lc.C1, (double)((en.w >> 13) & 511u));
+        const double cR = __dadd_rn(Rc.C1, (double)((en.w >> 22) & 511u));
+        const double tot = split_total(Lc.T1, Lc.T3, Lc.TS, cL, Rc.T1, Rc.T3, Rc.TS, cR);
+        const unsigned long long bb = (unsigned long long)__double_as_longlong(tot);
+        const uint32_t bk = en.z;
+        const unsigned addr = acc_s + 16u * (unsigned)idx;
+        unsigned long long cx, cy;
+        asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(cx), "=l"(cy) : "r"(addr) : "memory");
+#ifdef OOB_FLUSH_STATS
+        if (g_flush_stats_on) {
+            atomicAdd(&g_flush_stats[0], 1ull);
+            if (bb == cx) atomicAdd(&g_flush_stats[2], 1ull);
+            else if (bb > cx) atomicAdd(&g_flush_stats[3], 1ull);
+        }
+#endif
+        while (lex_less(bb, bk, cx, (uint32_t)cy)) {
+            unsigned long long ox, oy;
+            cas128_shared(addr, ox, oy, cx, cy, bb, (unsigned long long)bk);
+            if (ox == cx && oy == cy) {
+#ifdef OOB_FLUSH_STATS
+                if (g_flush_stats_on) atomicAdd(&g_flush_stats[1], 1ull);
+#endif
+                const unsigned fb = __float_as_uint(filt_of(bb));
+                asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(filt_s + 4u * (unsigned)idx), "r"(fb) : "memory");
+                atomicMin(gfr + idx, fb);     // share with the range's other CTAs (refreshed per unit)
+                break;
+            }
+            cx = ox;
+            cy = oy;
+        }
+    }
+    __syncwarp();
+    count = 0;
+}
+
+// Queue the candidate splits of the outputs flagged in pm (bit I: output E' = blk + I of
+// this lane; warp-collective).  Per output, the contributions t = 0..TE-1 (streamed cell
+// e = E' - t) whose own bound passes the current filter are queued.
+//  LT = true : tile = LEFT child (row rowB, s = S0 + t), stream = RIGHT child (row rs,
+//              S_R = rs + e); key = l1<<20 | rowB<<10 | s.
+//  LT = false: tile = RIGHT child (row rowB, S_R = S0 + t), stream = LEFT child (row rs,
+//              s = rs + e); key = l1<<20 | rs<<10 | s.
 template <int TE, bool LT>
-__device__ __forceinline__ void run_rows(XRing &xr, int M, int ls, int r_lo, int r_hi,
-                                         const double (&RT1)[TE], const double (&RT3)[TE], const double (&RTS)[TE],
-                                         const double (&RC1)[TE], int rowB, int e0, int l1, int L,
-                                         const int *outOff, int nout, unsigned acc_s, unsigned filt_s) {
+__device__ __forceinline__ void xq_push(unsigned pm, int blk, int64_t bidx, int ncell, int64_t srow_idx, int rl, int S0,
+                                     int rs, uint32_t kb, int idx0, const float (&TA)[TE], const float (&TB)[TE],
+                                     const float (&TS)[TE], const float (&TC)[TE], const XRing &xr, int rb,
+                                     uint4 *q, int &count, const Cell4 *CELL, unsigned acc_s, unsigned filt_s,
+                                     unsigned *gfr) {
+    const unsigned lane_lt = (1u << (threadIdx.x & 31)) - 1u;
+    for (;;) {
+        const bool act = pm != 0;
+        if (!__any_sync(0xFFFFFFFFu, act)) break;
+        unsigned cand = 0;
+        int Ep = 0;
+        if (act) {
+            Ep = blk + __ffs(pm) - 1;
+            pm &= pm - 1;
+            float f;
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(f) : "r"(filt_s + 4u * (unsigned)(idx0 + Ep)) : "memory");
+#pragma unroll
+            for (int t = 0; t < TE; ++t) {
+                const int e = Ep - t;
+                if (t < ncell && e >= 0 && e < rl) {
+                    const float fst = (float)((LT ? 3 : 4) * (rs + e));
+                    if (split_lb<LT>(TA[t], TB[t], TS[t], TC[t], *xr_at(xr, rb + e), fst) <= f) cand |= 1u << t;
+                }
+            }
+        }
+        for (;;) {
+            const bool h = cand != 0;
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, h);
+            if (!bal) break;
+            const int n = __popc(bal);
+            if (count + n > XQ_CAP) xq_flush(q, count, CELL, acc_s, filt_s, gfr);
+            if (h) {
+                const int t = __ffs(cand) - 1;
+                cand &= cand - 1;
+                const int e = Ep - t;
+                const unsigned addL = LT ? 3u * (unsigned)(rs + e) : 3u * (unsigned)(S0 + t);
+                const unsigned addR = LT ? 4u * (unsigned)(S0 + t) : 4u * (unsigned)(rs + e);
+                q[count + __popc(bal & lane_lt)] =
+                    make_uint4((unsigned)(bidx + t), (unsigned)(srow_idx + e), LT ? kb + (uint32_t)t : kb + (uint32_t)e,
+                               (unsigned)(idx0 + Ep) | (addL << 13) | (addR << 22) | (LT ? 1u << 31 : 0u));
+            }
+            count += n;
+        }
+    }
+}
+
+#ifdef OOB_DBG_FILTER
+// Debug build: an output that did not pass must not hold a split that beats (or ties with a
+// smaller key) the accumulator entry; violations are recorded in g_dbg.
+__device__ unsigned long long g_dbg[256];
+template <int TE, bool LT>
+__device__ void dbg_check(const Cell4 *bp, int ncell, const Cell4 *srow, int rl, int Ep, int S0, int rs, uint32_t kb,
+                          unsigned acc_s, int idx, float mnv, float fv, const float (&TA)[TE], const float (&TB)[TE],
+                          const float (&TS)[TE], const float (&TC)[TE], const XRing &xr, int rb) {
+    unsigned long long cx, cy;
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(cx), "=l"(cy) : "r"(acc_s + 16u * (unsigned)idx) : "memory");
+    for (int t = 0; t < TE; ++t) {
+        const int e = Ep - t;
+        if (t >= ncell || e < 0 || e >= rl) continue;
+        const Cell4 tc = d_load(bp + t), sc = d_load(srow + e);
+        double tot;
+        uint32_t key;
+        if (LT) {
+            tot = split_total(tc.T1, tc.T3, tc.TS, __dadd_rn(tc.C1, (double)(3 * (rs + e))), sc.T1, sc.T3, sc.TS,
+                              __dadd_rn(sc.C1, (double)(4 * (S0 + t))));
+            key = kb + (uint32_t)t;
+        } else {
+            tot = split_total(sc.T1, sc.T3, sc.TS, __dadd_rn(sc.C1, (double)(3 * (S0 + t))), tc.T1, tc.T3, tc.TS,
+                              __dadd_rn(tc.C1, (double)(4 * (rs + e))));
+            key = kb + (uint32_t)e;
+        }
+        const unsigned long long tb = (unsigned long long)__double_as_longlong(tot);
+        if (lex_less(tb, key, cx, (uint32_t)cy)) {
+            const unsigned long long n = atomicAdd(&g_dbg[0], 1ull);
+            if (n < 7) {
+                unsigned long long *r = g_dbg + 1 + 9 * n;
+                r[0] = tb; r[1] = cx; r[2] = key | ((unsigned long long)(uint32_t)cy << 32);
+                r[3] = __float_as_uint(mnv) | ((unsigned long long)__float_as_uint(fv) << 32);
+                r[4] = (unsigned long long)t | ((unsigned long long)e << 16) | ((unsigned long long)Ep << 32);
+                r[5] = (unsigned long long)LT | ((unsigned long long)TE << 8) | ((unsigned long long)rl << 16) |
+                       ((unsigned long long)ncell << 32);
+                const float4 ts = LT ? make_float4(0, 0, 0, 0) : make_float4(0, 0, 0, 0);
+                (void)ts;
+                r[6] = (unsigned long long)idx | ((unsigned long long)S0 << 32);
+                r[7] = (unsigned long long)rs;
+                r[8] = (unsigned long long)(threadIdx.x & 31);
+                if (n < 3) {
+                    float *q = reinterpret_cast<float *>(g_dbg + 100 + 8 * n);
+                    float ta = 0, tb = 0, tsv = 0, tcv = 0;
+#pragma unroll
+                    for (int tt = 0; tt < TE; ++tt)
+                        if (tt == t) { ta = TA[tt]; tb = TB[tt]; tsv = TS[tt]; tcv = TC[tt]; }
+                    q[0] = ta; q[1] = tb; q[2] = tsv; q[3] = tcv;
+                    const float4 x = *xr_at(xr, rb + e);
+                    q[4] = x.x; q[5] = x.y; q[6] = x.z; q[7] = x.w;
+                    const float4 a = __ldcg(reinterpret_cast<const float4 *>(xr.src - (threadIdx.x & 31) * 16) + rb + e),
+                                 b = d_shadow(sc.T1, sc.T3, sc.TS, sc.C1);
+                    r[7] = (unsigned long long)rs | ((unsigned long long)xr.nb_ok << 16) | ((unsigned long long)xr.nb_iss << 32) |
+                           ((unsigned long long)rb << 48);
+                    q[8] = a.x; q[9] = a.y; q[10] = a.z; q[11] = a.w;
+                    q[12] = b.x; q[13] = b.y; q[14] = b.z; q[15] = b.w;
+                }
+            }
+        }
+    }
+}
+#endif
+
+// One step (streamed cell x, uniform factor fst: LT 3 S_R, else 4 s) of a lane's TE splits:
+// lower bounds into the ring slots (output E' = e + t lives in slot E' mod TE; its first
+// contribution t = TE-1 assigns the slot).
+template <int TE, bool LT>
+__device__ __forceinline__ void fast_step(const float4 x, float fst, int I, const float (&TA)[TE],
+                                          const float (&TB)[TE], const float (&TS)[TE], const float (&TC)[TE],
+                                          float (&mn)[TE]) {
+#pragma unroll
+    for (int t = 0; t < TE; ++t) {
+        const int sl = (I + t) % TE;
+        const float lb = split_lb<LT>(TA[t], TB[t], TS[t], TC[t], x, fst);
+        mn[sl] = (t == TE - 1) ? lb : fminf(mn[sl], lb);
+    }
+}
+
+// The small-side rows r_lo..r_hi-1 of one unit against this lane's register tile (shadow
+// lower bounds TA/TB/TS/TC; binary64 tile at bp for the exact path).  Each row runs full
+// blocks of TE steps (no guards) and a guarded tail; the outputs whose bounds pass the
+// filter are collected per block (bit mask) and re-evaluated exactly.
+template <int TE, bool LT>
+__device__ __forceinline__ void run_rows(XRing &xr, int64_t sidx, int M, int ls, int r_lo, int r_hi,
+                                         const float (&TA)[TE], const float (&TB)[TE], const float (&TS)[TE],
+                                         const float (&TC)[TE], int64_t bidx, int ncell, int rowB, int e0,
+                                         int l1, int L, const int *outOff, int nout, unsigned acc_s,
+                                         unsigned filt_s, unsigned *gfr, uint4 *xq_buf, const Cell4 *CELL) {
+    int qn = 0;                                           // queued candidates (warp-uniform)
     const int S0 = rowB + e0;
-    const double xadd = (double)((LT ? 4 : 3) * S0);
+    const float *filt = reinterpret_cast<const float *>(__cvta_shared_to_generic(filt_s));
     int rb = 0;                                           // chunk cell of the row's first cell
     for (int rs = r_lo; rs < r_hi; ++rs) {
         const int rl = c_wlen(M, ls, rs);
         const int q = rowB + rs;
         const int ob = outOff[min(q, L + 1)];
         const int idx0 = (ob == nout) ? nout : ob + e0;  // accumulator entry of E' = 0
-        double cst = (double)((LT ? 3 : 4) * rs);
         const uint32_t kb = LT ? (((uint32_t)l1 << 20) | ((uint32_t)rowB << 10) | (uint32_t)S0)
                                : (((uint32_t)l1 << 20) | ((uint32_t)rs << 10) | (uint32_t)rs);
-        double best[TE];
-        int widx[TE];
+        const int64_t srow = sidx + rb;
+        const float *fr = filt + idx0;
+        float fst = (float)((LT ? 3 : 4) * rs);
+        float mn[TE];
 #pragma unroll
-        for (int t = 0; t < TE; ++t) { best[t] = D_INF; widx[t] = 0; }
-        xr_ensure(xr, rb + TE);
+        for (int t = 0; t < TE; ++t) mn[t] = __int_as_float(0x7f800000);
         int blk = 0;
-        const double2 *xq = xr_at(xr, rb);
-#define OOB_STEP(I)                                                                             \
-    {                                                                                           \
-        const Cell4 x = xr_cell(xq, (I));                                                       \
-        const double xc = __dadd_rn(x.C1, xadd);                                                \
-        _Pragma("unroll") for (int t = 0; t < TE; ++t) {                                        \
-            const int sl = ((I) + t) % TE;                                                      \
-            const double cs = t == 0 ? xc : __dadd_rn(xc, (double)((LT ? 4 : 3) * t));          \
-            const double ct = __dadd_rn(RC1[t], cst);                                           \
-            const double tot = LT ? split_total(RT1[t], RT3[t], RTS[t], ct, x.T1, x.T3, x.TS, cs) \
-                                  : split_total(x.T1, x.T3, x.TS, cs, RT1[t], RT3[t], RTS[t], ct); \
-            if (t == TE - 1) {                                                                  \
-                best[sl] = tot;                                                                 \
-                widx[sl] = t;                                                                   \
-            } else {                                                                            \
-                const bool upd = LT ? (tot <= best[sl]) : (tot < best[sl]);                     \
-                best[sl] = upd ? tot : best[sl];                                                \
-                widx[sl] = upd ? t : widx[sl];                                                  \
-            }                                                                                   \
-        }                                                                                       \
-        cst = __dadd_rn(cst, LT ? 3.0 : 4.0);                                                   \
-        acc_flush(acc_s, filt_s, idx0 + blk + (I), best[(I)],                                   \
-                  LT ? kb + (uint32_t)widx[(I)] : kb + (uint32_t)(blk + (I) - widx[(I)]));      \
-    }
-        // blocks of TE steps; the last one stops at the row end (one copy of the step code
-        // keeps the kernel inside the instruction cache)
+        const int full = rl - rl % TE;
 #pragma unroll 1
-        for (; blk < rl; blk += TE) {
+        for (; blk < full; blk += TE) {
             xr_ensure(xr, rb + blk + TE);
-            xq = xr_at(xr, rb + blk);
+            const float4 *xq = xr_at(xr, rb + blk);
+            unsigned pm = 0;
 #pragma unroll
+            for (int I = 0; I < TE; ++I) {
+                fast_step<TE, LT>(xq[I], fst, I, TA, TB, TS, TC, mn);
+                fst += LT ? 3.0f : 4.0f;
+                pm |= (mn[I] <= fr[blk + I]) ? (1u << I) : 0u;
+            }
+#ifdef OOB_DBG_FILTER
             for (int I = 0; I < TE; ++I)
-                if (I == 0 || blk + I < rl) OOB_STEP(I)
+                if (!((pm >> I) & 1))
+                    dbg_check<TE, LT>(CELL + bidx, ncell, CELL + srow, rl, blk + I, S0, rs, kb, acc_s, idx0 + blk + I,
+                                      mn[I], fr[blk + I], TA, TB, TS, TC, xr, rb);
+#endif
+            if (__any_sync(0xFFFFFFFFu, pm != 0))
+                xq_push<TE, LT>(pm, blk, bidx, ncell, srow, rl, S0, rs, kb, idx0, TA, TB, TS, TC, xr, rb, xq_buf, qn,
+                                CELL, acc_s, filt_s, gfr);
         }
-#undef OOB_STEP
-        // pending: slot sl holds E' = rl + ((sl - rl) mod TE); E' = rl + TE - 1 is the slot of
-        // E' = rl - 1, already flushed
+        // tail block (rl % TE steps) and the pending outputs E' = rl .. rl + TE - 2
+        {
+            xr_ensure(xr, rb + blk + TE);
+            const float4 *xq = xr_at(xr, rb + blk);
+            unsigned pm = 0;
 #pragma unroll
-        for (int sl = 0; sl < TE; ++sl) {
-            const int Ep = rl + (((sl - rl) % TE) + TE) % TE;
-            if (Ep <= rl + TE - 2)
-                acc_flush(acc_s, filt_s, idx0 + Ep, best[sl],
-                          LT ? kb + (uint32_t)widx[sl] : kb + (uint32_t)(Ep - widx[sl]));
+            for (int I = 0; I < TE - 1; ++I) {
+                if (blk + I < rl) {
+                    fast_step<TE, LT>(xq[I], fst, I, TA, TB, TS, TC, mn);
+                    fst += LT ? 3.0f : 4.0f;
+                    pm |= (mn[I] <= fr[blk + I]) ? (1u << I) : 0u;
+                }
+            }
+            // slot sl holds E' = rl + ((sl - rl) mod TE) for the pending outputs
+#pragma unroll
+            for (int sl = 0; sl < TE; ++sl) {
+                const int Ep = rl + (((sl - rl) % TE) + TE) % TE;
+                if (Ep <= rl + TE - 2 && mn[sl] <= fr[Ep]) pm |= 1u << (Ep - blk);
+            }
+            if (__any_sync(0xFFFFFFFFu, pm != 0))
+                xq_push<TE, LT>(pm, blk, bidx, ncell, srow, rl, S0, rs, kb, idx0, TA, TB, TS, TC, xr, rb, xq_buf, qn,
+                                CELL, acc_s, filt_s, gfr);
         }
         rb += rl;
     }
+    if (qn) xq_flush(xq_buf, qn, CELL, acc_s, filt_s, gfr);
     asm volatile("cp.async.wait_group 0;" ::: "memory");   // no copy of this chunk outlives the unit
     __syncwarp();
 }
@@ -385,6 +561,7 @@ __device__ __forceinline__ void fin_w_one(const DevGeom &g, const FinArgs &f, in
     ulonglong2 *ga = f.GACC + t;
     ulonglong2 a = __ldcg(ga);
     __stcg(ga, make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull));
+    __stcg(f.GFW + t, FILT_EMPTY);
     for (int r = 0; r < f.world && f.world > 1; ++r) {   // lexicographic min over the ranks
         const ulonglong2 b = __ldcg(f.GPART + (int64_t)r * f.part_stride + t);
         if (lex_less(b.x, (uint32_t)b.y, a.x, (uint32_t)a.y)) a = b;
@@ -392,9 +569,7 @@ __device__ __forceinline__ void fin_w_one(const DevGeom &g, const FinArgs &f, in
     const int64_t pc = (int64_t)p * g.C;
     const int aW = (g.M - 1) + q - 1;
     if (a.x >= ACC_EMPTY) {   // no split found: impossible for a valid cell; poison it
-        const int64_t c = pc + d_cell(g, Sp, u, l, aW);
-        g.CELL[c].T1 = __longlong_as_double(0x7ff8000000000000LL);
-        g.ARG[c] = 0xFFFFFFFEu;
+        d_poison(g, pc + d_cell(g, Sp, u, l, aW), 0xFFFFFFFEu);
         return;
     }
     const uint32_t key = (uint32_t)a.y;
@@ -403,9 +578,7 @@ __device__ __forceinline__ void fin_w_one(const DevGeom &g, const FinArgs &f, in
     const int l2 = l - l1, jr = q - j, sr = Sp - s;
     if (l1 < 1 || l2 < 1 || j < 1 || jr < 1 || s < j || sr < jr || s > min(l1, g.M * j) ||
         sr > min(l2, g.M * jr)) {
-        const int64_t c = pc + d_cell(g, Sp, u, l, aW);
-        g.CELL[c].T1 = __longlong_as_double(0x7ff8000000000000LL);
-        g.ARG[c] = 0xFFFFFFFDu;
+        d_poison(g, pc + d_cell(g, Sp, u, l, aW), 0xFFFFFFFDu);
         return;
     }
     d_write_winner(g, pc, Sp, u, l, aW, l1, j - 1, s);
@@ -443,6 +616,7 @@ __device__ __forceinline__ void fin_w_range(const DevGeom &g, const FinArgs &f, 
             ulonglong2 *ga = f.GACC + (int64_t)pr * nout + i;
             a[j] = __ldcg(ga);
             __stcg(ga, make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull));
+            __stcg(f.GFW + (int64_t)pr * nout + i, FILT_EMPTY);
         }
         Cell4 Lc[FB], Rc[FB];
         int l1v[FB], sv[FB], ok[FB];
@@ -454,9 +628,7 @@ __device__ __forceinline__ void fin_w_range(const DevGeom &g, const FinArgs &f, 
             if (q[j] < 2) continue;
             const int aW = (M - 1) + q[j] - 1;
             if (a[j].x >= ACC_EMPTY) {       // no split found: impossible for a valid cell; poison it
-                const int64_t c = pc + d_cell(g, Sp[j], u, l, aW);
-                g.CELL[c].T1 = __longlong_as_double(0x7ff8000000000000LL);
-                g.ARG[c] = 0xFFFFFFFEu;
+                d_poison(g, pc + d_cell(g, Sp[j], u, l, aW), 0xFFFFFFFEu);
                 continue;
             }
             const uint32_t key = (uint32_t)a[j].y;
@@ -464,9 +636,7 @@ __device__ __forceinline__ void fin_w_range(const DevGeom &g, const FinArgs &f, 
             const int l2 = l - l1, jr = q[j] - jj, sr = Sp[j] - s;
             if (l1 < 1 || l2 < 1 || jj < 1 || jr < 1 || s < jj || sr < jr || s > min(l1, M * jj) ||
                 sr > min(l2, M * jr)) {      // corrupt key: flag, never read outside the table
-                const int64_t c = pc + d_cell(g, Sp[j], u, l, aW);
-                g.CELL[c].T1 = __longlong_as_double(0x7ff8000000000000LL);
-                g.ARG[c] = 0xFFFFFFFDu;
+                d_poison(g, pc + d_cell(g, Sp[j], u, l, aW), 0xFFFFFFFDu);
                 continue;
             }
             // children W(jj) of (u, u+l1) and W(jr) of (u+l1, u+l)
@@ -485,7 +655,7 @@ __device__ __forceinline__ void fin_w_range(const DevGeom &g, const FinArgs &f, 
             const bool left = Lc[j].TS >= Rc[j].TS;
             const double kd = left ? d_kd(Lc[j].C1, s) : __dadd_rn((double)s, d_kd(Rc[j].C1, Sp[j] - s));
             const int64_t c = pc + d_cell(g, Sp[j], u, l, (M - 1) + q[j] - 1);
-            d_store(g.CELL + c, __dadd_rn(Lc[j].T1, Rc[j].T1), left ? __dadd_rn(Lc[j].T3, Rc[j].T1) : Rc[j].T3,
+            d_store(g, c, __dadd_rn(Lc[j].T1, Rc[j].T1), left ? __dadd_rn(Lc[j].T3, Rc[j].T1) : Rc[j].T3,
                     left ? Lc[j].TS : Rc[j].TS, d_c1(kd, Sp[j]));
             g.ARG[c] = (uint32_t)(l1v[j] - 1) | ((uint32_t)(jj - 1) << 10) | ((uint32_t)s << 20);
         }
@@ -585,6 +755,7 @@ __device__ __forceinline__ void fin_seed_one(const DevGeom &g, const FinArgs &f,
         }
     }
     __stcg(f.GSEED + t, make_ulonglong2(bb, (unsigned long long)bk));
+    __stcg(f.GFS + t, __float_as_uint(filt_of(bb)));
     return;
 }
 
@@ -687,9 +858,9 @@ __global__ void __launch_bounds__(NTW, 2) k_wave_w(DevGeom g, WaveW w) {
     const int l = w.l;
     const int nout = w.nout;
     const int L = g.L, M = g.M;
-    const int ndum = L + 2 * TE + 2;                              // dummy entries
+    const int ndum = L + 2 * TE + 2;                              // dummy entries (absent parent rows)
     ulonglong2 *acc = reinterpret_cast<ulonglong2 *>(smem);     // [nout] + dummy[ndum]
-    unsigned *filt = reinterpret_cast<unsigned *>(acc + nout + ndum);  // [nout + ndum] high words
+    unsigned *filt = reinterpret_cast<unsigned *>(acc + nout + ndum);  // [nout + ndum] binary32 filters F(min)
     int4 *sents = reinterpret_cast<int4 *>(filt + ((nout + ndum + 3) & ~3));   // [nents] (16 B aligned)
     int64_t *sbase = reinterpret_cast<int64_t *>(sents + w.nents);               // [L+2]
     int *scells = reinterpret_cast<int *>(sbase + L + 2);        // [L+1]
@@ -697,7 +868,7 @@ __global__ void __launch_bounds__(NTW, 2) k_wave_w(DevGeom g, WaveW w) {
     int *upre = outOff + (L + 2);                                // [nents + 1]
     // per-warp streamed-side rings (16 B aligned) after upre
     const size_t ring_off = ((size_t)(reinterpret_cast<unsigned char *>(upre + w.nents + 1) - smem) + 15) & ~(size_t)15;
-    double2 *rings = reinterpret_cast<double2 *>(smem + ring_off);
+    float4 *rings = reinterpret_cast<float4 *>(smem + ring_off);
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int pr = blockIdx.x / w.cpr;
@@ -707,12 +878,13 @@ __global__ void __launch_bounds__(NTW, 2) k_wave_w(DevGeom g, WaveW w) {
     const int Ql = (l == L) ? g.n_hi : max(1, g.n_hi - 1);
 
     const ulonglong2 *gseed = w.GACC + ((size_t)(blockIdx.x / w.cpr)) * nout;   // this range's entries
+    unsigned *gfilt = w.GFILT + ((size_t)(blockIdx.x / w.cpr)) * nout;
     for (int i = tid; i < nout + ndum; i += NTW) {
         const bool real = i < nout;
         ulonglong2 a = real ? make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull) : make_ulonglong2(0ull, 0ull);
         if (real && w.seeded) a = __ldcg(gseed + i);
         acc[i] = a;
-        filt[i] = real ? (unsigned)(a.x >> 32) : 0u;
+        filt[i] = real ? min(__float_as_uint(filt_of(a.x)), __ldcg(gfilt + i)) : 0xBF800000u;   // dummies: -1
     }
     for (int i = tid; i < L + 2; i += NTW) {
         sbase[i] = g.base[i];
@@ -762,28 +934,46 @@ __global__ void __launch_bounds__(NTW, 2) k_wave_w(DevGeom g, WaveW w) {
         const int e0 = has ? (code & 0xFFFF) : 0;
         const int lenB = has ? c_wlen(M, lb, rowB) : 0;
         const int ncell = max(0, min(TE, lenB - e0));             // valid cells of the tile
-        const Cell4 *bp = g.CELL + pc + sbase[lb] + (int64_t)ub * scells[lb] + c_ipart(M, lb) +
-                          (has ? c_woff(M, lb, rowB) : 0) + e0;
-        // register tile: T1, T3, t*, C1 of TE big-side cells (sentinels beyond the row)
-        double RT1[TE], RT3[TE], RTS[TE], RC1[TE];
+        // register tile: shadow lower bounds of TE big-side cells (+inf beyond the row: every
+        // bound of a sentinel is +inf and never passes)
+        const int64_t bidx = pc + sbase[lb] + (int64_t)ub * scells[lb] + c_ipart(M, lb) +
+                             (has ? c_woff(M, lb, rowB) : 0) + e0;
+        float TA[TE], TB[TE], TS[TE], TC[TE];
 #pragma unroll
         for (int t = 0; t < TE; ++t) {
-            if (t < ncell) {
-                const Cell4 c = d_load(bp + t);
-                RT1[t] = c.T1; RT3[t] = c.T3; RTS[t] = c.TS; RC1[t] = c.C1;
-            } else {
-                RT1[t] = D_INF; RT3[t] = D_INF; RTS[t] = D_INF; RC1[t] = 1.0;
+            const float inf = __int_as_float(0x7f800000);
+            float4 c = make_float4(inf, inf, inf, inf);
+            if (t < ncell) c = __ldg(g.SH + bidx + t);
+            TA[t] = c.x;
+            TB[t] = ltiled ? c.y : c.w;
+            TS[t] = c.z;
+            TC[t] = (float)((ltiled ? 4 : 3) * (rowB + e0 + t));
+        }
+        {   // refresh the filter of the outputs this unit can touch (rows q = rowB + rs) from the
+            // range's global filter: minima other CTAs found since this CTA last looked
+            const int tb0 = blk * 32, tb1 = min(blk * 32 + 31, w.tile_cnt[lb] - 1);
+            const int rmin = w.tiles[w.tile_off[lb] + tb0] >> 16, rmax = w.tiles[w.tile_off[lb] + tb1] >> 16;
+            const int olo = outOff[min(rmin + r_lo, L + 1)], ohi = outOff[min(rmax + r_hi, L + 1)];
+            for (int i0 = olo + lane; i0 < ohi; i0 += 128) {   // 4 loads in flight per lane
+                unsigned gv[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) gv[j] = i0 + 32 * j < ohi ? __ldcg(gfilt + i0 + 32 * j) : 0xFFFFFFFFu;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (gv[j] < filt[i0 + 32 * j]) atomicMin(filt + i0 + 32 * j, gv[j]);
             }
         }
-        const Cell4 *sp = g.CELL + pc + sbase[ls] + (int64_t)us * scells[ls] + c_ipart(M, ls);
+        const int64_t sidx = pc + sbase[ls] + (int64_t)us * scells[ls] + c_ipart(M, ls) + c_woff(M, ls, r_lo);
+        unsigned char *wsm = reinterpret_cast<unsigned char *>(rings) + (size_t)(tid >> 5) * (XR_BYTES + XQ_BYTES);
+        uint4 *xq_buf = reinterpret_cast<uint4 *>(wsm + XR_BYTES);   // this warp's candidate queue
         XRing xr;                                            // rows r_lo.. are contiguous
-        xr_start(xr, rings + (size_t)(tid >> 5) * (XR_BYTES / 16), sp + c_woff(M, ls, r_lo), lane);
+        xr_start(xr, reinterpret_cast<float4 *>(wsm), g.SH + sidx, lane);
         if (ltiled)
-            run_rows<TE, true>(xr, M, ls, r_lo, r_hi, RT1, RT3, RTS, RC1, rowB, e0, l1, L, outOff, nout, acc_s,
-                               filt_s);
+            run_rows<TE, true>(xr, sidx, M, ls, r_lo, r_hi, TA, TB, TS, TC, bidx, ncell, rowB, e0, l1, L, outOff, nout,
+                               acc_s, filt_s, gfilt, xq_buf, g.CELL);
         else
-            run_rows<TE, false>(xr, M, ls, r_lo, r_hi, RT1, RT3, RTS, RC1, rowB, e0, l1, L, outOff, nout, acc_s,
-                                filt_s);
+            run_rows<TE, false>(xr, sidx, M, ls, r_lo, r_hi, TA, TB, TS, TC, bidx, ncell, rowB, e0, l1, L, outOff,
+                                nout, acc_s, filt_s, gfilt, xq_buf, g.CELL);
     }
     __syncthreads();
     // merge into the range's global accumulator (L2-coherent loads; a stale value is an
@@ -823,9 +1013,12 @@ __global__ void __launch_bounds__(NTW, 2) k_wave_w(DevGeom g, WaveW w) {
     }
 }
 
-__global__ void k_gacc_init(ulonglong2 *gacc, int64_t n) {
+__global__ void k_gacc_init(ulonglong2 *gacc, unsigned *gfilt, int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) gacc[i] = make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull);
+    if (i < n) {
+        gacc[i] = make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull);
+        gfilt[i] = FILT_EMPTY;
+    }
 }
 
 }  // namespace oob
