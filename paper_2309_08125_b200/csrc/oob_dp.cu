@@ -188,7 +188,7 @@ struct WCfg { int te, nt; };
 constexpr WCfg WCFGS[] = {{4, NTW}, {5, NTW}, {3, NTW}, {2, NTW}};
 constexpr double SHARD_MIN_SPLITS = 2e7;   // wavefronts sharded across ranks (oob_dp_set_comm)
 constexpr int SEED_MIN_L = 6;      // waves seeded with proportional splits (k_fin)
-constexpr int CTAS_PER_SM = 512 / NTW;   // k_wave_w: 16 resident warps per SM (register bound: 128 regs)
+constexpr int CTAS_PER_SM = WAVE_CTAS_PER_SM;   // k_wave_w: resident CTAs per SM (register bound; smem may allow fewer)
 constexpr int NWCFG = 4;
 
 struct WaveHost {
@@ -403,15 +403,20 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
             WaveHost wh;
             // smaller chunks (more, shorter units) until every warp slot has ~4 units and every
             // CTA has >= units_per_cta units of its range's queue (short tails per CTA)
-            for (int CH = 96;; CH /= 2) {
-                build_wave(pl, l, ci, CTAS_PER_SM * 148, wh, CH);
-                if (CH <= 12 || ((int64_t)wh.nunits * num_profiles * (L - l + 1) >= 4LL * CTAS_PER_SM * 148 * (NTW / 32) &&
-                                 wh.nunits >= pl->units_per_cta * wh.cpr))
-                    break;
+            // resident CTAs per SM: launch bounds (registers), then shared memory
+            int per_sm = CTAS_PER_SM;
+            for (int pass = 0; pass < 2; ++pass) {
+                for (int CH = 96;; CH /= 2) {
+                    build_wave(pl, l, ci, per_sm * 148, wh, CH);
+                    if (CH <= 12 || ((int64_t)wh.nunits * num_profiles * (L - l + 1) >= 4LL * per_sm * 148 * (NTW / 32) &&
+                                     wh.nunits >= pl->units_per_cta * wh.cpr))
+                        break;
+                }
+                const int by_smem = std::max<int>(1, (int)((228 * 1024) / (std::max<size_t>(wh.smem, 1) + 1024)));
+                const int ps = std::max(1, std::min(CTAS_PER_SM, by_smem));
+                if (ps == per_sm) break;
+                per_sm = ps;
             }
-            // resident CTAs per SM: launch bounds 256 x 2, smem
-            const int by_smem = std::max<int>(1, (int)((227 * 1024) / std::max<size_t>(wh.smem, 1)));
-            const int per_sm = std::max(1, std::min(CTAS_PER_SM, by_smem));
             const double warps_per_smsp = per_sm * (NTW / 32) / 4.0;
             // issue efficiency saturates at ~4 resident warps per scheduler; TE = 5 (larger
             // code, measured slower on B200) is kept as a forced option (OOB_DP_WCFG=1)

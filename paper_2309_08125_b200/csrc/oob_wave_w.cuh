@@ -38,6 +38,7 @@
 namespace oob {
 
 constexpr int NTW = 256;                                          // threads per k_wave_w CTA
+constexpr int WAVE_CTAS_PER_SM = 2;                               // register budget: 128 per thread
 constexpr unsigned long long ACC_EMPTY = 0x7FEFFFFFFFFFFFFFull;   // DBL_MAX: "no split yet"
 constexpr double D_INF = __builtin_huge_val();
 
@@ -267,117 +268,113 @@ __device__ __forceinline__ float split_lb(float TA, float TB, float TS, float TC
     }
 }
 
-// Candidate queue: the splits whose lower bound passes the filter are not evaluated in place
-// (divergent, global-latency bound) but appended to a per-warp queue in shared memory and
-// evaluated by the whole warp, one split per lane, when the queue is full and at the end of
-// each unit.  An entry (16 B): the two children's table indices, the split key, and
-// idx | addL << 13 | addR << 22 | LT << 31 (accumulator entry, the exact integers added to
-// the left / right child's C1 for the parent's coefficient, tile = left child).
+// Candidate queue: the outputs whose slot bound passes the filter are not re-evaluated in
+// place (divergent, global-latency bound) but appended to a per-warp queue in shared memory
+// and re-evaluated by the whole warp, one output per lane, when the queue is full and at the
+// end of each unit.  An entry (24 B) names one output E' of one (tile, streamed row) pair:
+//   x = tile cell index, y = streamed row's first cell index, z = key base kb,
+//   w = accumulator entry | E' << 13 | ncell << 20 | LT << 23 | rl << 24,
+//   v = the stage count the key does not carry (LT: rs, else S0).
 constexpr int XQ_CAP = 32;
-constexpr int XQ_BYTES = XQ_CAP * 16;     // per warp
+constexpr int XQ_BYTES = XQ_CAP * 24;     // per warp
 
-// Exact evaluation of the queued splits (warp-collective; lane i takes entry i) in binary64
-// in the oracle's operation order; each result is merged as the lexicographic minimum of
-// (total, key) with the 128-bit CAS into the CTA's accumulator entry (entries only
-// decrease: a stale read is an upper bound, the loop stays exact), then the CTA's and the
-// range's global filters are lowered.
-__device__ __forceinline__ void xq_flush(const uint4 *q, int &count, const Cell4 *CELL, unsigned acc_s,
-                                         unsigned filt_s, unsigned *gfr) {
+// Exact evaluation of the queued outputs (warp-collective; lane i takes entry i): every
+// valid contribution t (tile cell t, streamed cell e = E' - t) in binary64 in the oracle's
+// operation order, the lexicographic minimum of (total, key), merged with the 128-bit CAS
+// into the CTA's accumulator entry (entries only decrease: a stale read is an upper bound,
+// the loop stays exact); then the CTA's and the range's global filters are lowered.
+//  LT = true : tile = LEFT child (s = S0 + t), stream = RIGHT child (S_R = rs + e);
+//              key = kb + t, kb = l1<<20 | rowB<<10 | S0.
+//  LT = false: tile = RIGHT child (S_R = S0 + t), stream = LEFT child (s = rs + e);
+//              key = kb + e, kb = l1<<20 | rs<<10 | rs.
+template <int TE>
+__device__ __noinline__ void xq_flush(const uint4 *q4, const unsigned *q1, int count, const Cell4 *CELL,
+                                      unsigned acc_s, unsigned filt_s, unsigned *gfr) {
     __syncwarp();
     const int lane = threadIdx.x & 31;
     if (lane < count) {
-        const uint4 en = q[lane];
-        const bool lt = en.w >> 31;
-        const int idx = (int)(en.w & 8191u);
-        const Cell4 tc = d_load(CELL + en.x), sc = d_load(CELL + en.y);
-        const Cell4 &Lc = lt ? tc : sc, &Rc = lt ? sc : tc;
-        const double cL = __dadd_rn(Lc.C1, (double)((en.w >> 13) & 511u));
-        const double cR = __dadd_rn(Rc.C1, (double)((en.w >> 22) & 511u));
-        const double tot = split_total(Lc.T1, Lc.T3, Lc.TS, cL, Rc.T1, Rc.T3, Rc.TS, cR);
-        const unsigned long long bb = (unsigned long long)__double_as_longlong(tot);
-        const uint32_t bk = en.z;
-        const unsigned addr = acc_s + 16u * (unsigned)idx;
-        unsigned long long cx, cy;
-        asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(cx), "=l"(cy) : "r"(addr) : "memory");
-#ifdef OOB_FLUSH_STATS
-        if (g_flush_stats_on) {
-            atomicAdd(&g_flush_stats[0], 1ull);
-            if (bb == cx) atomicAdd(&g_flush_stats[2], 1ull);
-            else if (bb > cx) atomicAdd(&g_flush_stats[3], 1ull);
-        }
-#endif
-        while (lex_less(bb, bk, cx, (uint32_t)cy)) {
-            unsigned long long ox, oy;
-            cas128_shared(addr, ox, oy, cx, cy, bb, (unsigned long long)bk);
-            if (ox == cx && oy == cy) {
-#ifdef OOB_FLUSH_STATS
-                if (g_flush_stats_on) atomicAdd(&g_flush_stats[1], 1ull);
-#endif
-                const unsigned fb = __float_as_uint(filt_of(bb));
-                asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(filt_s + 4u * (unsigned)idx), "r"(fb) : "memory");
-                atomicMin(gfr + idx, fb);     // share with the range's other CTAs (refreshed per unit)
-                break;
+        const uint4 en = q4[lane];
+        const unsigned v = q1[lane];
+        const int idx = (int)(en.w & 8191u), Ep = (int)((en.w >> 13) & 127u), ncell = (int)((en.w >> 20) & 7u);
+        const bool lt = (en.w >> 23) & 1u;
+        const int rl = (int)(en.w >> 24);
+        const int rs = lt ? (int)v : (int)(en.z & 1023u), S0 = lt ? (int)(en.z & 1023u) : (int)v;
+        unsigned long long bb = ACC_EMPTY;
+        uint32_t bk = 0xFFFFFFFFu;
+#pragma unroll
+        for (int t = 0; t < TE; ++t) {
+            const int e = Ep - t;
+            if (t < ncell && e >= 0 && e < rl) {
+                const Cell4 tc = d_load(CELL + en.x + t), sc = d_load(CELL + en.y + e);
+                const Cell4 &Lc = lt ? tc : sc, &Rc = lt ? sc : tc;
+                const int sL = lt ? S0 + t : rs + e, sR = lt ? rs + e : S0 + t;   // stages of left / right
+                const double cL = __dadd_rn(Lc.C1, (double)(3 * sR));
+                const double cR = __dadd_rn(Rc.C1, (double)(4 * sL));
+                const double tot = split_total(Lc.T1, Lc.T3, Lc.TS, cL, Rc.T1, Rc.T3, Rc.TS, cR);
+                const unsigned long long tb = (unsigned long long)__double_as_longlong(tot);
+                const uint32_t key = en.z + (uint32_t)(lt ? t : e);
+                if (lex_less(tb, key, bb, bk)) { bb = tb; bk = key; }
             }
-            cx = ox;
-            cy = oy;
+        }
+        if (bb < ACC_EMPTY) {
+            const unsigned addr = acc_s + 16u * (unsigned)idx;
+            unsigned long long cx, cy;
+            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(cx), "=l"(cy) : "r"(addr) : "memory");
+#ifdef OOB_FLUSH_STATS
+            if (g_flush_stats_on) {
+                atomicAdd(&g_flush_stats[0], 1ull);
+                if (bb == cx) atomicAdd(&g_flush_stats[2], 1ull);
+                else if (bb > cx) atomicAdd(&g_flush_stats[3], 1ull);
+            }
+#endif
+            while (lex_less(bb, bk, cx, (uint32_t)cy)) {
+                unsigned long long ox, oy;
+                cas128_shared(addr, ox, oy, cx, cy, bb, (unsigned long long)bk);
+                if (ox == cx && oy == cy) {
+#ifdef OOB_FLUSH_STATS
+                    if (g_flush_stats_on) atomicAdd(&g_flush_stats[1], 1ull);
+#endif
+                    const unsigned fb = __float_as_uint(filt_of(bb));
+                    asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(filt_s + 4u * (unsigned)idx), "r"(fb) : "memory");
+                    atomicMin(gfr + idx, fb);     // share with the range's other CTAs (refreshed per unit)
+                    break;
+                }
+                cx = ox;
+                cy = oy;
+            }
         }
     }
     __syncwarp();
-    count = 0;
 }
 
-// Queue the candidate splits of the outputs flagged in pm (bit I: output E' = blk + I of
-// this lane; warp-collective).  Per output, the contributions t = 0..TE-1 (streamed cell
-// e = E' - t) whose own bound passes the current filter are queued.
-//  LT = true : tile = LEFT child (row rowB, s = S0 + t), stream = RIGHT child (row rs,
-//              S_R = rs + e); key = l1<<20 | rowB<<10 | s.
-//  LT = false: tile = RIGHT child (row rowB, S_R = S0 + t), stream = LEFT child (row rs,
-//              s = rs + e); key = l1<<20 | rs<<10 | s.
+// Queue the outputs flagged in `mask` (bit b: output E' = base + b of this lane's tile and
+// the current streamed row; warp-collective, a no-op when no lane has a bit).
 template <int TE, bool LT>
-__device__ __forceinline__ void xq_push(unsigned pm, int blk, int64_t bidx, int ncell, int64_t srow_idx, int rl, int S0,
-                                     int rs, uint32_t kb, int idx0, const float (&TA)[TE], const float (&TB)[TE],
-                                     const float (&TS)[TE], const float (&TC)[TE], const XRing &xr, int rb,
-                                     uint4 *q, int &count, const Cell4 *CELL, unsigned acc_s, unsigned filt_s,
-                                     unsigned *gfr) {
+__device__ __noinline__ int xq_push(unsigned mask, int base, unsigned bidx, int ncell, unsigned srow, int rl, int S0,
+                                    int rs, uint32_t kb, int idx0, uint4 *q4, unsigned *q1, int count,
+                                    const Cell4 *CELL, unsigned acc_s, unsigned filt_s, unsigned *gfr) {
     const unsigned lane_lt = (1u << (threadIdx.x & 31)) - 1u;
     for (;;) {
-        const bool act = pm != 0;
-        if (!__any_sync(0xFFFFFFFFu, act)) break;
-        unsigned cand = 0;
-        int Ep = 0;
-        if (act) {
-            Ep = blk + __ffs(pm) - 1;
-            pm &= pm - 1;
-            float f;
-            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(f) : "r"(filt_s + 4u * (unsigned)(idx0 + Ep)) : "memory");
-#pragma unroll
-            for (int t = 0; t < TE; ++t) {
-                const int e = Ep - t;
-                if (t < ncell && e >= 0 && e < rl) {
-                    const float fst = (float)((LT ? 3 : 4) * (rs + e));
-                    if (split_lb<LT>(TA[t], TB[t], TS[t], TC[t], *xr_at(xr, rb + e), fst) <= f) cand |= 1u << t;
-                }
-            }
+        const bool h = mask != 0;
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, h);
+        if (!bal) break;
+        const int n = __popc(bal);
+        if (count + n > XQ_CAP) {
+            xq_flush<TE>(q4, q1, count, CELL, acc_s, filt_s, gfr);
+            count = 0;
         }
-        for (;;) {
-            const bool h = cand != 0;
-            const unsigned bal = __ballot_sync(0xFFFFFFFFu, h);
-            if (!bal) break;
-            const int n = __popc(bal);
-            if (count + n > XQ_CAP) xq_flush(q, count, CELL, acc_s, filt_s, gfr);
-            if (h) {
-                const int t = __ffs(cand) - 1;
-                cand &= cand - 1;
-                const int e = Ep - t;
-                const unsigned addL = LT ? 3u * (unsigned)(rs + e) : 3u * (unsigned)(S0 + t);
-                const unsigned addR = LT ? 4u * (unsigned)(S0 + t) : 4u * (unsigned)(rs + e);
-                q[count + __popc(bal & lane_lt)] =
-                    make_uint4((unsigned)(bidx + t), (unsigned)(srow_idx + e), LT ? kb + (uint32_t)t : kb + (uint32_t)e,
-                               (unsigned)(idx0 + Ep) | (addL << 13) | (addR << 22) | (LT ? 1u << 31 : 0u));
-            }
-            count += n;
+        if (h) {
+            const int Ep = base + __ffs(mask) - 1;
+            mask &= mask - 1;
+            const int slot = count + __popc(bal & lane_lt);
+            q4[slot] = make_uint4(bidx, srow, kb,
+                                  (unsigned)(idx0 + Ep) | ((unsigned)Ep << 13) | ((unsigned)ncell << 20) |
+                                      (LT ? 1u << 23 : 0u) | ((unsigned)rl << 24));
+            q1[slot] = LT ? (unsigned)rs : (unsigned)S0;
         }
+        count += n;
     }
+    return count;
 }
 
 #ifdef OOB_DBG_FILTER
@@ -466,8 +463,10 @@ __device__ __forceinline__ void run_rows(XRing &xr, int64_t sidx, int M, int ls,
                                          const float (&TA)[TE], const float (&TB)[TE], const float (&TS)[TE],
                                          const float (&TC)[TE], int64_t bidx, int ncell, int rowB, int e0,
                                          int l1, int L, const int *outOff, int nout, unsigned acc_s,
-                                         unsigned filt_s, unsigned *gfr, uint4 *xq_buf, const Cell4 *CELL) {
-    int qn = 0;                                           // queued candidates (warp-uniform)
+                                         unsigned filt_s, unsigned *gfr, uint4 *q4, unsigned *q1,
+                                         const Cell4 *CELL) {
+    static_assert(32 % TE == 0 || TE == 3 || TE == 5, "TE");
+    int qn = 0;                                           // queued outputs (warp-uniform)
     const int S0 = rowB + e0;
     const float *filt = reinterpret_cast<const float *>(__cvta_shared_to_generic(filt_s));
     int rb = 0;                                           // chunk cell of the row's first cell
@@ -486,28 +485,36 @@ __device__ __forceinline__ void run_rows(XRing &xr, int64_t sidx, int M, int ls,
         for (int t = 0; t < TE; ++t) mn[t] = __int_as_float(0x7f800000);
         int blk = 0;
         const int full = rl - rl % TE;
+        unsigned pmask = 0;                               // passed outputs E' = mbase + bit
+        int mbase = 0;
 #pragma unroll 1
         for (; blk < full; blk += TE) {
             xr_ensure(xr, rb + blk + TE);
             const float4 *xq = xr_at(xr, rb + blk);
-            unsigned pm = 0;
+            if (blk - mbase > 32 - TE) {                  // the mask window is full: queue it
+                if (__any_sync(0xFFFFFFFFu, pmask != 0))
+                    qn = xq_push<TE, LT>(pmask, mbase, (unsigned)bidx, ncell, (unsigned)srow, rl, S0, rs, kb, idx0, q4,
+                                         q1, qn, CELL, acc_s, filt_s, gfr);
+                pmask = 0;
+                mbase = blk;
+            }
 #pragma unroll
             for (int I = 0; I < TE; ++I) {
                 fast_step<TE, LT>(xq[I], fst, I, TA, TB, TS, TC, mn);
                 fst += LT ? 3.0f : 4.0f;
-                pm |= (mn[I] <= fr[blk + I]) ? (1u << I) : 0u;
+                pmask |= (mn[I] <= fr[blk + I]) ? (1u << (blk + I - mbase)) : 0u;
             }
 #ifdef OOB_DBG_FILTER
             for (int I = 0; I < TE; ++I)
-                if (!((pm >> I) & 1))
+                if (!((pmask >> (blk + I - mbase)) & 1))
                     dbg_check<TE, LT>(CELL + bidx, ncell, CELL + srow, rl, blk + I, S0, rs, kb, acc_s, idx0 + blk + I,
                                       mn[I], fr[blk + I], TA, TB, TS, TC, xr, rb);
 #endif
-            if (__any_sync(0xFFFFFFFFu, pm != 0))
-                xq_push<TE, LT>(pm, blk, bidx, ncell, srow, rl, S0, rs, kb, idx0, TA, TB, TS, TC, xr, rb, xq_buf, qn,
-                                CELL, acc_s, filt_s, gfr);
         }
         // tail block (rl % TE steps) and the pending outputs E' = rl .. rl + TE - 2
+        if (__any_sync(0xFFFFFFFFu, pmask != 0))
+            qn = xq_push<TE, LT>(pmask, mbase, (unsigned)bidx, ncell, (unsigned)srow, rl, S0, rs, kb, idx0, q4, q1, qn,
+                                 CELL, acc_s, filt_s, gfr);
         {
             xr_ensure(xr, rb + blk + TE);
             const float4 *xq = xr_at(xr, rb + blk);
@@ -520,19 +527,24 @@ __device__ __forceinline__ void run_rows(XRing &xr, int64_t sidx, int M, int ls,
                     pm |= (mn[I] <= fr[blk + I]) ? (1u << I) : 0u;
                 }
             }
-            // slot sl holds E' = rl + ((sl - rl) mod TE) for the pending outputs
+            // pending outputs E' = rl + d (d = 0..TE-2) live in slot (rl + d) mod TE: one
+            // unrolled case per rl mod TE keeps the slot indices static
+            const int r0 = rl - blk;                      // = rl mod TE
 #pragma unroll
-            for (int sl = 0; sl < TE; ++sl) {
-                const int Ep = rl + (((sl - rl) % TE) + TE) % TE;
-                if (Ep <= rl + TE - 2 && mn[sl] <= fr[Ep]) pm |= 1u << (Ep - blk);
+            for (int r = 0; r < TE; ++r) {
+                if (r == r0) {
+#pragma unroll
+                    for (int d = 0; d <= TE - 2; ++d)
+                        if (mn[(r + d) % TE] <= fr[rl + d]) pm |= 1u << (r + d);
+                }
             }
             if (__any_sync(0xFFFFFFFFu, pm != 0))
-                xq_push<TE, LT>(pm, blk, bidx, ncell, srow, rl, S0, rs, kb, idx0, TA, TB, TS, TC, xr, rb, xq_buf, qn,
-                                CELL, acc_s, filt_s, gfr);
+                qn = xq_push<TE, LT>(pm, blk, (unsigned)bidx, ncell, (unsigned)srow, rl, S0, rs, kb, idx0, q4, q1, qn,
+                                     CELL, acc_s, filt_s, gfr);
         }
         rb += rl;
     }
-    if (qn) xq_flush(xq_buf, qn, CELL, acc_s, filt_s, gfr);
+    if (qn) xq_flush<TE>(q4, q1, qn, CELL, acc_s, filt_s, gfr);
     asm volatile("cp.async.wait_group 0;" ::: "memory");   // no copy of this chunk outlives the unit
     __syncwarp();
 }
@@ -844,7 +856,7 @@ __global__ void __launch_bounds__(256) k_fin(DevGeom g, FinArgs f) {
 }
 
 template <int TE>
-__global__ void __launch_bounds__(NTW, 2) k_wave_w(DevGeom g, WaveW w) {
+__global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, WaveW w) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_last;
     if ((int)blockIdx.x >= w.nbmain) {        // next wave's seeds and in-node cells
@@ -965,15 +977,16 @@ __global__ void __launch_bounds__(NTW, 2) k_wave_w(DevGeom g, WaveW w) {
         }
         const int64_t sidx = pc + sbase[ls] + (int64_t)us * scells[ls] + c_ipart(M, ls) + c_woff(M, ls, r_lo);
         unsigned char *wsm = reinterpret_cast<unsigned char *>(rings) + (size_t)(tid >> 5) * (XR_BYTES + XQ_BYTES);
-        uint4 *xq_buf = reinterpret_cast<uint4 *>(wsm + XR_BYTES);   // this warp's candidate queue
+        uint4 *q4 = reinterpret_cast<uint4 *>(wsm + XR_BYTES);         // this warp's candidate queue
+        unsigned *q1 = reinterpret_cast<unsigned *>(q4 + XQ_CAP);
         XRing xr;                                            // rows r_lo.. are contiguous
         xr_start(xr, reinterpret_cast<float4 *>(wsm), g.SH + sidx, lane);
         if (ltiled)
             run_rows<TE, true>(xr, sidx, M, ls, r_lo, r_hi, TA, TB, TS, TC, bidx, ncell, rowB, e0, l1, L, outOff, nout,
-                               acc_s, filt_s, gfilt, xq_buf, g.CELL);
+                               acc_s, filt_s, gfilt, q4, q1, g.CELL);
         else
             run_rows<TE, false>(xr, sidx, M, ls, r_lo, r_hi, TA, TB, TS, TC, bidx, ncell, rowB, e0, l1, L, outOff,
-                                nout, acc_s, filt_s, gfilt, xq_buf, g.CELL);
+                                nout, acc_s, filt_s, gfilt, q4, q1, g.CELL);
     }
     __syncthreads();
     // merge into the range's global accumulator (L2-coherent loads; a stale value is an
