@@ -234,6 +234,7 @@ struct oob_dp_plan {
     int fuse_fin = 1;                    // OOB_DP_FUSE=0: separate k_fin launch per wave
     int perm_order = 0;                  // OOB_DP_PERM=1: pseudo-random unit order
     int rev_lanes = 0;                   // OOB_DP_REV=1: reversed lane <-> tile order
+    int chunk_max = 192;                 // OOB_DP_CHMAX: streamed cells per unit (upper bound)
     size_t geom_bytes = 0, ws_bytes = 0, tpl_bytes = 0;
     std::vector<unsigned char> geom_blob;   // host image of the geometry region
     size_t off_cells = 0, off_base = 0, off_off = 0, off_tiles = 0, off_tile_off = 0, off_tile_cnt = 0,
@@ -387,6 +388,7 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     if (const char *fu = std::getenv("OOB_DP_FUSE")) pl->fuse_fin = std::atoi(fu) != 0;
     if (const char *po = std::getenv("OOB_DP_PERM")) pl->perm_order = std::atoi(po) != 0;
     if (const char *rv = std::getenv("OOB_DP_REV")) pl->rev_lanes = std::atoi(rv) != 0;
+    if (const char *cm = std::getenv("OOB_DP_CHMAX")) pl->chunk_max = std::max(12, std::atoi(cm));
     for (int ci = 0; ci < NWCFG; ++ci) build_tiles(pl, WCFGS[ci].te);
     pl->stream_steps.assign(L + 1, 0.0);
     for (int ls = 1; ls <= L; ++ls) {
@@ -406,7 +408,7 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
             // resident CTAs per SM: launch bounds (registers), then shared memory
             int per_sm = CTAS_PER_SM;
             for (int pass = 0; pass < 2; ++pass) {
-                for (int CH = 96;; CH /= 2) {
+                for (int CH = pl->chunk_max;; CH /= 2) {
                     build_wave(pl, l, ci, per_sm * 148, wh, CH);
                     if (CH <= 12 || ((int64_t)wh.nunits * num_profiles * (L - l + 1) >= 4LL * per_sm * 148 * (NTW / 32) &&
                                      wh.nunits >= pl->units_per_cta * wh.cpr))

@@ -41,6 +41,7 @@ constexpr int NTW = 256;                                          // threads per
 constexpr int WAVE_CTAS_PER_SM = 2;                               // register budget: 128 per thread
 constexpr unsigned long long ACC_EMPTY = 0x7FEFFFFFFFFFFFFFull;   // DBL_MAX: "no split yet"
 constexpr double D_INF = __builtin_huge_val();
+constexpr unsigned long long ACC_DIRTY = 1ull << 32;   // accumulator key word: improved by this CTA
 
 // Finalize / in-node work of one wavefront (k_fin, or k_wave_w's extra blocks and last CTAs).
 struct FinArgs {
@@ -329,7 +330,7 @@ __device__ __noinline__ void xq_flush(const uint4 *q4, const unsigned *q1, int c
 #endif
             while (lex_less(bb, bk, cx, (uint32_t)cy)) {
                 unsigned long long ox, oy;
-                cas128_shared(addr, ox, oy, cx, cy, bb, (unsigned long long)bk);
+                cas128_shared(addr, ox, oy, cx, cy, bb, (unsigned long long)bk | ACC_DIRTY);
                 if (ox == cx && oy == cy) {
 #ifdef OOB_FLUSH_STATS
                     if (g_flush_stats_on) atomicAdd(&g_flush_stats[1], 1ull);
@@ -1000,6 +1001,7 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
         for (int j = 0; j < MB; ++j) {
             const int i = i0 + j * NTW;
             a[j] = i < nout ? acc[i] : make_ulonglong2(ACC_EMPTY, 0ull);
+            if (!(a[j].y & ACC_DIRTY)) a[j] = make_ulonglong2(ACC_EMPTY, 0ull);   // only this CTA's improvements
             cur[j] = a[j].x < ACC_EMPTY ? __ldcg(ga + i) : make_ulonglong2(0ull, 0ull);
         }
 #pragma unroll

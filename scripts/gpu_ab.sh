@@ -1,10 +1,9 @@
 #!/bin/bash
-# A/B timing (scripts/dp_time.py) of alternative builds build/lib_<v>.so against the in-tree library.
+# A/B of env settings on the cfg4 bench: VARIANTS="A=1 B=2;C=3" (';'-separated sets)
 mkdir -p gpurun_out
-cp paper_2309_08125_b200/liboobleck_plan.so /tmp/lib_main.so
-for v in ${VARIANTS}; do
-  cp build/lib_$v.so paper_2309_08125_b200/liboobleck_plan.so
-  echo -n "$v: "; timeout 300 python scripts/dp_time.py ${WL:-cfg4} 5 2>&1 | tail -1
-  cp /tmp/lib_main.so paper_2309_08125_b200/liboobleck_plan.so
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -20 gpurun_out/build.log; exit 1; }
+IFS=';' read -ra VS <<< "${VARIANTS:-}"
+for v in "" "${VS[@]}"; do
+  env $v timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline ${BENCHARGS} > gpurun_out/ab.log 2>&1
+  tail -1 gpurun_out/ab.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('[$v]', 'ms', round(d['ms_per_step'],3), 'frac', round(d['roofline']['frac'],4))" 2>&1 | tail -1
 done
-echo -n "main: "; timeout 300 python scripts/dp_time.py ${WL:-cfg4} 5 2>&1 | tail -1
