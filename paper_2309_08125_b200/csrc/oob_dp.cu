@@ -229,7 +229,7 @@ struct oob_dp_plan {
     int auto_cfgs = 2;                   // OOB_DP_AUTOCFGS: WCFGS entries the wave model chooses from
     int seed_pass = 0;                   // OOB_DP_SEED=1 enables the seeding pass
     int seed_init = 1;                   // OOB_DP_SEEDINIT=0: no proportional-split seeds
-    double seed_spo = 1000.0;            // OOB_DP_SEEDSPO: seed waves with >= this many splits per W output
+    double seed_spo = 0.0;               // OOB_DP_SEEDSPO: seed waves with >= this many splits per W output
     int small_pairs = 1;                 // OOB_DP_SMALLPAIRS: layer splits per thread of a small cell
     int fuse_fin = 1;                    // OOB_DP_FUSE=0: separate k_fin launch per wave
     int perm_order = 0;                  // OOB_DP_PERM=1: pseudo-random unit order
