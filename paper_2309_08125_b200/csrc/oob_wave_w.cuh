@@ -54,6 +54,7 @@ struct FinArgs {
     int lseed, nout_s, nbseed;     // seeds of wave lseed (0: none): W outputs per range, blocks
     ulonglong2 *GSEED;             // accumulator of wave lseed (the other parity buffer)
     unsigned *GFW, *GFS;           // global filters (binary32 bits of F(min)) of waves lw / lseed
+    int seedw;                     // warm-start seeds: (j, s) neighbourhood radius
     int ls, nsmall;                // small cells of wave ls (ls = 0: none); cells per range
     int tpc;                       // threads per small cell
 };
@@ -84,6 +85,7 @@ struct WaveW {
     int nbmain;
     int fin_inline;
     int *rdone;                // [P][nranges] CTAs of the range that have merged
+    int *rclaim;               // [P][nranges] finalize shares claimed
     FinArgs fa, fw;
 };
 
@@ -326,6 +328,7 @@ __device__ __noinline__ void xq_flush(const uint4 *q4, const unsigned *q1, int c
                 atomicAdd(&g_flush_stats[0], 1ull);
                 if (bb == cx) atomicAdd(&g_flush_stats[2], 1ull);
                 else if (bb > cx) atomicAdd(&g_flush_stats[3], 1ull);
+                if (bb == cx && bk == (uint32_t)cy) atomicAdd(&g_flush_stats[1], 1ull << 32);   // same split
             }
 #endif
             while (lex_less(bb, bk, cx, (uint32_t)cy)) {
@@ -602,18 +605,20 @@ __device__ __forceinline__ void fin_w_one(const DevGeom &g, const FinArgs &f, in
 // last CTA of the range): fin_w_one's steps in three phases over FB outputs per thread
 // (accumulator loads; child loads; recompute + store) so their memory latencies overlap.
 template <int NT>
-__device__ __forceinline__ void fin_w_range(const DevGeom &g, const FinArgs &f, int pr, int tid) {
+__device__ __forceinline__ void fin_w_range(const DevGeom &g, const FinArgs &f, int pr, int tid, int part = 0,
+                                            int nparts = 1) {
     constexpr int FB = 4;
     const int l = f.lw, nout = f.nout_w, M = g.M;
     const int u = pr % f.nranges_w, p = pr / f.nranges_w;
     const int64_t pc = (int64_t)p * g.C;
     const int Ql = (l == g.L) ? g.n_hi : max(1, g.n_hi - 1);
-    for (int i0 = tid; i0 < nout; i0 += FB * NT) {
+    const int stride = NT * nparts;               // share `part`: outputs part NT + tid + k stride
+    for (int i0 = part * NT + tid; i0 < nout; i0 += FB * stride) {
         int q[FB], Sp[FB];
         ulonglong2 a[FB];
 #pragma unroll
         for (int j = 0; j < FB; ++j) {
-            const int i = i0 + j * NT;
+            const int i = i0 + j * stride;
             q[j] = 0;
             Sp[j] = 0;
             a[j] = make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull);
@@ -743,14 +748,18 @@ __device__ __forceinline__ void fin_seed_one(const DevGeom &g, const FinArgs &f,
                 const uint32_t arg = g.ARG[pc + g.base[lp] + (int64_t)up * g.cells[lp] + c_ipart(M, lp) +
                                            c_woff(M, lp, q) + (Sp - q)];
                 if (arg >= 0xFFFFFFFEu) continue;
-                const int l1p = (int)(arg & 1023u) + 1 + 2 * side, j = (int)((arg >> 10) & 1023u) + 1;
-                const int s = (int)(arg >> 20);
-                const int jr = q - j, sr = Sp - s;
+                const int l1p = (int)(arg & 1023u) + 1 + 2 * side, j0 = (int)((arg >> 10) & 1023u) + 1;
+                const int s0 = (int)(arg >> 20);
+                const int nw = 2 * f.seedw + 1;
 #pragma unroll 1
-                for (int d = 0; d < 3; ++d) {
+                for (int dd = 0; dd < 3 * nw * nw; ++dd) {   // l1 shifts x (j, s) neighbourhood
+                    const int d = dd % 3, j = j0 + (dd / 3) % nw - f.seedw, s = s0 + dd / (3 * nw) - f.seedw;
+                    const int jr = q - j, sr = Sp - s;
                     const int l1 = l1p + d - side;   // shifts 0..2 (left range) / 1..3 - 1 (right)
                     const int l2 = l - l1;
-                    if (l1 < 2 || l2 < 2 || s > l1 || sr > l2 || j > l1 || jr > l2 || jr < 1) continue;
+                    if (l1 < 2 || l2 < 2 || s > l1 || sr > l2 || j < 1 || j > l1 || jr > l2 || jr < 1 || s < 1 ||
+                        j > Qp || jr > Qp)
+                        continue;
                     const Cell4 *lc = g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + c_ipart(M, l1) +
                                       c_woff(M, l1, j) + (s - j);
                     const Cell4 *rc = g.CELL + pc + g.base[l2] + (int64_t)(u + l1) * g.cells[l2] +
@@ -1016,14 +1025,34 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
             }
         }
     }
-    if (w.fin_inline) {                        // the range's last CTA finalizes its W outputs
+    if (w.fin_inline) {
+        // The range's W outputs are final once all its cpr CTAs have merged.  The host sizes
+        // the main grid to the resident CTA slots whenever cpr > 1 (the extra blocks come
+        // after it), so the range's CTAs are co-resident: each waits for the others, then
+        // they claim the cpr shares of the finalize from a counter.  The wait is bounded: on
+        // timeout (a GPU shared with other work) a CTA just exits; the last CTA to merge never
+        // waits and claims every share left, so each share is finalized exactly once.
         __threadfence();
         __syncthreads();
-        if (tid == 0) s_last = atomicAdd(w.rdone + pr, 1) == w.cpr - 1;
+        if (tid == 0) {
+            int ok = atomicAdd(w.rdone + pr, 1) + 1 == w.cpr;
+            for (int it = 0; !ok && it < (1 << 22); ++it) {
+                __nanosleep(128);
+                ok = *(volatile int *)(w.rdone + pr) >= w.cpr;
+            }
+            s_last = ok;
+        }
         __syncthreads();
         if (s_last) {
             __threadfence();
-            fin_w_range<NTW>(g, w.fw, pr, tid);
+            for (;;) {
+                __syncthreads();
+                if (tid == 0) s_last = atomicAdd(w.rclaim + pr, 1);
+                __syncthreads();
+                const int c = s_last;
+                if (c >= w.cpr) break;
+                fin_w_range<NTW>(g, w.fw, pr, tid, c, w.cpr);
+            }
         }
     }
 }

@@ -28,5 +28,5 @@ f(1, None)
 plan.run(fwd.data_ptr(), bwd.data_ptr(), ws.data_ptr(), ws.numel(), packed.data_ptr(), torch.cuda.current_stream().cuda_stream)
 torch.cuda.synchronize()
 f(0, out)
-print(f"{key}: filter passes {out[0]}, CAS successes {out[1]}, exact ties {out[2]}, exact worse {out[3]}, "
+print(f"{key}: filter passes {out[0]}, CAS successes {out[1] & 0xFFFFFFFF}, exact ties {out[2]} (same split {out[1] >> 32}), exact worse {out[3]}, "
       f"feasible splits {info.splits_per_profile}")
