@@ -238,7 +238,7 @@ struct oob_dp_plan {
     int seed_w = 0;                      // OOB_DP_SEEDW: warm-start seed (j, s) neighbourhood radius
     size_t geom_bytes = 0, ws_bytes = 0, tpl_bytes = 0;
     std::vector<unsigned char> geom_blob;   // host image of the geometry region
-    size_t off_cells = 0, off_base = 0, off_off = 0, off_tiles = 0, off_tile_off = 0, off_tile_cnt = 0,
+    size_t off_cells = 0, off_base = 0, off_off = 0, off_wofs = 0, off_tiles = 0, off_tile_off = 0, off_tile_cnt = 0,
            off_items = 0;
     size_t off_CELL = 0, off_SH = 0, off_ARG = 0, off_STK = 0, off_GACC = 0, off_GFILT = 0, off_CTR = 0;
     int64_t gacc_n = 0;
@@ -474,6 +474,7 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     pl->off_cells = o; o = align_up(o + sizeof(int32_t) * (L + 1), 256);
     pl->off_base = o;  o = align_up(o + sizeof(int64_t) * (L + 2), 256);
     pl->off_off = o;   o = align_up(o + sizeof(int32_t) * (size_t)(L + 1) * g.A, 256);
+    pl->off_wofs = o;  o = align_up(o + sizeof(int32_t) * (size_t)(L + 1) * (L + 2), 256);
     pl->off_tiles = o; o = align_up(o + sizeof(int32_t) * pl->tiles.size(), 256);
     pl->off_tile_off = o; o = align_up(o + sizeof(int32_t) * (L + 1) * NWCFG, 256);
     pl->off_tile_cnt = o; o = align_up(o + sizeof(int32_t) * (L + 1) * NWCFG, 256);
@@ -496,6 +497,19 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     std::memcpy(b + pl->off_cells, g.cells.data(), sizeof(int32_t) * (L + 1));
     std::memcpy(b + pl->off_base, g.base.data(), sizeof(int64_t) * (L + 2));
     std::memcpy(b + pl->off_off, g.off.data(), sizeof(int32_t) * (size_t)(L + 1) * g.A);
+    {   // W row offsets per slab length (I part + rows 1..q-1), DevGeom::wofs
+        int32_t *wo = reinterpret_cast<int32_t *>(b + pl->off_wofs);
+        for (int l = 0; l <= L; ++l) {
+            const int ip = l >= M - 1 ? (M - 1) * M / 2 : l * (l + 1) / 2 + (M - 1 - l) * l;   // I(1..M-1) cells
+            int acc = ip;
+            wo[(size_t)l * (L + 2)] = ip;
+            for (int q = 1; q <= L + 1; ++q) {
+                wo[(size_t)l * (L + 2) + q] = acc;
+                const int hi = std::min(l, M * q);
+                acc += hi >= q ? hi - q + 1 : 0;
+            }
+        }
+    }
     if (!pl->tiles.empty()) std::memcpy(b + pl->off_tiles, pl->tiles.data(), sizeof(int32_t) * pl->tiles.size());
     for (int ti = 0; ti < NWCFG; ++ti) {
         std::memcpy(b + pl->off_tile_off + sizeof(int32_t) * (L + 1) * ti, pl->tab[ti].off.data(), sizeof(int32_t) * (L + 1));
@@ -688,6 +702,7 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
     dg.cells = (const int32_t *)(ws + pl->off_cells);
     dg.base = (const int64_t *)(ws + pl->off_base);
     dg.off = (const int32_t *)(ws + pl->off_off);
+    dg.wofs = (const int32_t *)(ws + pl->off_wofs);
     dg.CELL = (Cell4 *)(ws + pl->off_CELL);
     dg.SH = (float4 *)(ws + pl->off_SH);
     dg.ARG = (uint32_t *)(ws + pl->off_ARG);

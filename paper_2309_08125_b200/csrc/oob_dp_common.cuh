@@ -27,6 +27,7 @@ struct DevGeom {
     const int32_t *cells;     // [L+1]
     const int64_t *base;      // [L+2]
     const int32_t *off;       // [(L+1)*A]
+    const int32_t *wofs;      // [(L+1)*(L+2)]: offset of W row q (1..l+1) in a slab of length l (incl. I part)
     Cell4 *CELL;              // [P*C]
     float4 *SH;               // [P*C] shadow lower bounds (filter only)
     uint32_t *ARG;            // [P*C]
@@ -34,6 +35,9 @@ struct DevGeom {
 };
 
 __device__ __forceinline__ bool d_is_whole(const DevGeom &g, int a) { return a >= g.M - 1; }
+// slab offset of W row q in a slab of length l (rows are contiguous: row q has
+// d_wofs(l, q+1) - d_wofs(l, q) cells)
+__device__ __forceinline__ int d_wofs(const DevGeom &g, int l, int q) { return __ldg(g.wofs + l * (g.L + 2) + q); }
 __device__ __forceinline__ int d_alloc_n(const DevGeom &g, int a) {
     return d_is_whole(g, a) ? a - (g.M - 1) + 1 : a + 1;
 }

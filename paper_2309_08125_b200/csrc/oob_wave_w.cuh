@@ -463,7 +463,7 @@ __device__ __forceinline__ void fast_step(const float4 x, float fst, int I, cons
 // blocks of TE steps (no guards) and a guarded tail; the outputs whose bounds pass the
 // filter are collected per block (bit mask) and re-evaluated exactly.
 template <int TE, bool LT>
-__device__ __forceinline__ void run_rows(XRing &xr, int64_t sidx, int M, int ls, int r_lo, int r_hi,
+__device__ __forceinline__ void run_rows(XRing &xr, int64_t sidx, const int32_t *wls, int r_lo, int r_hi,
                                          const float (&TA)[TE], const float (&TB)[TE], const float (&TS)[TE],
                                          const float (&TC)[TE], int64_t bidx, int ncell, int rowB, int e0,
                                          int l1, int L, const int *outOff, int nout, unsigned acc_s,
@@ -475,7 +475,7 @@ __device__ __forceinline__ void run_rows(XRing &xr, int64_t sidx, int M, int ls,
     const float *filt = reinterpret_cast<const float *>(__cvta_shared_to_generic(filt_s));
     int rb = 0;                                           // chunk cell of the row's first cell
     for (int rs = r_lo; rs < r_hi; ++rs) {
-        const int rl = c_wlen(M, ls, rs);
+        const int rl = __ldg(wls + rs + 1) - __ldg(wls + rs);
         const int q = rowB + rs;
         const int ob = outOff[min(q, L + 1)];
         const int idx0 = (ob == nout) ? nout : ob + e0;  // accumulator entry of E' = 0
@@ -570,9 +570,9 @@ __device__ __forceinline__ void fin_w_one(const DevGeom &g, const FinArgs &f, in
     int lo = 1, hi = min(Ql, l);
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (c_woff(g.M, l, mid) <= i) lo = mid; else hi = mid - 1;
+        if (d_wofs(g, l, mid) - d_wofs(g, l, 1) <= i) lo = mid; else hi = mid - 1;
     }
-    const int q = lo, Sp = q + (i - c_woff(g.M, l, q));
+    const int q = lo, Sp = q + (i - (d_wofs(g, l, q) - d_wofs(g, l, 1)));
     if (q < 2) return;        // W(1) cell (computed with the small cells)
     ulonglong2 *ga = f.GACC + t;
     ulonglong2 a = __ldcg(ga);
@@ -626,10 +626,10 @@ __device__ __forceinline__ void fin_w_range(const DevGeom &g, const FinArgs &f, 
             int lo = 1, hi = min(Ql, l);
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
-                if (c_woff(M, l, mid) <= i) lo = mid; else hi = mid - 1;
+                if (d_wofs(g, l, mid) - d_wofs(g, l, 1) <= i) lo = mid; else hi = mid - 1;
             }
             q[j] = lo;
-            Sp[j] = lo + (i - c_woff(M, l, lo));
+            Sp[j] = lo + (i - (d_wofs(g, l, lo) - d_wofs(g, l, 1)));
             if (lo < 2) continue;
             ulonglong2 *ga = f.GACC + (int64_t)pr * nout + i;
             a[j] = __ldcg(ga);
@@ -658,10 +658,9 @@ __device__ __forceinline__ void fin_w_range(const DevGeom &g, const FinArgs &f, 
                 continue;
             }
             // children W(jj) of (u, u+l1) and W(jr) of (u+l1, u+l)
-            Lc[j] = d_load(g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + c_ipart(M, l1) + c_woff(M, l1, jj) +
+            Lc[j] = d_load(g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + d_wofs(g, l1, jj) +
                            (s - jj));
-            Rc[j] = d_load(g.CELL + pc + g.base[l2] + (int64_t)(u + l1) * g.cells[l2] + c_ipart(M, l2) +
-                           c_woff(M, l2, jr) + (sr - jr));
+            Rc[j] = d_load(g.CELL + pc + g.base[l2] + (int64_t)(u + l1) * g.cells[l2] + d_wofs(g, l2, jr) + (sr - jr));
             l1v[j] = l1;
             sv[j] = s | (jj << 16);
             ok[j] = 1;
@@ -698,9 +697,9 @@ __device__ __forceinline__ void fin_seed_one(const DevGeom &g, const FinArgs &f,
     int lo = 1, hi = min(Ql, l);
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (c_woff(M, l, mid) <= i) lo = mid; else hi = mid - 1;
+        if (d_wofs(g, l, mid) - d_wofs(g, l, 1) <= i) lo = mid; else hi = mid - 1;
     }
-    const int q = lo, Sp = q + (i - c_woff(M, l, q));
+    const int q = lo, Sp = q + (i - (d_wofs(g, l, q) - d_wofs(g, l, 1)));
     unsigned long long bb = ACC_EMPTY;
     uint32_t bk = 0xFFFFFFFFu;
     if (q >= 2) {
@@ -720,10 +719,9 @@ __device__ __forceinline__ void fin_seed_one(const DevGeom &g, const FinArgs &f,
                     const int l1 = (l * s) / Sp + kk - 1;
                     const int l2 = l - l1;
                     if (l1 < 2 || l2 < 2 || s > l1 || sr > l2 || j > l1 || jr > l2) continue;
-                    const Cell4 *lc = g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + c_ipart(M, l1) +
-                                      c_woff(M, l1, j) + (s - j);
+                    const Cell4 *lc = g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + d_wofs(g, l1, j) + (s - j);
                     const Cell4 *rc = g.CELL + pc + g.base[l2] + (int64_t)(u + l1) * g.cells[l2] +
-                                      c_ipart(M, l2) + c_woff(M, l2, jr) + (sr - jr);
+                                      d_wofs(g, l2, jr) + (sr - jr);
                     const Cell4 L = d_load(lc), R = d_load(rc);
                     const double cL = __dadd_rn(L.C1, (double)(3 * sr));
                     const double cR = __dadd_rn(R.C1, (double)(4 * s));
@@ -745,8 +743,7 @@ __device__ __forceinline__ void fin_seed_one(const DevGeom &g, const FinArgs &f,
 #pragma unroll 1
             for (int side = 0; side < 2; ++side) {
                 const int up = u + 2 * side;
-                const uint32_t arg = g.ARG[pc + g.base[lp] + (int64_t)up * g.cells[lp] + c_ipart(M, lp) +
-                                           c_woff(M, lp, q) + (Sp - q)];
+                const uint32_t arg = g.ARG[pc + g.base[lp] + (int64_t)up * g.cells[lp] + d_wofs(g, lp, q) + (Sp - q)];
                 if (arg >= 0xFFFFFFFEu) continue;
                 const int l1p = (int)(arg & 1023u) + 1 + 2 * side, j0 = (int)((arg >> 10) & 1023u) + 1;
                 const int s0 = (int)(arg >> 20);
@@ -760,10 +757,9 @@ __device__ __forceinline__ void fin_seed_one(const DevGeom &g, const FinArgs &f,
                     if (l1 < 2 || l2 < 2 || s > l1 || sr > l2 || j < 1 || j > l1 || jr > l2 || jr < 1 || s < 1 ||
                         j > Qp || jr > Qp)
                         continue;
-                    const Cell4 *lc = g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + c_ipart(M, l1) +
-                                      c_woff(M, l1, j) + (s - j);
+                    const Cell4 *lc = g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + d_wofs(g, l1, j) + (s - j);
                     const Cell4 *rc = g.CELL + pc + g.base[l2] + (int64_t)(u + l1) * g.cells[l2] +
-                                      c_ipart(M, l2) + c_woff(M, l2, jr) + (sr - jr);
+                                      d_wofs(g, l2, jr) + (sr - jr);
                     if (s < j || sr < jr || s > M * j || sr > M * jr) continue;
                     const Cell4 Lc = d_load(lc), Rc = d_load(rc);
                     const double cL = __dadd_rn(Lc.C1, (double)(3 * sr));
@@ -954,12 +950,12 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
         const int32_t code = has ? w.tiles[w.tile_off[lb] + ti] : 0;
         const int rowB = has ? (code >> 16) : 1;
         const int e0 = has ? (code & 0xFFFF) : 0;
-        const int lenB = has ? c_wlen(M, lb, rowB) : 0;
+        const int wb0 = has ? d_wofs(g, lb, rowB) : 0;
+        const int lenB = has ? d_wofs(g, lb, rowB + 1) - wb0 : 0;
         const int ncell = max(0, min(TE, lenB - e0));             // valid cells of the tile
         // register tile: shadow lower bounds of TE big-side cells (+inf beyond the row: every
         // bound of a sentinel is +inf and never passes)
-        const int64_t bidx = pc + sbase[lb] + (int64_t)ub * scells[lb] + c_ipart(M, lb) +
-                             (has ? c_woff(M, lb, rowB) : 0) + e0;
+        const int64_t bidx = pc + sbase[lb] + (int64_t)ub * scells[lb] + (has ? wb0 : d_wofs(g, lb, 1)) + e0;
         float TA[TE], TB[TE], TS[TE], TC[TE];
 #pragma unroll
         for (int t = 0; t < TE; ++t) {
@@ -985,17 +981,17 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
                     if (gv[j] < filt[i0 + 32 * j]) atomicMin(filt + i0 + 32 * j, gv[j]);
             }
         }
-        const int64_t sidx = pc + sbase[ls] + (int64_t)us * scells[ls] + c_ipart(M, ls) + c_woff(M, ls, r_lo);
+        const int64_t sidx = pc + sbase[ls] + (int64_t)us * scells[ls] + d_wofs(g, ls, r_lo);
         unsigned char *wsm = reinterpret_cast<unsigned char *>(rings) + (size_t)(tid >> 5) * (XR_BYTES + XQ_BYTES);
         uint4 *q4 = reinterpret_cast<uint4 *>(wsm + XR_BYTES);         // this warp's candidate queue
         unsigned *q1 = reinterpret_cast<unsigned *>(q4 + XQ_CAP);
         XRing xr;                                            // rows r_lo.. are contiguous
         xr_start(xr, reinterpret_cast<float4 *>(wsm), g.SH + sidx, lane);
         if (ltiled)
-            run_rows<TE, true>(xr, sidx, M, ls, r_lo, r_hi, TA, TB, TS, TC, bidx, ncell, rowB, e0, l1, L, outOff, nout,
+            run_rows<TE, true>(xr, sidx, g.wofs + ls * (L + 2), r_lo, r_hi, TA, TB, TS, TC, bidx, ncell, rowB, e0, l1, L, outOff, nout,
                                acc_s, filt_s, gfilt, q4, q1, g.CELL);
         else
-            run_rows<TE, false>(xr, sidx, M, ls, r_lo, r_hi, TA, TB, TS, TC, bidx, ncell, rowB, e0, l1, L, outOff,
+            run_rows<TE, false>(xr, sidx, g.wofs + ls * (L + 2), r_lo, r_hi, TA, TB, TS, TC, bidx, ncell, rowB, e0, l1, L, outOff,
                                 nout, acc_s, filt_s, gfilt, q4, q1, g.CELL);
     }
     __syncthreads();
