@@ -32,6 +32,7 @@ import numpy as np  # noqa: E402
 from workloads import CONFIGS, config_profiles  # noqa: E402
 
 FP64_PER_SPLIT = 7          # algorithmic FP64 instructions per split
+SCREEN_INSTR_PER_SPLIT = 6  # k_wave_w's binary32 screen: FFMA, FADD, FADD, FSETP, FFMA, FMNMX
 SMS = 148
 FP64_LANES_PER_SM = 64      # B200 FP64 (non-tensor) FMA lanes per SM per clock
 METRIC = "template-DP cells/s"
@@ -274,6 +275,16 @@ def main():
                 "kernel": "k_wave_w (W-cell wavefront DP)", "kernel_ms_per_step": kern_ms_per_step,
                 "kernel_share_of_step": kern_ms_per_step / (total_ms / args.steps) if world == 1 else None,
                 "peak_basis": f"148 SMs x 64 FP64 lanes x {sm_max:.0f} MHz (max clock)",
+                "work_basis": "7 algorithmic FP64 instructions per feasible split (the method's binary64 "
+                              "Eq.1-3 combine); the kernel screens splits with a binary32 round-down lower "
+                              "bound (6 FMA/ALU instructions) and re-evaluates candidates in binary64",
+                # the kernel's own limit: instruction issue (1 warp-instruction per scheduler per
+                # clock) at the 6 instructions per split of its binary32 screen
+                "issue_roofline": {"achieved_splits_per_s": rank_splits / (kern_ms_per_step / 1e3),
+                                   "peak_splits_per_s": SMS * 4 * 32 * sm_max * 1e6 / SCREEN_INSTR_PER_SPLIT,
+                                   "frac": rank_splits / (kern_ms_per_step / 1e3) /
+                                   (SMS * 4 * 32 * sm_max * 1e6 / SCREEN_INSTR_PER_SPLIT),
+                                   "basis": "148 SMs x 4 schedulers x 32 lanes x max clock / 6 instructions"},
                 "frac_at_observed_clock": (achieved / (SMS * FP64_LANES_PER_SM * clocks["sm_mhz"] * 1e6 / 1e12))
                 if clocks.get("sm_mhz") else None}
 

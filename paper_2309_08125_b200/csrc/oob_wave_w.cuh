@@ -502,12 +502,15 @@ __device__ __forceinline__ void run_rows(XRing &xr, int64_t sidx, const int32_t 
                 pmask = 0;
                 mbase = blk;
             }
+            unsigned pm4 = 0;                             // this block's passes (static bits)
+            const float *fb = fr + blk;
 #pragma unroll
             for (int I = 0; I < TE; ++I) {
                 fast_step<TE, LT>(xq[I], fst, I, TA, TB, TS, TC, mn);
                 fst += LT ? 3.0f : 4.0f;
-                pmask |= (mn[I] <= fr[blk + I]) ? (1u << (blk + I - mbase)) : 0u;
+                pm4 |= (mn[I] <= fb[I]) ? (1u << I) : 0u;
             }
+            pmask |= pm4 << (blk - mbase);
 #ifdef OOB_DBG_FILTER
             for (int I = 0; I < TE; ++I)
                 if (!((pmask >> (blk + I - mbase)) & 1))
