@@ -718,17 +718,25 @@ __device__ __forceinline__ void fin_seed_one(const DevGeom &g, const FinArgs &f,
                 if (ss == 1 && s == (Sp * j) / q) continue;
                 const int sr = Sp - s;
                 if (s < j || sr < jr || s > M * j || sr > M * jr) continue;
+                Cell4 Lk[3], Rk[3];                         // the 3 l1 candidates' loads in flight together
+                bool okk[3];
+#pragma unroll
                 for (int kk = 0; kk < 3; ++kk) {
                     const int l1 = (l * s) / Sp + kk - 1;
                     const int l2 = l - l1;
-                    if (l1 < 2 || l2 < 2 || s > l1 || sr > l2 || j > l1 || jr > l2) continue;
-                    const Cell4 *lc = g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + d_wofs(g, l1, j) + (s - j);
-                    const Cell4 *rc = g.CELL + pc + g.base[l2] + (int64_t)(u + l1) * g.cells[l2] +
-                                      d_wofs(g, l2, jr) + (sr - jr);
-                    const Cell4 L = d_load(lc), R = d_load(rc);
-                    const double cL = __dadd_rn(L.C1, (double)(3 * sr));
-                    const double cR = __dadd_rn(R.C1, (double)(4 * s));
-                    const double tot = split_total(L.T1, L.T3, L.TS, cL, R.T1, R.T3, R.TS, cR);
+                    okk[kk] = !(l1 < 2 || l2 < 2 || s > l1 || sr > l2 || j > l1 || jr > l2);
+                    if (!okk[kk]) continue;
+                    Lk[kk] = d_load(g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + d_wofs(g, l1, j) + (s - j));
+                    Rk[kk] = d_load(g.CELL + pc + g.base[l2] + (int64_t)(u + l1) * g.cells[l2] + d_wofs(g, l2, jr) +
+                                    (sr - jr));
+                }
+#pragma unroll
+                for (int kk = 0; kk < 3; ++kk) {
+                    if (!okk[kk]) continue;
+                    const int l1 = (l * s) / Sp + kk - 1;
+                    const double cL = __dadd_rn(Lk[kk].C1, (double)(3 * sr));
+                    const double cR = __dadd_rn(Rk[kk].C1, (double)(4 * s));
+                    const double tot = split_total(Lk[kk].T1, Lk[kk].T3, Lk[kk].TS, cL, Rk[kk].T1, Rk[kk].T3, Rk[kk].TS, cR);
                     const unsigned long long tb = (unsigned long long)__double_as_longlong(tot);
                     const uint32_t key = ((uint32_t)l1 << 20) | ((uint32_t)j << 10) | (uint32_t)s;
                     if (lex_less(tb, key, bb, bk)) { bb = tb; bk = key; }
@@ -743,31 +751,37 @@ __device__ __forceinline__ void fin_seed_one(const DevGeom &g, const FinArgs &f,
         const int lp = l - 2;
         const int Qp = max(1, g.n_hi - 1);
         if (q <= Qp && q <= lp && Sp <= min(lp, M * q)) {
-#pragma unroll 1
+            uint32_t args[2];                               // both sides' argmins in flight together
+#pragma unroll
+            for (int side = 0; side < 2; ++side)
+                args[side] = g.ARG[pc + g.base[lp] + (int64_t)(u + 2 * side) * g.cells[lp] + d_wofs(g, lp, q) + (Sp - q)];
+#pragma unroll
             for (int side = 0; side < 2; ++side) {
-                const int up = u + 2 * side;
-                const uint32_t arg = g.ARG[pc + g.base[lp] + (int64_t)up * g.cells[lp] + d_wofs(g, lp, q) + (Sp - q)];
+                const uint32_t arg = args[side];
                 if (arg >= 0xFFFFFFFEu) continue;
-                const int l1p = (int)(arg & 1023u) + 1 + 2 * side, j0 = (int)((arg >> 10) & 1023u) + 1;
-                const int s0 = (int)(arg >> 20);
-                const int nw = 2 * f.seedw + 1;
-#pragma unroll 1
-                for (int dd = 0; dd < 3 * nw * nw; ++dd) {   // l1 shifts x (j, s) neighbourhood
-                    const int d = dd % 3, j = j0 + (dd / 3) % nw - f.seedw, s = s0 + dd / (3 * nw) - f.seedw;
-                    const int jr = q - j, sr = Sp - s;
+                const int l1p = (int)(arg & 1023u) + 1 + 2 * side, j = (int)((arg >> 10) & 1023u) + 1;
+                const int s = (int)(arg >> 20);
+                const int jr = q - j, sr = Sp - s;
+                Cell4 Lk[3], Rk[3];
+                bool okk[3];
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
                     const int l1 = l1p + d - side;   // shifts 0..2 (left range) / 1..3 - 1 (right)
                     const int l2 = l - l1;
-                    if (l1 < 2 || l2 < 2 || s > l1 || sr > l2 || j < 1 || j > l1 || jr > l2 || jr < 1 || s < 1 ||
-                        j > Qp || jr > Qp)
-                        continue;
-                    const Cell4 *lc = g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + d_wofs(g, l1, j) + (s - j);
-                    const Cell4 *rc = g.CELL + pc + g.base[l2] + (int64_t)(u + l1) * g.cells[l2] +
-                                      d_wofs(g, l2, jr) + (sr - jr);
-                    if (s < j || sr < jr || s > M * j || sr > M * jr) continue;
-                    const Cell4 Lc = d_load(lc), Rc = d_load(rc);
-                    const double cL = __dadd_rn(Lc.C1, (double)(3 * sr));
-                    const double cR = __dadd_rn(Rc.C1, (double)(4 * s));
-                    const double tot = split_total(Lc.T1, Lc.T3, Lc.TS, cL, Rc.T1, Rc.T3, Rc.TS, cR);
+                    okk[d] = !(l1 < 2 || l2 < 2 || s > l1 || sr > l2 || j > l1 || jr > l2 || jr < 1 || s < j || sr < jr ||
+                               s > M * j || sr > M * jr);
+                    if (!okk[d]) continue;
+                    Lk[d] = d_load(g.CELL + pc + g.base[l1] + (int64_t)u * g.cells[l1] + d_wofs(g, l1, j) + (s - j));
+                    Rk[d] = d_load(g.CELL + pc + g.base[l2] + (int64_t)(u + l1) * g.cells[l2] + d_wofs(g, l2, jr) +
+                                   (sr - jr));
+                }
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    if (!okk[d]) continue;
+                    const int l1 = l1p + d - side;
+                    const double cL = __dadd_rn(Lk[d].C1, (double)(3 * sr));
+                    const double cR = __dadd_rn(Rk[d].C1, (double)(4 * s));
+                    const double tot = split_total(Lk[d].T1, Lk[d].T3, Lk[d].TS, cL, Rk[d].T1, Rk[d].T3, Rk[d].TS, cR);
                     const unsigned long long tb = (unsigned long long)__double_as_longlong(tot);
                     const uint32_t key = ((uint32_t)l1 << 20) | ((uint32_t)j << 10) | (uint32_t)s;
                     if (lex_less(tb, key, bb, bk)) { bb = tb; bk = key; }
