@@ -235,7 +235,7 @@ struct oob_dp_plan {
     int perm_order = 0;                  // OOB_DP_PERM=1: pseudo-random unit order
     int rev_lanes = 0;                   // OOB_DP_REV=1: reversed lane <-> tile order
     int chunk_max = 192;                 // OOB_DP_CHMAX: streamed cells per unit (upper bound)
-    int seed_w = 0;                      // OOB_DP_SEEDW: warm-start seed (j, s) neighbourhood radius
+    int aux_first = 0;                   // OOB_DP_AUXFIRST: extra blocks first in k_wave_w's grid
     size_t geom_bytes = 0, ws_bytes = 0, tpl_bytes = 0;
     std::vector<unsigned char> geom_blob;   // host image of the geometry region
     size_t off_cells = 0, off_base = 0, off_off = 0, off_wofs = 0, off_tiles = 0, off_tile_off = 0, off_tile_cnt = 0,
@@ -390,7 +390,7 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     if (const char *po = std::getenv("OOB_DP_PERM")) pl->perm_order = std::atoi(po) != 0;
     if (const char *rv = std::getenv("OOB_DP_REV")) pl->rev_lanes = std::atoi(rv) != 0;
     if (const char *cm = std::getenv("OOB_DP_CHMAX")) pl->chunk_max = std::max(12, std::atoi(cm));
-    if (const char *sw = std::getenv("OOB_DP_SEEDW")) pl->seed_w = std::max(0, std::min(3, std::atoi(sw)));
+    if (const char *af = std::getenv("OOB_DP_AUXFIRST")) pl->aux_first = std::atoi(af) != 0;
     for (int ci = 0; ci < NWCFG; ++ci) build_tiles(pl, WCFGS[ci].te);
     pl->stream_steps.assign(L + 1, 0.0);
     for (int ls = 1; ls <= L; ++ls) {
@@ -650,7 +650,6 @@ static FinArgs make_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglong2 *ga
     f.nbseed = (int)((nsd + 255) / 256);
     f.GSEED = gacc_of(pl, gacc, ls);
     f.GFS = gfilt_of(pl, gacc, ls);
-    f.seedw = pl->seed_w;
     f.ls = ls;
     f.nsmall = ls ? small_cells(G, ls) : 0;
     f.tpc = ls ? small_tpc(G, ls, pl->small_pairs) : 32;
@@ -776,6 +775,7 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
         const bool fused = pl->fuse_fin && ctas > 0 && !shard && wh.seed_units == 0;
         int64_t aux = 0;
         w.nbmain = (int)ctas;
+        w.aux_first = pl->aux_first;
         w.fin_inline = fused ? 1 : 0;
         w.rdone = (int *)(ws + pl->off_CTR) + wh.done_off;
         w.rclaim = w.rdone + (size_t)pl->P * w.nranges;

@@ -54,7 +54,6 @@ struct FinArgs {
     int lseed, nout_s, nbseed;     // seeds of wave lseed (0: none): W outputs per range, blocks
     ulonglong2 *GSEED;             // accumulator of wave lseed (the other parity buffer)
     unsigned *GFW, *GFS;           // global filters (binary32 bits of F(min)) of waves lw / lseed
-    int seedw;                     // warm-start seeds: (j, s) neighbourhood radius
     int ls, nsmall;                // small cells of wave ls (ls = 0: none); cells per range
     int tpc;                       // threads per small cell
 };
@@ -83,6 +82,7 @@ struct WaveW {
     // the next wave (fa: nbw = 0; independent of this wave, they fill its tail); the last CTA
     // of each range (rdone counter) finalizes the range's W outputs of this wave (fw: lw = l)
     int nbmain;
+    int aux_first;             // 1: the extra blocks come first in the grid (start with the main work)
     int fin_inline;
     int *rdone;                // [P][nranges] CTAs of the range that have merged
     int *rclaim;               // [P][nranges] finalize shares claimed
@@ -882,8 +882,11 @@ template <int TE>
 __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, WaveW w) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_last;
-    if ((int)blockIdx.x >= w.nbmain) {        // next wave's seeds and in-node cells
-        const int ab = (int)blockIdx.x - w.nbmain;
+    // block order: aux_first ? [extra blocks][main CTAs] : [main CTAs][extra blocks]
+    const int naux = (int)gridDim.x - w.nbmain;
+    const int bid = w.aux_first ? (int)blockIdx.x - naux : (int)blockIdx.x;   // main CTA index
+    if (bid < 0 || bid >= w.nbmain) {         // next wave's seeds and in-node cells
+        const int ab = w.aux_first ? (int)blockIdx.x : (int)blockIdx.x - w.nbmain;
         if (ab < w.fa.nbseed)
             fin_seed_one(g, w.fa, (int64_t)ab * NTW + threadIdx.x);
         else
@@ -906,20 +909,35 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
     float4 *rings = reinterpret_cast<float4 *>(smem + ring_off);
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    const int pr = blockIdx.x / w.cpr;
+    const int pr = bid / w.cpr;
     const int u = pr % w.nranges;
     const int p = pr / w.nranges;
     const int64_t pc = (int64_t)p * g.C;
     const int Ql = (l == L) ? g.n_hi : max(1, g.n_hi - 1);
 
-    const ulonglong2 *gseed = w.GACC + ((size_t)(blockIdx.x / w.cpr)) * nout;   // this range's entries
-    unsigned *gfilt = w.GFILT + ((size_t)(blockIdx.x / w.cpr)) * nout;
-    for (int i = tid; i < nout + ndum; i += NTW) {
-        const bool real = i < nout;
-        ulonglong2 a = real ? make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull) : make_ulonglong2(0ull, 0ull);
-        if (real && w.seeded) a = __ldcg(gseed + i);
-        acc[i] = a;
-        filt[i] = real ? min(__float_as_uint(filt_of(a.x)), __ldcg(gfilt + i)) : 0xBF800000u;   // dummies: -1
+    const ulonglong2 *gseed = w.GACC + (size_t)pr * nout;   // this range's entries
+    unsigned *gfilt = w.GFILT + (size_t)pr * nout;
+    // accumulator from the seeds, filter from the range's global filter (F of the seeds and
+    // of every improvement so far: <= F(seed)); 4 entries per thread in flight together
+    for (int i0 = tid; i0 < nout + ndum; i0 += 4 * NTW) {
+        ulonglong2 a[4];
+        unsigned fv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int i = i0 + j * NTW;
+            const bool real = i < nout;
+            a[j] = real ? make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull) : make_ulonglong2(0ull, 0ull);
+            if (real && w.seeded) a[j] = __ldcg(gseed + i);
+            fv[j] = real ? __ldcg(gfilt + i) : 0xBF800000u;   // dummies: -1 (nothing passes)
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int i = i0 + j * NTW;
+            if (i < nout + ndum) {
+                acc[i] = a[j];
+                filt[i] = fv[j];
+            }
+        }
     }
     for (int i = tid; i < L + 2; i += NTW) {
         sbase[i] = g.base[i];
