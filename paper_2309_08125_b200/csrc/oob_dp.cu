@@ -108,7 +108,11 @@ __global__ void k_wave_v1(DevGeom g, int l) {
 // ------------------------------------------------------------------ K_extract
 // One thread per (profile, template size n): argmin over S (strict <, smaller S wins),
 // then the split-tree backtrack (left child first => stages in pipeline order).
-__global__ void k_extract(DevGeom g, unsigned char *packed, size_t tpl_bytes) {
+__global__ void k_extract(DevGeom g, unsigned char *packed, size_t tpl_bytes, Pipe pp) {
+    if (pp.on) {                      // the pipelined waves' last cells (and, by monotonicity, all)
+        if (threadIdx.x == 0) pipe_wait(pp, g.L, g.L, 6);
+        __syncthreads();
+    }
     const int p_cnt = g.n_hi - g.n_lo + 1;
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= p_cnt * g.P) return;
@@ -236,9 +240,11 @@ struct oob_dp_plan {
     int rev_lanes = 0;                   // OOB_DP_REV=1: reversed lane <-> tile order
     int chunk_max = 192;                 // OOB_DP_CHMAX: streamed cells per unit (upper bound)
     int aux_first = 0;                   // OOB_DP_AUXFIRST: extra blocks first in k_wave_w's grid
+    int pipe = 1;                        // OOB_DP_PIPE=0: plain kernel boundaries between wavefronts
+    size_t pipe_cnt_off = 0;             // ints into the counter region: [3][L+2] + error word
     size_t geom_bytes = 0, ws_bytes = 0, tpl_bytes = 0;
     std::vector<unsigned char> geom_blob;   // host image of the geometry region
-    size_t off_cells = 0, off_base = 0, off_off = 0, off_wofs = 0, off_tiles = 0, off_tile_off = 0, off_tile_cnt = 0,
+    size_t off_cells = 0, off_base = 0, off_off = 0, off_wofs = 0, off_pexp = 0, off_tiles = 0, off_tile_off = 0, off_tile_cnt = 0,
            off_items = 0;
     size_t off_CELL = 0, off_SH = 0, off_ARG = 0, off_STK = 0, off_GACC = 0, off_GFILT = 0, off_CTR = 0;
     int64_t gacc_n = 0;
@@ -391,6 +397,7 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     if (const char *rv = std::getenv("OOB_DP_REV")) pl->rev_lanes = std::atoi(rv) != 0;
     if (const char *cm = std::getenv("OOB_DP_CHMAX")) pl->chunk_max = std::max(12, std::atoi(cm));
     if (const char *af = std::getenv("OOB_DP_AUXFIRST")) pl->aux_first = std::atoi(af) != 0;
+    if (const char *pp = std::getenv("OOB_DP_PIPE")) pl->pipe = std::atoi(pp) != 0;
     for (int ci = 0; ci < NWCFG; ++ci) build_tiles(pl, WCFGS[ci].te);
     pl->stream_steps.assign(L + 1, 0.0);
     for (int ls = 1; ls <= L; ++ls) {
@@ -459,6 +466,8 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
         }
         pl->max_smem = std::max(pl->max_smem, wh.smem);
     }
+    pl->pipe_cnt_off = ctr_total;
+    ctr_total += 3 * (size_t)(L + 2) + 1;
     pl->ctr_n = ctr_total;
     if (pl->max_smem > 227 * 1024) pl->kernel = 1;
     if (std::getenv("OOB_DP_DEBUG")) {
@@ -475,19 +484,20 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     pl->off_base = o;  o = align_up(o + sizeof(int64_t) * (L + 2), 256);
     pl->off_off = o;   o = align_up(o + sizeof(int32_t) * (size_t)(L + 1) * g.A, 256);
     pl->off_wofs = o;  o = align_up(o + sizeof(int32_t) * (size_t)(L + 1) * (L + 2), 256);
+    pl->off_pexp = o;  o = align_up(o + sizeof(int32_t) * 3 * (size_t)(L + 2), 256);
     pl->off_tiles = o; o = align_up(o + sizeof(int32_t) * pl->tiles.size(), 256);
     pl->off_tile_off = o; o = align_up(o + sizeof(int32_t) * (L + 1) * NWCFG, 256);
     pl->off_tile_cnt = o; o = align_up(o + sizeof(int32_t) * (L + 1) * NWCFG, 256);
     pl->off_items = o;    o = align_up(o + items_total, 256);
     pl->geom_bytes = o;
-    const size_t n = (size_t)g.total_cells * num_profiles;
+    const size_t n = (size_t)g.table_cells * num_profiles;
     pl->off_CELL = o; o = align_up(o + 32 * (n + 16 + XR_CELLS), 256);   // + padding: row streams read ahead
     pl->off_SH = o; o = align_up(o + 16 * (n + 16 + XR_CELLS), 256);     // shadow lower bounds (+ padding)
     pl->off_ARG = o; o = align_up(o + 4 * n, 256);
     pl->off_STK = o; o = align_up(o + 8 * (size_t)num_profiles * (n_hi - n_lo + 1) * (L + 1), 256);
     pl->gacc_n = (int64_t)gacc_max;
-    pl->off_GACC = o; o = align_up(o + 2 * 16 * gacc_max, 256);   // two parity buffers
-    pl->off_GFILT = o; o = align_up(o + 2 * 4 * gacc_max, 256);   // their filters
+    pl->off_GACC = o; o = align_up(o + 3 * 16 * gacc_max, 256);   // three buffers (wave mod 3)
+    pl->off_GFILT = o; o = align_up(o + 3 * 4 * gacc_max, 256);   // their filters
     pl->off_CTR = o; o = align_up(o + 4 * pl->ctr_n + 4, 256);
     pl->ws_bytes_base = o;
     pl->ws_bytes = o;
@@ -497,6 +507,21 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     std::memcpy(b + pl->off_cells, g.cells.data(), sizeof(int32_t) * (L + 1));
     std::memcpy(b + pl->off_base, g.base.data(), sizeof(int64_t) * (L + 2));
     std::memcpy(b + pl->off_off, g.off.data(), sizeof(int32_t) * (size_t)(L + 1) * g.A);
+    {   // pipeline: blocks / shares that make each wave's seeds, in-node cells and W part ready
+        int32_t *ex = reinterpret_cast<int32_t *>(b + pl->off_pexp);
+        for (int l = 2; l <= L; ++l) {
+            const WaveHost &wh = pl->waves[l];
+            const int64_t nr = L - l + 1;
+            if (l >= 3) {                       // produced by launch l-1's extra blocks
+                const int64_t nsd = wh.seed ? (int64_t)num_profiles * nr * wh.nout : 0;
+                ex[l] = (int32_t)((nsd + 255) / 256);
+                const int tpc = small_tpc(g, l, pl->small_pairs);
+                const int64_t ns = (int64_t)num_profiles * nr * small_cells(g, l);
+                ex[(L + 2) + l] = (int32_t)((ns + (256 / tpc) - 1) / (256 / tpc));
+            }
+            ex[2 * (L + 2) + l] = wh.nents > 0 ? (int32_t)((int64_t)num_profiles * nr * wh.cpr) : 0;
+        }
+    }
     {   // W row offsets per slab length (I part + rows 1..q-1), DevGeom::wofs
         int32_t *wo = reinterpret_cast<int32_t *>(b + pl->off_wofs);
         for (int l = 0; l <= L; ++l) {
@@ -620,17 +645,18 @@ extern "C" oob_status oob_dp_kernel_time(oob_dp_plan *pl, double *ms_out, int64_
 // accumulator of wave l: two parity buffers (k_fin finalizes wave l-1 from one while it
 // seeds wave l into the other)
 static ulonglong2 *gacc_of(const oob_dp_plan *pl, ulonglong2 *gacc, int l) {
-    return gacc + (size_t)(l & 1) * (size_t)pl->gacc_n;
+    return gacc + (size_t)(l % 3) * (size_t)pl->gacc_n;
 }
 // global filter of wave l's accumulator (same parity and index)
 static unsigned *gfilt_of(const oob_dp_plan *pl, ulonglong2 *gacc, int l) {
-    return (unsigned *)((unsigned char *)gacc - pl->off_GACC + pl->off_GFILT) + (size_t)(l & 1) * (size_t)pl->gacc_n;
+    return (unsigned *)((unsigned char *)gacc - pl->off_GACC + pl->off_GFILT) + (size_t)(l % 3) * (size_t)pl->gacc_n;
 }
 
 // Finalize arguments for wave lw (0: none) and in-node cells + seeds of wave ls (0: none);
 // *nbsmall receives the blocks of the small-cell part.
 static FinArgs make_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglong2 *gacc, int lw, int ls, bool sharded,
-                        int64_t *nbsmall) {
+                        int64_t *nbsmall, int lsd = -1) {
+    if (lsd < 0) lsd = ls;                 // seeds of wave lsd (pipelined waves: two waves ahead)
     const Geometry &G = pl->g;
     FinArgs f;
     f.lw = lw;
@@ -644,12 +670,12 @@ static FinArgs make_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglong2 *ga
     f.part_stride = (int64_t)pl->P * f.nranges_w * f.nout_w;   // all-gather: rank r at r x (wave partial)
     f.GPART = (const ulonglong2 *)((const unsigned char *)dg.CELL - pl->off_CELL + pl->off_GPART);
     // seeds for wave ls (children of length <= ls-2: final before this launch)
-    f.lseed = (ls >= 2 && pl->waves[ls].seed) ? ls : 0;
-    f.nout_s = f.lseed ? pl->waves[ls].nout : 0;
-    const int64_t nsd = f.lseed ? (int64_t)pl->P * (G.L - ls + 1) * f.nout_s : 0;
+    f.lseed = (lsd >= 2 && lsd <= G.L && pl->waves[lsd].seed) ? lsd : 0;
+    f.nout_s = f.lseed ? pl->waves[lsd].nout : 0;
+    const int64_t nsd = f.lseed ? (int64_t)pl->P * (G.L - lsd + 1) * f.nout_s : 0;
     f.nbseed = (int)((nsd + 255) / 256);
-    f.GSEED = gacc_of(pl, gacc, ls);
-    f.GFS = gfilt_of(pl, gacc, ls);
+    f.GSEED = gacc_of(pl, gacc, lsd);
+    f.GFS = gfilt_of(pl, gacc, lsd);
     f.ls = ls;
     f.nsmall = ls ? small_cells(G, ls) : 0;
     f.tpc = ls ? small_tpc(G, ls, pl->small_pairs) : 32;
@@ -697,7 +723,7 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
     }
     DevGeom dg;
     dg.L = G.L; dg.M = G.M; dg.n_lo = G.n_lo; dg.n_hi = G.n_hi; dg.A = G.A; dg.P = pl->P;
-    dg.C = G.total_cells;
+    dg.C = G.table_cells;
     dg.cells = (const int32_t *)(ws + pl->off_cells);
     dg.base = (const int64_t *)(ws + pl->off_base);
     dg.off = (const int32_t *)(ws + pl->off_off);
@@ -724,10 +750,22 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
         }
     }
     ulonglong2 *gacc = (ulonglong2 *)(ws + pl->off_GACC);
+    // pipelined wavefronts: only the fused single-pass, unsharded W kernel
+    bool pipe_on = pl->pipe && pl->kernel == 2 && pl->world == 1 && pl->fuse_fin;
+    // ... and only when every wave's main grid fits the resident CTA slots (a single profile):
+    // batched sweeps have far more CTAs than slots and gain nothing from the overlap
+    for (int l = 2; l <= G.L && pipe_on; ++l)
+        pipe_on = pl->waves[l].nents > 0 && pl->waves[l].seed_units == 0 &&
+                  (int64_t)pl->P * (G.L - l + 1) * pl->waves[l].cpr <= (int64_t)CTAS_PER_SM * 148;
+    Pipe pp;
+    pp.cnt = (int *)(ws + pl->off_CTR) + pl->pipe_cnt_off;
+    pp.expc = (const int *)(ws + pl->off_pexp);
+    pp.err = pp.cnt + 3 * (G.L + 2);
+    pp.on = pipe_on ? 1 : 0;
     if (pl->kernel == 2) {
         if (pl->gacc_ready != d_ws && pl->gacc_n > 0) {   // finalize resets what it reads
-            k_gacc_init<<<(unsigned)((2 * pl->gacc_n + 255) / 256), 256, 0, stream>>>(gacc, gfilt_of(pl, gacc, 0),
-                                                                                     2 * pl->gacc_n);
+            k_gacc_init<<<(unsigned)((3 * pl->gacc_n + 255) / 256), 256, 0, stream>>>(gacc, gfilt_of(pl, gacc, 0),
+                                                                                     3 * pl->gacc_n);
             e = cudaGetLastError();
             if (e != cudaSuccess) return cuda_fail(e, "k_gacc_init launch");
             pl->gacc_ready = d_ws;
@@ -785,7 +823,8 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
             w.fw = make_fin(pl, dg, gacc, l, 0, false, &nbw);
             aux = w.fa.nbseed + nbs;
         }
-        if (pl->timing) cudaEventRecord(pl->ev[pl->ev_used], stream);
+        if (pl->timing && (!pipe_on || l == 2)) cudaEventRecord(pl->ev[pl->ev_used], stream);
+        w.pp = pp;
         if (ctas > 0) {
             // pass 1 (optional): the seeding units; pass 2: the rest, from the seeded minima
             for (int pass = wh.seed_units > 0 ? 0 : 1; pass < 2; ++pass) {
@@ -802,15 +841,30 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
                     w.perm_a = n > 2 ? a : 1;
                 }
                 const unsigned grid = (unsigned)(ctas + aux);
-                switch (WCFGS[wh.cfg].te) {
-                    case 2: k_wave_w<2><<<grid, NTW, wh.smem, stream>>>(dg, w); break;
-                    case 3: k_wave_w<3><<<grid, NTW, wh.smem, stream>>>(dg, w); break;
-                    case 4: k_wave_w<4><<<grid, NTW, wh.smem, stream>>>(dg, w); break;
-                    default: k_wave_w<5><<<grid, NTW, wh.smem, stream>>>(dg, w); break;
+                void (*kern)(DevGeom, WaveW) = WCFGS[wh.cfg].te == 2 ? k_wave_w<2> : WCFGS[wh.cfg].te == 3 ? k_wave_w<3>
+                                               : WCFGS[wh.cfg].te == 4 ? k_wave_w<4> : k_wave_w<5>;
+                if (pipe_on && l >= 3) {   // programmatic dependent of wave l-1 (counters, not the boundary)
+                    cudaLaunchConfig_t lc = {};
+                    lc.gridDim = dim3(grid);
+                    lc.blockDim = dim3(NTW);
+                    lc.dynamicSmemBytes = wh.smem;
+                    lc.stream = stream;
+                    cudaLaunchAttribute at[1];
+                    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                    at[0].val.programmaticStreamSerializationAllowed = 1;
+                    lc.attrs = at;
+                    lc.numAttrs = 1;
+                    e = cudaLaunchKernelEx(&lc, kern, dg, w);
+                    if (e != cudaSuccess) return cuda_fail(e, "k_wave_w launch (pipelined)");
+                } else {
+                    kern<<<grid, NTW, wh.smem, stream>>>(dg, w);
                 }
             }
         }
-        if (pl->timing) { cudaEventRecord(pl->ev[pl->ev_used + 1], stream); pl->ev_used += 2; }
+        if (pl->timing && (!pipe_on || l == G.L)) {
+            cudaEventRecord(pl->ev[pl->ev_used + 1], stream);
+            pl->ev_used += 2;
+        }
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "k_wave_w launch");
         if (shard) {   // one all-gather of the wave's partial argmins (every rank finalizes all)
@@ -824,7 +878,7 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
     }
     {
         int n = (G.n_hi - G.n_lo + 1) * pl->P;
-        k_extract<<<(n + 63) / 64, 64, 0, stream>>>(dg, (unsigned char *)d_packed, pl->tpl_bytes);
+        k_extract<<<(n + 63) / 64, 64, 0, stream>>>(dg, (unsigned char *)d_packed, pl->tpl_bytes, pp);
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "k_extract launch");
     }

@@ -44,11 +44,13 @@ bool build_geometry(int L, int M, int n_lo, int n_hi, Geometry &g) {
         g.cells[l] = off;
     }
     g.base[1] = 0;
+    g.total_cells = 0;
     for (int l = 1; l <= L; ++l) {
-        g.base[l + 1] = g.base[l] + (int64_t)(L - l + 1) * g.cells[l];
         g.wave_cells[l] = (int64_t)(L - l + 1) * g.cells[l];
+        g.base[l + 1] = g.base[l] + g.wave_cells[l] + WAVE_PAD;
+        g.total_cells += g.wave_cells[l];
     }
-    g.total_cells = g.base[L + 1];
+    g.table_cells = g.base[L + 1];
 
     // Feasible splits.  For a split at l1 = k-u (l2 = l-l1) the valid (s, S-s) pairs of a
     // device split (a1, a2) are exactly len(a1, l1) x len(a2, l2): every such pair lands

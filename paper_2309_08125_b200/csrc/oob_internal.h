@@ -25,6 +25,11 @@ inline size_t align_up_host(size_t x, size_t a = 256) { return (x + a - 1) / a *
 //  Cells of one wavefront l = v-u are laid out per range start u (a "slab" of cells(l)
 //  cells), inside a slab by allocation then S'.  Global cell index
 //     base[l] + u*cells[l] + off[l*A + a] + (S' - lo(a)).
+// Cells of padding after each wavefront's cells: no 32-byte sector of the cell, shadow or
+// argmin table holds cells of two wavefronts, and a streamed row's read-ahead (<= 96 cells)
+// never reaches the next wavefront (pipelined waves may still be producing it).
+constexpr int64_t WAVE_PAD = 128;
+
 struct Geometry {
     int L = 0, M = 0, n_lo = 0, n_hi = 0, A = 0;
     std::vector<int32_t> Q;          // [L+1]
@@ -33,7 +38,8 @@ struct Geometry {
     std::vector<int32_t> off;        // [(L+1)*A] offset of alloc a in a slab of length l, -1 if empty
     std::vector<int64_t> wave_splits;   // [L+1] feasible splits of wavefront l (all u)
     std::vector<int64_t> wave_cells;    // [L+1] cells of wavefront l (all u)
-    int64_t total_cells = 0;
+    int64_t total_cells = 0;         // cells of the table universe (reported)
+    int64_t table_cells = 0;         // per-profile table stride: the waves plus WAVE_PAD cells after each
     int64_t total_splits = 0;
 
     bool is_whole(int a) const { return a >= M - 1; }

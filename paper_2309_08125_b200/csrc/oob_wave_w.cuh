@@ -43,6 +43,14 @@ constexpr unsigned long long ACC_EMPTY = 0x7FEFFFFFFFFFFFFFull;   // DBL_MAX: "n
 constexpr double D_INF = __builtin_huge_val();
 constexpr unsigned long long ACC_DIRTY = 1ull << 32;   // accumulator key word: improved by this CTA
 
+// Wavefront pipeline state (see pipe_wait below)
+struct Pipe {
+    int *cnt;              // [3][L+2]: seeds, in-node cells, finalize shares done per wave
+    const int *expc;       // [3][L+2]: the counts that make each part ready
+    int *err;              // timeout flag
+    int on;
+};
+
 // Finalize / in-node work of one wavefront (k_fin, or k_wave_w's extra blocks and last CTAs).
 struct FinArgs {
     int lw, nranges_w, nout_w;     // W finalize of wave lw (lw = 0: none)
@@ -86,9 +94,11 @@ struct WaveW {
     int fin_inline;
     int *rdone;                // [P][nranges] CTAs of the range that have merged
     int *rclaim;               // [P][nranges] finalize shares claimed
+    Pipe pp;                   // wavefront pipeline (pp.on = 0: plain kernel boundaries)
     FinArgs fa, fw;
 };
 
+__device__ __forceinline__ int L_of(const DevGeom &g) { return g.L; }
 __device__ __forceinline__ int d_wcells(const DevGeom &g, int l) {
     return g.cells[l] - g.off[l * g.A + (g.M - 1)];
 }
@@ -859,10 +869,52 @@ __device__ __forceinline__ void fin_small_block(const DevGeom &g, const FinArgs 
         const uint32_t ok = __shfl_down_sync(0xFFFFFFFFu, bkey, d, wd);
         if (ob < best || (ob == best && ok < bkey)) { best = ob; bkey = ok; }
     }
-    if (tl != 0) return;
-    if (!active) return;
-    d_write_winner(g, (int64_t)p * g.C, Sp, u, l, a, (int)(bkey >> 20), (int)((bkey >> 10) & 1023u),
-                   (int)(bkey & 1023u));
+    if (tl == 0 && active)
+        d_write_winner(g, (int64_t)p * g.C, Sp, u, l, a, (int)(bkey >> 20), (int)((bkey >> 10) & 1023u),
+                       (int)(bkey & 1023u));
+}
+
+// ---------------------------------------------------------------- wavefront pipeline
+// With OOB_DP_PIPE, wavefront l+1's kernel is launched as a programmatic dependent of wave
+// l's (it starts once every CTA of wave l has started) and synchronises through per-wave
+// counters instead of kernel boundaries.  Per wave c: seeds (aux blocks of launch c-1),
+// in-node cells (aux blocks of launch c-1, or k_fin for c = 2) and the W-part finalize
+// shares (main CTAs of launch c); each producer block fences and increments its counter
+// after writing.  Readiness is monotone in c (a wave's finalize follows units that waited
+// for the previous wave), so "wave c ready" covers every shorter wave.  Every cell of a
+// wave is read only after its wave is ready (and the tables pad each wave to whole 32-byte
+// sectors plus the streams' read-ahead), so L1-cached loads never see a stale line.  Waits
+// are bounded; a timeout sets the error word and releases every later wait (the results
+// are then wrong and the parity tests fail, but the GPU never hangs).
+__device__ __forceinline__ int ld_acquire(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// one thread waits until the parts in `mask` (bit kind: 0 seeds, 1 in-node cells,
+// 2 finalize shares) of wave c are ready
+__device__ __noinline__ void pipe_wait_raw(int *cnt, const int *expc, int *err, int L, int c, int mask) {
+    for (long long it = 0;; ++it) {
+        bool ok = true;
+        for (int kind = 0; kind < 3; ++kind)
+            if ((mask >> kind) & 1) ok = ok && ld_acquire(cnt + kind * (L + 2) + c) >= expc[kind * (L + 2) + c];
+        if (ok || *(volatile int *)err) break;
+        if (it > (1ll << 24)) { atomicExch(err, 1); break; }
+        __nanosleep(200);
+    }
+    __threadfence();
+}
+__device__ __forceinline__ void pipe_wait(const Pipe &pp, int L, int c, int mask) {
+    if (pp.on && c >= 2) pipe_wait_raw(pp.cnt, pp.expc, pp.err, L, c, mask);
+}
+// the calling block has finished writing its part of wave c (all threads reach this)
+__device__ __forceinline__ void pipe_signal(const Pipe &pp, int L, int kind, int c) {
+    if (!pp.on) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(pp.cnt + kind * (L + 2) + c, 1);
+    }
 }
 
 __global__ void __launch_bounds__(256) k_fin(DevGeom g, FinArgs f) {
@@ -885,12 +937,22 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
     // block order: aux_first ? [extra blocks][main CTAs] : [main CTAs][extra blocks]
     const int naux = (int)gridDim.x - w.nbmain;
     const int bid = w.aux_first ? (int)blockIdx.x - naux : (int)blockIdx.x;   // main CTA index
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // the next wave may start (pipeline)
     if (bid < 0 || bid >= w.nbmain) {         // next wave's seeds and in-node cells
         const int ab = w.aux_first ? (int)blockIdx.x : (int)blockIdx.x - w.nbmain;
-        if (ab < w.fa.nbseed)
+        if (ab < w.fa.nbseed) {
+            // seeds of wave l+1 read cells of waves <= l-1 and reuse wave l-1's accumulator buffer
+            if (threadIdx.x == 0) pipe_wait(w.pp, L_of(g), w.fa.lseed - 2, 7);
+            __syncthreads();
             fin_seed_one(g, w.fa, (int64_t)ab * NTW + threadIdx.x);
-        else
+            pipe_signal(w.pp, L_of(g), 0, w.fa.lseed);
+        } else {
+            // in-node cells of wave l+1 read in-node cells of waves <= l
+            if (threadIdx.x == 0) pipe_wait(w.pp, L_of(g), w.fa.ls - 1, 2);
+            __syncthreads();
             fin_small_block(g, w.fa, (int64_t)ab - w.fa.nbseed);
+            pipe_signal(w.pp, L_of(g), 1, w.fa.ls);
+        }
         return;
     }
     const int l = w.l;
@@ -917,6 +979,14 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
 
     const ulonglong2 *gseed = w.GACC + (size_t)pr * nout;   // this range's entries
     unsigned *gfilt = w.GFILT + (size_t)pr * nout;
+    __shared__ int s_rdy;                      // every wave <= s_rdy is ready (pipeline)
+    if (tid == 0) {
+        if (w.seeded) pipe_wait(w.pp, L, l, 1);   // this wave's seeds (launch l-1's extra blocks)
+        // the accumulator buffer's previous user (wave l-3) has finalized: wave l-2 ready
+        pipe_wait(w.pp, L, l - 2, 6);
+        s_rdy = w.pp.on ? max(1, l - 2) : L;
+    }
+    __syncthreads();
     // accumulator from the seeds, filter from the range's global filter (F of the seeds and
     // of every improvement so far: <= F(seed)); 4 entries per thread in flight together
     for (int i0 = tid; i0 < nout + ndum; i0 += 4 * NTW) {
@@ -975,6 +1045,16 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
         const int r_lo = w.cb[en.w + chunk], r_hi = w.cb[en.w + chunk + 1];
         const int k = u + l1;
         const int l2 = l - l1;
+        if (w.pp.on) {                                           // both children's waves ready?
+            const int cmax = max(l1, l2);
+            if (cmax > *(volatile int *)&s_rdy) {
+                if (lane == 0) {
+                    pipe_wait(w.pp, L, cmax, 6);                 // in-node cells + W finalize
+                    atomicMax(&s_rdy, cmax);
+                }
+                __syncwarp();
+            }
+        }
         const bool ltiled = (en.x >> 16) & 1;                     // tiled side = left child
         const int ls = ltiled ? l2 : l1;                           // small side length
         const int lb = ltiled ? l1 : l2;
@@ -1083,6 +1163,7 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
                 const int c = s_last;
                 if (c >= w.cpr) break;
                 fin_w_range<NTW>(g, w.fw, pr, tid, c, w.cpr);
+                pipe_signal(w.pp, L, 2, l);
             }
         }
     }
