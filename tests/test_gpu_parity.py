@@ -82,13 +82,16 @@ def test_batched_profiles_vs_oracle(planner):
         _assert_same(ts.templates(i), want, f"cfg5 profile {i}")
 
 
-@pytest.mark.parametrize("fuse", ["default", "0", "1"])
+@pytest.mark.parametrize("fuse", ["default", "0", "1", "pipe0"])
 @pytest.mark.parametrize("mode", ["real", "dyadic"])
 def test_cfg4_full_vs_golden(planner, mode, fuse, monkeypatch):
     """Full template set of the north-star config (96 layers, 512 x 8 GPUs, f=4, n0=3)
     vs the C oracle's output stored by scripts/make_golden.py; with the finalize fused into
-    k_wave_w (OOB_DP_FUSE=1) and as separate k_fin launches (0)."""
-    if fuse != "default":
+    k_wave_w (OOB_DP_FUSE=1, pipelined wavefronts by default), as separate k_fin launches
+    (0), and fused without the wavefront pipeline (pipe0)."""
+    if fuse == "pipe0":
+        monkeypatch.setenv("OOB_DP_PIPE", "0")
+    elif fuse != "default":
         monkeypatch.setenv("OOB_DP_FUSE", fuse)
     rec = load_golden("cfg4", mode)
     if rec is None:
@@ -166,9 +169,13 @@ VARIANTS = [
     {"OOB_DP_WCFG": "3"},            # TE = 2
     {"OOB_DP_FUSE": "0"},            # separate k_fin launches
     {"OOB_DP_FUSE": "1"},            # finalize + next wave's in-node cells inside k_wave_w
-    {"OOB_DP_SEEDSPO": "0"},         # every wave >= 6 seeded
+    {"OOB_DP_SEEDSPO": "1000"},      # only waves with >= 1000 splits per output seeded
     {"OOB_DP_SEEDINIT": "0"},        # no seeds
     {"OOB_DP_SMALLPAIRS": "4"},      # fewer threads per in-node cell
+    {"OOB_DP_PIPE": "0"},            # plain kernel boundaries between wavefronts
+    {"OOB_DP_PIPE": "0", "OOB_DP_SEEDINIT": "0"},
+    {"OOB_DP_CHMAX": "24"},          # short units: many per range, long queues
+    {"OOB_DP_AUXFIRST": "1"},        # extra blocks first in the grid (finalize waits bounded)
 ]
 
 
