@@ -240,6 +240,7 @@ struct oob_dp_plan {
     int rev_lanes = 0;                   // OOB_DP_REV=1: reversed lane <-> tile order
     int chunk_max = 192;                 // OOB_DP_CHMAX: streamed cells per unit (upper bound)
     int aux_first = 0;                   // OOB_DP_AUXFIRST: extra blocks first in k_wave_w's grid
+    int refresh = 1;                     // OOB_DP_REFRESH=0: no per-unit filter refresh
     int pipe = 1;                        // OOB_DP_PIPE=0: plain kernel boundaries between wavefronts
     size_t pipe_cnt_off = 0;             // ints into the counter region: [3][L+2] + error word
     size_t geom_bytes = 0, ws_bytes = 0, tpl_bytes = 0;
@@ -397,6 +398,7 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     if (const char *rv = std::getenv("OOB_DP_REV")) pl->rev_lanes = std::atoi(rv) != 0;
     if (const char *cm = std::getenv("OOB_DP_CHMAX")) pl->chunk_max = std::max(12, std::atoi(cm));
     if (const char *af = std::getenv("OOB_DP_AUXFIRST")) pl->aux_first = std::atoi(af) != 0;
+    if (const char *rf = std::getenv("OOB_DP_REFRESH")) pl->refresh = std::atoi(rf) != 0;
     if (const char *pp = std::getenv("OOB_DP_PIPE")) pl->pipe = std::atoi(pp) != 0;
     for (int ci = 0; ci < NWCFG; ++ci) build_tiles(pl, WCFGS[ci].te);
     pl->stream_steps.assign(L + 1, 0.0);
@@ -814,6 +816,7 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
         int64_t aux = 0;
         w.nbmain = (int)ctas;
         w.aux_first = pl->aux_first;
+        w.refresh = pl->refresh;
         w.fin_inline = fused ? 1 : 0;
         w.rdone = (int *)(ws + pl->off_CTR) + wh.done_off;
         w.rclaim = w.rdone + (size_t)pl->P * w.nranges;

@@ -95,6 +95,7 @@ struct WaveW {
     int *rdone;                // [P][nranges] CTAs of the range that have merged
     int *rclaim;               // [P][nranges] finalize shares claimed
     Pipe pp;                   // wavefront pipeline (pp.on = 0: plain kernel boundaries)
+    int refresh;               // 1: each unit refreshes its filter entries from the range's global filter
     FinArgs fa, fw;
 };
 
@@ -1082,7 +1083,7 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
             TS[t] = c.z;
             TC[t] = (float)((ltiled ? 4 : 3) * (rowB + e0 + t));
         }
-        {   // refresh the filter of the outputs this unit can touch (rows q = rowB + rs) from the
+        if (w.refresh) {   // refresh the filter of the outputs this unit can touch (rows q = rowB + rs) from the
             // range's global filter: minima other CTAs found since this CTA last looked
             const int tb0 = blk * 32, tb1 = min(blk * 32 + 31, w.tile_cnt[lb] - 1);
             const int rmin = w.tiles[w.tile_off[lb] + tb0] >> 16, rmax = w.tiles[w.tile_off[lb] + tb1] >> 16;
