@@ -816,7 +816,7 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
         int64_t aux = 0;
         w.nbmain = (int)ctas;
         w.aux_first = pl->aux_first;
-        w.refresh = pl->refresh;
+        w.refresh = pl->refresh && wh.cpr > 1;   // one CTA per range: its own filter is current
         w.fin_inline = fused ? 1 : 0;
         w.rdone = (int *)(ws + pl->off_CTR) + wh.done_off;
         w.rclaim = w.rdone + (size_t)pl->P * w.nranges;
