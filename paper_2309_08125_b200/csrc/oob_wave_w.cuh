@@ -469,6 +469,19 @@ __device__ __forceinline__ void fast_step(const float4 x, float fst, int I, cons
     }
 }
 
+// Pass bits (bit r + d) of the pending outputs E' = rl + d, d = 0..TE-2, when rl mod TE = R
+// (slot (R + d) mod TE), against their filter entries fp[d].
+template <int TE, int R>
+__device__ __forceinline__ unsigned pending_mask(const float (&mn)[TE], const float *fp) {
+    unsigned pm = 0;
+    if (R < TE) {
+#pragma unroll
+        for (int d = 0; d <= TE - 2; ++d)
+            pm |= (mn[(R + d) % TE] <= fp[d]) ? (1u << (R + d)) : 0u;
+    }
+    return pm;
+}
+
 // The small-side rows r_lo..r_hi-1 of one unit against this lane's register tile (shadow
 // lower bounds TA/TB/TS/TC; binary64 tile at bp for the exact path).  Each row runs full
 // blocks of TE steps (no guards) and a guarded tail; the outputs whose bounds pass the
@@ -545,16 +558,14 @@ __device__ __forceinline__ void run_rows(XRing &xr, int64_t sidx, const int32_t 
                     pm |= (mn[I] <= fr[blk + I]) ? (1u << I) : 0u;
                 }
             }
-            // pending outputs E' = rl + d (d = 0..TE-2) live in slot (rl + d) mod TE: one
-            // unrolled case per rl mod TE keeps the slot indices static
-            const int r0 = rl - blk;                      // = rl mod TE
-#pragma unroll
-            for (int r = 0; r < TE; ++r) {
-                if (r == r0) {
-#pragma unroll
-                    for (int d = 0; d <= TE - 2; ++d)
-                        if (mn[(r + d) % TE] <= fr[rl + d]) pm |= 1u << (r + d);
-                }
+            // pending outputs E' = rl + d (d = 0..TE-2) live in slot (rl + d) mod TE; rl mod TE
+            // is warp-uniform, so a switch branches to one case with static slot indices
+            switch (rl - blk) {                           // = rl mod TE
+                case 0: pm |= pending_mask<TE, 0>(mn, fr + rl); break;
+                case 1: pm |= pending_mask<TE, 1>(mn, fr + rl); break;
+                case 2: pm |= pending_mask<TE, 2>(mn, fr + rl); break;
+                case 3: pm |= pending_mask<TE, 3>(mn, fr + rl); break;
+                default: pm |= pending_mask<TE, 4>(mn, fr + rl); break;
             }
             if (__any_sync(0xFFFFFFFFu, pm != 0))
                 qn = xq_push<TE, LT>(pm, blk, (unsigned)bidx, ncell, (unsigned)srow, rl, S0, rs, kb, idx0, q4, q1, qn,
