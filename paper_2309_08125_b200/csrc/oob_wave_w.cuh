@@ -1,36 +1,32 @@
-// Wavefront kernels for cells with S' >= 2 (SURVEY §8(a) a4, the hot loop).
+// Wavefront kernels for cells with S' >= 2 (SURVEY §8(a) a4, the hot loop; DESIGN.md §6).
 //
-// k_wave_w — whole-node cells W(q >= 2).  For a range (u, v) of length l and a layer split
-// k (l1 = k-u, l2 = v-k), W(q) cells combine left children W(j) of (u, k) with right
+// k_wave_w — whole-node cells W(q >= 2) of wavefront l.  For a range (u, v) and a layer
+// split k (l1 = k-u, l2 = v-k), W(q) cells combine left children W(j) of (u, k) with right
 // children W(q-j) of (k, v) (PAPER Eq.1-3, two-level device split: reading R2).  In
 // (nodes, stages) coordinates every pair (left cell, right cell) is a valid split of
-// exactly one parent cell (q = j + j', S' = s + S_R): for each row pair (j, j') the work is
-// a dense a_j x b_j' rectangle of splits.  Mapping (one CTA per (item, profile, range);
-// items are lists of layer splits k, ordered by decreasing cost so the block scheduler
-// runs them longest-first):
-//   * the child slab with more W cells ("big side") is register-tiled: a lane holds TE
-//     consecutive cells of one row; 32 consecutive tiles (rows may straddle lanes) and one
-//     chunk of small-side rows form a warp work unit; warps pull units from a counter;
-//   * a unit walks its rows of the other slab ("small side") cell by cell; all lanes read
-//     the same cell (L1 broadcast, 2 x 16-byte loads) and evaluate TE splits;
-//   * the outputs a lane touches slide by one cell per step: a ring of TE slots keeps, per
-//     in-flight output, only the minimum HIGH WORD of its totals (one 32-bit min per
-//     split).  When an output's last contribution from this lane has arrived, the slot is
-//     compared with the high word of the CTA's shared-memory accumulator entry; only if it
-//     is <= (it can win or tie) does the lane recompute that output's TE splits exactly
-//     (the same binary64 operations, hence the same bits) and merge the lexicographic
-//     minimum of (total, split key) with a 128-bit compare-and-swap — exact under any
-//     interleaving.  Since the high word of a positive binary64 is monotone in its value,
-//     the filter never drops a winner.
-//   * at the end of the task the CTA's accumulator is merged into the global accumulator
-//     of the range (128-bit global CAS); k_fin recomputes each winner's cell.
-// Tie semantics: the oracle keeps the first strictly smaller total in (k, m, s) order; the
-// key l1<<20 | j<<10 | s is monotone in (k, m, s), so the lexicographic minimum of
-// (total, key) is exactly the oracle's argmin.
+// exactly one parent (q = j + j', S' = s + S_R): each row pair (j, j') is a dense rectangle.
+//   * Work: per wave one unit queue (layer split k, chunk of streamed rows, block of 32
+//     register tiles of TE cells), balanced splits first; `cpr` CTAs per (profile, range)
+//     pull units; a lane streams its unit's rows cell by cell (all lanes the same cell,
+//     from a per-warp shared-memory ring filled by cp.async) against its TE tile cells.
+//   * Screen: per split a binary32 lower bound of the binary64 total from the children's
+//     round-down shadows (6 FMA/ALU instructions, no FP64); per output (slot ring: outputs
+//     slide by one cell per step) the minimum bound is compared with the output's filter
+//     F(min) = float_ru(min (1 + 2^-40)); the bound never exceeds the total by more than
+//     2^-43, so winners and ties always pass (derivation: DESIGN.md §6; checked against the
+//     oracle by tests/test_filter_bound.py).
+//   * Exact path: passing outputs are queued per warp and re-evaluated in binary64 in the
+//     oracle's operation order, one output per lane, merged as the lexicographic minimum of
+//     (total, key) with a 128-bit CAS into the CTA's accumulator (exact under any
+//     interleaving: the key l1<<20 | j<<10 | s is monotone in the oracle's (k, m, s) order,
+//     so the lexicographic minimum is the oracle's first strict minimum).
+//   * End: the CTA merges its improved entries into the range's global accumulator; the
+//     range's co-resident CTAs then finalize the winners' cells in shares; extra blocks of
+//     the launch compute the next wave's in-node cells and seeds.  Single-profile sets
+//     pipeline the waves (programmatic dependent launches + per-wave counters).
 //
-// k_fin — per wavefront: the winners of the W(q >= 2) cells of wave l, and every cell
-// inside one node (I(r), W(1)) of wave l+1 (those depend only on shorter cells inside a
-// node), a group of threads per cell with a lexicographic argmin reduction.
+// k_fin — per wavefront (unfused / sharded modes and wave 2): the winners of the W(q >= 2)
+// cells of wave l, the in-node cells (I(r), W(1)) of wave l+1 and the seeds of wave l+1.
 #pragma once
 
 #include "oob_dp_common.cuh"
