@@ -286,6 +286,10 @@ __device__ __forceinline__ float split_lb(float TA, float TB, float TS, float TC
 //   w = accumulator entry | E' << 13 | ncell << 20 | LT << 23 | rl << 24,
 //   v = the stage count the key does not carry (LT: rs, else S0).
 constexpr int XQ_CAP = 32;
+#ifndef OOB_XQ_PREFETCH
+#define OOB_XQ_PREFETCH 0   // L1 prefetch of the queued children: measured slower (cfg4 +2%)
+#endif
+constexpr bool XQ_PREFETCH = OOB_XQ_PREFETCH;
 constexpr int XQ_BYTES = XQ_CAP * 24;     // per warp
 
 // Exact evaluation of the queued outputs (warp-collective; lane i takes entry i): every
@@ -382,6 +386,13 @@ __device__ __noinline__ int xq_push(unsigned mask, int base, unsigned bidx, int 
                                   (unsigned)(idx0 + Ep) | ((unsigned)Ep << 13) | ((unsigned)ncell << 20) |
                                       (LT ? 1u << 23 : 0u) | ((unsigned)rl << 24));
             q1[slot] = LT ? (unsigned)rs : (unsigned)S0;
+            if (XQ_PREFETCH) {   // warm L1 with the children the flush will load
+                const Cell4 *tp = CELL + bidx, *sp = CELL + srow + max(0, Ep - (TE - 1));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(tp));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(tp + TE - 1));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(sp));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(sp + TE - 1));
+            }
         }
         count += n;
     }
