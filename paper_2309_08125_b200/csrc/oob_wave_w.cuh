@@ -638,7 +638,9 @@ __device__ __forceinline__ void fin_w_one(const DevGeom &g, const FinArgs &f, in
 // (accumulator loads; child loads; recompute + store) so their memory latencies overlap.
 template <int NT>
 __device__ __forceinline__ void fin_w_range(const DevGeom &g, const FinArgs &f, int pr, int tid, int part = 0,
-                                            int nparts = 1) {
+                                            int nparts = 1, const ulonglong2 *sacc = nullptr) {
+    // sacc: the range's accumulator in this CTA's shared memory (the range's only CTA); the
+    // global entries are then only reset
     constexpr int FB = 4;
     const int l = f.lw, nout = f.nout_w, M = g.M;
     const int u = pr % f.nranges_w, p = pr / f.nranges_w;
@@ -664,7 +666,7 @@ __device__ __forceinline__ void fin_w_range(const DevGeom &g, const FinArgs &f, 
             Sp[j] = lo + (i - (d_wofs(g, l, lo) - d_wofs(g, l, 1)));
             if (lo < 2) continue;
             ulonglong2 *ga = f.GACC + (int64_t)pr * nout + i;
-            a[j] = __ldcg(ga);
+            a[j] = sacc ? sacc[i] : __ldcg(ga);
             __stcg(ga, make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull));
             __stcg(f.GFW + (int64_t)pr * nout + i, FILT_EMPTY);
         }
@@ -1132,6 +1134,11 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
     // merge into the range's global accumulator (L2-coherent loads; a stale value is an
     // upper bound of the current one, so the CAS loop stays exact).  Loads are batched so
     // their latencies overlap.
+    if (w.cpr == 1 && w.fin_inline && w.world == 1) {   // the range's only CTA: finalize from shared memory
+        fin_w_range<NTW>(g, w.fw, pr, tid, 0, 1, acc);
+        pipe_signal(w.pp, L, 2, l);
+        return;
+    }
     ulonglong2 *ga = w.GACC + ((size_t)p * w.nranges + u) * nout;
     constexpr int MB = 4;
     for (int i0 = tid; i0 < nout; i0 += MB * NTW) {
