@@ -138,7 +138,15 @@ void oob_template_set_free(oob_template_set *s);
  *       {int32 nodes, S, kstar, status; double T1, T2, T3, tstar, iter}
  *     followed by L records {int32 layer_begin, layer_end, gpus, node, gpu_offset};
  *     stride info.packed_template_bytes, profile stride info.packed_profile_bytes.
- * Kernels are enqueued on `stream`; the call returns without synchronizing. */
+ * Kernels are enqueued on `stream`; the call returns without synchronizing.  The W-cell
+ * kernel screens splits with a binary32 round-down lower bound and re-evaluates every
+ * candidate in binary64 (never drops a winner or a tie).  For a single
+ * profile the wavefront kernels are programmatic dependent launches that synchronise
+ * through counters in the workspace (they may overlap each other, never the caller's
+ * other work on `stream`: the last kernel, the template extraction, waits for all of
+ * them); the workspace must not be shared by concurrent runs.  Diagnostic environment
+ * switches read at oob_dp_plan_create (OOB_DP_PIPE=0, OOB_DP_FUSE=0, OOB_DP_WCFG, ...)
+ * select equivalent variants with identical results. */
 typedef struct {
     int32_t L, M, n_lo, n_hi, num_profiles, wavefronts;
     int64_t cells_per_profile;      /* DP cells in the table universe */
