@@ -241,6 +241,7 @@ struct oob_dp_plan {
     int chunk_max = 192;                 // OOB_DP_CHMAX: streamed cells per unit (upper bound)
     int aux_first = 0;                   // OOB_DP_AUXFIRST: extra blocks first in k_wave_w's grid
     int refresh = 1;                     // OOB_DP_REFRESH=0: no per-unit filter refresh
+    double shard_min = SHARD_MIN_SPLITS; // OOB_DP_SHARDMIN: wavefronts with fewer splits run redundantly
     int pipe = 1;                        // OOB_DP_PIPE=0: plain kernel boundaries between wavefronts
     size_t pipe_cnt_off = 0;             // ints into the counter region: [3][L+2] + error word
     size_t geom_bytes = 0, ws_bytes = 0, tpl_bytes = 0;
@@ -399,6 +400,7 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     if (const char *cm = std::getenv("OOB_DP_CHMAX")) pl->chunk_max = std::max(12, std::atoi(cm));
     if (const char *af = std::getenv("OOB_DP_AUXFIRST")) pl->aux_first = std::atoi(af) != 0;
     if (const char *rf = std::getenv("OOB_DP_REFRESH")) pl->refresh = std::atoi(rf) != 0;
+    if (const char *sm = std::getenv("OOB_DP_SHARDMIN")) pl->shard_min = std::atof(sm);
     if (const char *pp = std::getenv("OOB_DP_PIPE")) pl->pipe = std::atoi(pp) != 0;
     for (int ci = 0; ci < NWCFG; ++ci) build_tiles(pl, WCFGS[ci].te);
     pl->stream_steps.assign(L + 1, 0.0);
@@ -575,7 +577,7 @@ static int64_t count_launches(const oob_dp_plan *pl) {
     int64_t n = 3;
     for (int l = 2; l <= G.L; ++l) {
         const WaveHost &wh = pl->waves[l];
-        const bool shard = pl->world > 1 && (double)G.wave_splits[l] * pl->P >= SHARD_MIN_SPLITS;
+        const bool shard = pl->world > 1 && (double)G.wave_splits[l] * pl->P >= pl->shard_min;
         const bool has = wh.nents > 0;
         n += has ? (wh.seed_units > 0 ? 2 : 1) : 0;
         n += (pl->fuse_fin && has && !shard && wh.seed_units == 0) ? 0 : 1;
@@ -806,7 +808,7 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
         w.tiles = (const int32_t *)(ws + pl->off_tiles);
         // shard only wavefronts whose work outweighs the all-gather (~10-20 us on NVLink);
         // short wavefronts run redundantly on every rank (identical results, no exchange)
-        const bool shard = pl->world > 1 && (double)G.wave_splits[l] * pl->P >= SHARD_MIN_SPLITS;
+        const bool shard = pl->world > 1 && (double)G.wave_splits[l] * pl->P >= pl->shard_min;
         w.rank = shard ? pl->rank : 0;
         w.world = shard ? pl->world : 1;
         const int64_t ctas = wh.nents > 0 ? (int64_t)pl->P * w.nranges * w.cpr : 0;
