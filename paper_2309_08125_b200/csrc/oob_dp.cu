@@ -357,7 +357,8 @@ static void build_wave(oob_dp_plan *pl, int l, int ci, int slots, WaveHost &wh, 
     // + upre[L+4] + ents[nents] (16 B)
     const size_t nent = (size_t)(wh.nout + g.L + 2 * TE + 2);
     const size_t before_ring = nent * 16 + (nent + 3) / 4 * 16 + (size_t)wh.nents * 16 + (size_t)(g.L + 2) * 8 +
-                               (size_t)(g.L + 1) * 4 + (size_t)(g.L + 2) * 4 + (size_t)(g.L + 4) * 4;
+                               (size_t)(g.L + 1) * 4 + (size_t)(g.L + 2) * 4 + (size_t)(g.L + 4) * 4 +
+                               2 * (size_t)(g.L + 1) * 4;   // + tile list offsets / counts
     wh.smem = before_ring + 32 + (size_t)(NTW / 32) * (XR_BYTES + XQ_BYTES);   // + per-warp rings and queues
     wh.cost = total * ranges;
 }

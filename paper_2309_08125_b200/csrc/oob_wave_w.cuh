@@ -987,8 +987,10 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
     int *scells = reinterpret_cast<int *>(sbase + L + 2);        // [L+1]
     int *outOff = scells + (L + 1);                              // [L+2] W(q) offsets (nout: none)
     int *upre = outOff + (L + 2);                                // [nents + 1]
-    // per-warp streamed-side rings (16 B aligned) after upre
-    const size_t ring_off = ((size_t)(reinterpret_cast<unsigned char *>(upre + w.nents + 1) - smem) + 15) & ~(size_t)15;
+    int *stoff = upre + w.nents + 1;                             // [L+1] tile list offsets
+    int *stcnt = stoff + (L + 1);                                // [L+1] tile counts
+    // per-warp streamed-side rings (16 B aligned) after the tile tables
+    const size_t ring_off = ((size_t)(reinterpret_cast<unsigned char *>(stcnt + L + 1) - smem) + 15) & ~(size_t)15;
     float4 *rings = reinterpret_cast<float4 *>(smem + ring_off);
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -1029,6 +1031,10 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
                 filt[i] = fv[j];
             }
         }
+    }
+    for (int i = tid; i <= L; i += NTW) {
+        stoff[i] = w.tile_off[i];
+        stcnt[i] = w.tile_cnt[i];
     }
     for (int i = tid; i < L + 2; i += NTW) {
         sbase[i] = g.base[i];
@@ -1082,8 +1088,8 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
         const int us = ltiled ? k : u;                             // small slab start
         const int ub = ltiled ? u : k;
         const int ti = blk * 32 + (w.rev_lanes ? 31 - lane : lane);
-        const bool has = ti < w.tile_cnt[lb];
-        const int32_t code = has ? w.tiles[w.tile_off[lb] + ti] : 0;
+        const bool has = ti < stcnt[lb];
+        const int32_t code = has ? w.tiles[stoff[lb] + ti] : 0;
         const int rowB = has ? (code >> 16) : 1;
         const int e0 = has ? (code & 0xFFFF) : 0;
         const int wb0 = has ? d_wofs(g, lb, rowB) : 0;
@@ -1105,8 +1111,8 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
         }
         if (w.refresh) {   // refresh the filter of the outputs this unit can touch (rows q = rowB + rs) from the
             // range's global filter: minima other CTAs found since this CTA last looked
-            const int tb0 = blk * 32, tb1 = min(blk * 32 + 31, w.tile_cnt[lb] - 1);
-            const int rmin = w.tiles[w.tile_off[lb] + tb0] >> 16, rmax = w.tiles[w.tile_off[lb] + tb1] >> 16;
+            const int tb0 = blk * 32, tb1 = min(blk * 32 + 31, stcnt[lb] - 1);
+            const int rmin = w.tiles[stoff[lb] + tb0] >> 16, rmax = w.tiles[stoff[lb] + tb1] >> 16;
             const int olo = outOff[min(rmin + r_lo, L + 1)], ohi = outOff[min(rmax + r_hi, L + 1)];
             for (int i0 = olo + lane; i0 < ohi; i0 += 128) {   // 4 loads in flight per lane
                 unsigned gv[4];
