@@ -358,7 +358,7 @@ static void build_wave(oob_dp_plan *pl, int l, int ci, int slots, WaveHost &wh, 
     const size_t nent = (size_t)(wh.nout + g.L + 2 * TE + 2);
     const size_t before_ring = nent * 16 + (nent + 3) / 4 * 16 + (size_t)wh.nents * 16 + (size_t)(g.L + 2) * 8 +
                                (size_t)(g.L + 1) * 4 + (size_t)(g.L + 2) * 4 + (size_t)(g.L + 4) * 4 +
-                               2 * (size_t)(g.L + 1) * 4;   // + tile list offsets / counts
+                               2 * (size_t)(g.L + 1) * 4 + wh.cb.size() * 4;   // + tile tables, chunk bounds
     wh.smem = before_ring + 32 + (size_t)(NTW / 32) * (XR_BYTES + XQ_BYTES);   // + per-warp rings and queues
     wh.cost = total * ranges;
 }
@@ -800,6 +800,7 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
         w.ents = (const int4 *)(ws + pl->off_items + wh.ents_off);
         w.upre = (const int32_t *)(ws + pl->off_items + wh.upre_off);
         w.cb = (const int32_t *)(ws + pl->off_items + wh.cb_off);
+        w.ncb = (int)wh.cb.size();
         w.ctr = (int *)(ws + pl->off_CTR) + wh.ctr_off;
         w.nout = wh.nout;
         w.GACC = gacc_of(pl, gacc, l);

@@ -70,6 +70,7 @@ struct WaveW {
     const int4 *ents;      // per entry: (l1, nblocks, nchunks, chunk_off)
     const int32_t *upre;   // [nents + 1] unit prefix: entry e owns units [upre[e], upre[e+1])
     const int32_t *cb;     // chunk row boundaries: rows [cb[off+c], cb[off+c+1])
+    int ncb;               // entries of cb (staged in shared memory)
     int *ctr;              // [P][nranges] unit counters of this pass (zeroed before the launch)
     int unit_lo, unit_hi;  // this pass processes queue units [unit_lo, unit_hi)
     int seeded;            // 1: start from the global accumulator (an earlier pass's minima)
@@ -989,8 +990,9 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
     int *upre = outOff + (L + 2);                                // [nents + 1]
     int *stoff = upre + w.nents + 1;                             // [L+1] tile list offsets
     int *stcnt = stoff + (L + 1);                                // [L+1] tile counts
-    // per-warp streamed-side rings (16 B aligned) after the tile tables
-    const size_t ring_off = ((size_t)(reinterpret_cast<unsigned char *>(stcnt + L + 1) - smem) + 15) & ~(size_t)15;
+    int *scb = stcnt + (L + 1);                                  // [ncb] chunk row boundaries
+    // per-warp streamed-side rings (16 B aligned) after the tables
+    const size_t ring_off = ((size_t)(reinterpret_cast<unsigned char *>(scb + w.ncb) - smem) + 15) & ~(size_t)15;
     float4 *rings = reinterpret_cast<float4 *>(smem + ring_off);
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -1036,6 +1038,7 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
         stoff[i] = w.tile_off[i];
         stcnt[i] = w.tile_cnt[i];
     }
+    for (int i = tid; i < w.ncb; i += NTW) scb[i] = w.cb[i];
     for (int i = tid; i < L + 2; i += NTW) {
         sbase[i] = g.base[i];
         if (i <= L) scells[i] = g.cells[i];
@@ -1069,7 +1072,7 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
         const int local = un - upre[ei];
         const int chunk = local / en.y;
         const int blk = local % en.y;
-        const int r_lo = w.cb[en.w + chunk], r_hi = w.cb[en.w + chunk + 1];
+        const int r_lo = scb[en.w + chunk], r_hi = scb[en.w + chunk + 1];
         const int k = u + l1;
         const int l2 = l - l1;
         if (w.pp.on) {                                           // both children's waves ready?
