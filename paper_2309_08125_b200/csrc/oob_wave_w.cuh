@@ -1098,6 +1098,13 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
         const int wb0 = has ? d_wofs(g, lb, rowB) : 0;
         const int lenB = has ? d_wofs(g, lb, rowB + 1) - wb0 : 0;
         const int ncell = max(0, min(TE, lenB - e0));             // valid cells of the tile
+        // the streamed chunk's first batches are in flight while the tile and the filter load
+        const int64_t sidx = pc + sbase[ls] + (int64_t)us * scells[ls] + d_wofs(g, ls, r_lo);
+        unsigned char *wsm = reinterpret_cast<unsigned char *>(rings) + (size_t)(tid >> 5) * (XR_BYTES + XQ_BYTES);
+        uint4 *q4 = reinterpret_cast<uint4 *>(wsm + XR_BYTES);         // this warp's candidate queue
+        unsigned *q1 = reinterpret_cast<unsigned *>(q4 + XQ_CAP);
+        XRing xr;                                            // rows r_lo.. are contiguous
+        xr_start(xr, reinterpret_cast<float4 *>(wsm), g.SH + sidx, lane);
         // register tile: shadow lower bounds of TE big-side cells (+inf beyond the row: every
         // bound of a sentinel is +inf and never passes)
         const int64_t bidx = pc + sbase[lb] + (int64_t)ub * scells[lb] + (has ? wb0 : d_wofs(g, lb, 1)) + e0;
@@ -1126,12 +1133,6 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
                     if (gv[j] < filt[i0 + 32 * j]) atomicMin(filt + i0 + 32 * j, gv[j]);
             }
         }
-        const int64_t sidx = pc + sbase[ls] + (int64_t)us * scells[ls] + d_wofs(g, ls, r_lo);
-        unsigned char *wsm = reinterpret_cast<unsigned char *>(rings) + (size_t)(tid >> 5) * (XR_BYTES + XQ_BYTES);
-        uint4 *q4 = reinterpret_cast<uint4 *>(wsm + XR_BYTES);         // this warp's candidate queue
-        unsigned *q1 = reinterpret_cast<unsigned *>(q4 + XQ_CAP);
-        XRing xr;                                            // rows r_lo.. are contiguous
-        xr_start(xr, reinterpret_cast<float4 *>(wsm), g.SH + sidx, lane);
         if (ltiled)
             run_rows<TE, true>(xr, sidx, g.wofs + ls * (L + 2), r_lo, r_hi, TA, TB, TS, TC, bidx, ncell, rowB, e0, l1, L, outOff, nout,
                                acc_s, filt_s, gfilt, q4, q1, g.CELL);
