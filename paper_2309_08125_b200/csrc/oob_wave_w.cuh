@@ -216,9 +216,18 @@ __device__ __forceinline__ float filt_of(unsigned long long bits) {
 // mirrored after its end, so the TE cells a block of steps reads are contiguous (one base
 // address per block, immediate offsets).  Copies are unguarded: a chunk's last batches may
 // read past the slab (the SH allocation is padded by XR_CELLS cells).
-constexpr int XR_CELLS = 128;
-constexpr int XR_BATCH = 32;
-constexpr int XR_AHEAD = 2;
+#ifndef OOB_XR_BATCH
+#define OOB_XR_BATCH 32
+#endif
+#ifndef OOB_XR_AHEAD
+#define OOB_XR_AHEAD 2
+#endif
+constexpr int XR_BATCH = OOB_XR_BATCH;                  // cells per copy batch (<= 32: one 16-B copy per lane)
+constexpr int XR_AHEAD = OOB_XR_AHEAD;                  // batches in flight ahead of the steps
+constexpr int xr_pow2(int x) { return x <= 1 ? 1 : 2 * xr_pow2((x + 1) / 2); }
+constexpr int XR_CELLS = xr_pow2(XR_BATCH * (XR_AHEAD + 2));   // ring: >= the batch in use, the previous one
+                                                                // and XR_AHEAD in flight (power of two)
+static_assert(XR_BATCH <= 32 && (XR_BATCH & (XR_BATCH - 1)) == 0, "one 16-B copy per lane per batch");
 constexpr int XR_MIRROR = 8;
 constexpr int XR_BYTES = (XR_CELLS + XR_MIRROR) * 16;   // per warp
 
@@ -234,6 +243,7 @@ __device__ __forceinline__ void xr_issue(XRing &r) {
     const int b = r.nb_iss++;
     const unsigned pos = (unsigned)((b * XR_BATCH) & (XR_CELLS - 1)) * 16u;
     const char *g = r.src + (size_t)b * (XR_BATCH * 16);
+    if (XR_BATCH == 32 || (threadIdx.x & 31) < XR_BATCH)
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(r.ring_s + pos), "l"(g) : "memory");
     if (pos == 0 && r.mirror)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(r.ring_s + XR_CELLS * 16u), "l"(g) : "memory");
