@@ -242,6 +242,7 @@ struct oob_dp_plan {
     int aux_first = 0;                   // OOB_DP_AUXFIRST: extra blocks first in k_wave_w's grid
     int refresh = 1;                     // OOB_DP_REFRESH=0: no per-unit filter refresh
     double shard_min = SHARD_MIN_SPLITS; // OOB_DP_SHARDMIN: wavefronts with fewer splits run redundantly
+    int seed_min_l = SEED_MIN_L;         // OOB_DP_SEEDMINL: first seeded wavefront
     int pipe = 1;                        // OOB_DP_PIPE=0: plain kernel boundaries between wavefronts
     size_t pipe_cnt_off = 0;             // ints into the counter region: [3][L+2] + error word
     size_t geom_bytes = 0, ws_bytes = 0, tpl_bytes = 0;
@@ -402,6 +403,7 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     if (const char *af = std::getenv("OOB_DP_AUXFIRST")) pl->aux_first = std::atoi(af) != 0;
     if (const char *rf = std::getenv("OOB_DP_REFRESH")) pl->refresh = std::atoi(rf) != 0;
     if (const char *sm = std::getenv("OOB_DP_SHARDMIN")) pl->shard_min = std::atof(sm);
+    if (const char *sl = std::getenv("OOB_DP_SEEDMINL")) pl->seed_min_l = std::max(3, std::atoi(sl));
     if (const char *pp = std::getenv("OOB_DP_PIPE")) pl->pipe = std::atoi(pp) != 0;
     for (int ci = 0; ci < NWCFG; ++ci) build_tiles(pl, WCFGS[ci].te);
     pl->stream_steps.assign(L + 1, 0.0);
@@ -455,7 +457,7 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
             int64_t wout = 0;
             for (int q = 2; q <= std::min(Q_of(g, l), l); ++q) wout += wlen_h(g, l, q);
             const double spo = wout ? (double)g.wave_splits[l] / ((double)(L - l + 1) * wout) : 0.0;
-            wh.seed = pl->seed_init && l >= SEED_MIN_L && spo >= pl->seed_spo;
+            wh.seed = pl->seed_init && l >= pl->seed_min_l && spo >= pl->seed_spo;
         }
         wh.ctr_off = ctr_total;
         ctr_total += 2 * (size_t)num_profiles * (L - l + 1);
