@@ -823,6 +823,9 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
         w.nbmain = (int)ctas;
         w.aux_first = pl->aux_first;
         w.refresh = pl->refresh && wh.cpr > 1;   // one CTA per range: its own filter is current
+        // batched sweeps (one CTA per range, small shared memory, a larger L1): the exact
+        // path's children are worth warming in L1 (cfg5 -2%; neutral to negative for cfg4)
+        w.prefetch = wh.cpr == 1 && pl->P > 1;
         w.fin_inline = fused ? 1 : 0;
         w.rdone = (int *)(ws + pl->off_CTR) + wh.done_off;
         w.rclaim = w.rdone + (size_t)pl->P * w.nranges;

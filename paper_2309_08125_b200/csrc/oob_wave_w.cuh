@@ -93,6 +93,7 @@ struct WaveW {
     int *rclaim;               // [P][nranges] finalize shares claimed
     Pipe pp;                   // wavefront pipeline (pp.on = 0: plain kernel boundaries)
     int refresh;               // 1: each unit refreshes its filter entries from the range's global filter
+    int prefetch;              // 1: each unit prefetches its tile and chunk cells into L1 (one CTA per range)
     FinArgs fa, fw;
 };
 
@@ -1115,6 +1116,14 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
         unsigned *q1 = reinterpret_cast<unsigned *>(q4 + XQ_CAP);
         XRing xr;                                            // rows r_lo.. are contiguous
         xr_start(xr, reinterpret_cast<float4 *>(wsm), g.SH + sidx, lane);
+        if (w.prefetch) {   // warm L1 with the binary64 cells the exact path may load
+            const Cell4 *tp = g.CELL + pc + sbase[lb] + (int64_t)ub * scells[lb] + (has ? d_wofs(g, lb, rowB) : 0) + e0;
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(tp));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(tp + TE - 1));
+            const Cell4 *sp0 = g.CELL + sidx + lane * 8;       // 32 lanes x 256 B covers a 256-cell chunk
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(sp0));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(sp0 + 4));
+        }
         // register tile: shadow lower bounds of TE big-side cells (+inf beyond the row: every
         // bound of a sentinel is +inf and never passes)
         const int64_t bidx = pc + sbase[lb] + (int64_t)ub * scells[lb] + (has ? wb0 : d_wofs(g, lb, 1)) + e0;
