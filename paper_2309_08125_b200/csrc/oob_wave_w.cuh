@@ -562,9 +562,6 @@ __device__ __forceinline__ void run_rows(XRing &xr, int64_t sidx, const int32_t 
 #endif
         }
         // tail block (rl % TE steps) and the pending outputs E' = rl .. rl + TE - 2
-        if (__any_sync(0xFFFFFFFFu, pmask != 0))
-            qn = xq_push<TE, LT>(pmask, mbase, (unsigned)bidx, ncell, (unsigned)srow, rl, S0, rs, kb, idx0, q4, q1, qn,
-                                 CELL, acc_s, filt_s, gfr);
         {
             xr_ensure(xr, rb + blk + TE);
             const float4 *xq = xr_at(xr, rb + blk);
@@ -586,6 +583,14 @@ __device__ __forceinline__ void run_rows(XRing &xr, int64_t sidx, const int32_t 
                 case 3: pm |= pending_mask<TE, 3>(mn, fr + rl); break;
                 default: pm |= pending_mask<TE, 4>(mn, fr + rl); break;
             }
+            // the row's last window and its tail / pending outputs in one push when they fit
+            if (blk - mbase + 2 * TE - 3 <= 31) {
+                pmask |= pm << (blk - mbase);
+                pm = 0;
+            }
+            if (__any_sync(0xFFFFFFFFu, pmask != 0))
+                qn = xq_push<TE, LT>(pmask, mbase, (unsigned)bidx, ncell, (unsigned)srow, rl, S0, rs, kb, idx0, q4, q1,
+                                     qn, CELL, acc_s, filt_s, gfr);
             if (__any_sync(0xFFFFFFFFu, pm != 0))
                 qn = xq_push<TE, LT>(pm, blk, (unsigned)bidx, ncell, (unsigned)srow, rl, S0, rs, kb, idx0, q4, q1, qn,
                                      CELL, acc_s, filt_s, gfr);
