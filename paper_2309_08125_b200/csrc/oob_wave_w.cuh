@@ -98,18 +98,6 @@ struct WaveW {
 };
 
 __device__ __forceinline__ int L_of(const DevGeom &g) { return g.L; }
-__device__ __forceinline__ int d_wcells(const DevGeom &g, int l) {
-    return g.cells[l] - g.off[l * g.A + (g.M - 1)];
-}
-// offset of W(q) inside the W-part of a slab of length l (-1 if absent)
-__device__ __forceinline__ int d_woff(const DevGeom &g, int l, int q) {
-    const int o = g.off[l * g.A + (g.M - 1) + q - 1];
-    return o < 0 ? -1 : o - g.off[l * g.A + (g.M - 1)];
-}
-__device__ __forceinline__ int d_wlen(const DevGeom &g, int l, int q) {
-    const int hi = min(l, q * g.M);
-    return hi >= q ? hi - q + 1 : 0;
-}
 
 // One split with operands in left / right roles (DESIGN.md §2 arithmetic contract):
 //   T1 = L.T1 + R.T1; left = L.t* >= R.t*; T3 = left ? L.T3 + R.T1 : R.T3;
@@ -157,22 +145,7 @@ __device__ __forceinline__ bool lex_less(unsigned long long b, uint32_t key, uns
     return b < A || (b == A && key < K);
 }
 
-// Lexicographic-min merge of (total bits b, key) into the shared accumulator entry at addr.
-__device__ __forceinline__ void acc_merge_shared(unsigned addr, unsigned long long b, uint32_t key) {
-    unsigned long long cx, cy;
-    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(cx), "=l"(cy) : "r"(addr) : "memory");
-    while (lex_less(b, key, cx, (uint32_t)cy)) {
-        unsigned long long ox, oy;
-        cas128_shared(addr, ox, oy, cx, cy, b, (unsigned long long)key);
-        if (ox == cx && oy == cy) return;
-        cx = ox;
-        cy = oy;
-    }
-}
-
 // ---------------------------------------------------------------- closed-form slab geometry
-// W rows of a slab of length l: row q (1 <= q <= min(Q_l, l)) holds S' = q..min(l, Mq).
-__device__ __forceinline__ int c_wlen(int M, int l, int q) { return min(l, M * q) - q + 1; }
 // offset of row q inside the W part of the slab
 __device__ __forceinline__ int c_woff(int M, int l, int q) {
     const int a = min(q - 1, l / M);            // rows q' < q with M q' <= l
