@@ -144,9 +144,16 @@ void oob_template_set_free(oob_template_set *s);
  * profile the wavefront kernels are programmatic dependent launches that synchronise
  * through counters in the workspace (they may overlap each other, never the caller's
  * other work on `stream`: the last kernel, the template extraction, waits for all of
- * them); the workspace must not be shared by concurrent runs.  Diagnostic environment
- * switches read at oob_dp_plan_create (OOB_DP_PIPE=0, OOB_DP_FUSE=0, OOB_DP_WCFG, ...)
- * select equivalent variants with identical results. */
+ * them); the workspace must not be shared by concurrent runs.  Its contents need not
+ * persist between runs: every run re-initialises the accumulators and counters it uses,
+ * and the plan's read-only index geometry lives in plan-owned device memory (allocated and
+ * uploaded on the first run on each device, freed by oob_dp_plan_free).  A plan is sized
+ * for the SM count of the device current at oob_dp_plan_create; running it on a device
+ * with another SM count returns OOB_E_INVALID.  A timed-out pipeline wait (a GPU shared
+ * with other work) marks the packed templates (status 2): oob_template_set_from_packed
+ * then returns OOB_E_CUDA.  Diagnostic environment switches read at oob_dp_plan_create
+ * (OOB_DP_PIPE=0, OOB_DP_FUSE=0, OOB_DP_KERNEL=v1, ...) select equivalent variants with
+ * identical results; the effective ones are reported in oob_dp_info. */
 typedef struct {
     int32_t L, M, n_lo, n_hi, num_profiles, wavefronts;
     int64_t cells_per_profile;      /* DP cells in the table universe */
@@ -154,6 +161,15 @@ typedef struct {
     int64_t kernel_launches;        /* device kernels launched per oob_dp_run */
     size_t workspace_bytes;
     size_t packed_template_bytes, packed_profile_bytes, packed_bytes;
+    /* effective plan switches (identical results in every combination) */
+    int32_t kernel;                 /* 2 = tiled W-cell kernel, 1 = thread-per-cell fallback */
+    int32_t pipelined;              /* wavefronts as programmatic dependent launches */
+    int32_t fused;                  /* finalize + next wave's in-node cells inside k_wave_w */
+    int32_t seeded;                 /* wavefronts whose accumulators start from seed splits */
+    int32_t chunk_max, refresh, small_pairs;
+    int32_t num_sms;                /* SMs of the device the plan was built for */
+    int32_t world;                  /* ranks sharing the wavefronts (oob_dp_set_comm) */
+    int32_t reserved;
 } oob_dp_info;
 
 oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int32_t n_hi,

@@ -51,7 +51,9 @@ class OobDpInfo(ctypes.Structure):
                 ("cells_per_profile", c_int64), ("splits_per_profile", c_int64),
                 ("kernel_launches", c_int64), ("workspace_bytes", c_size_t),
                 ("packed_template_bytes", c_size_t), ("packed_profile_bytes", c_size_t),
-                ("packed_bytes", c_size_t)]
+                ("packed_bytes", c_size_t), ("kernel", c_int32), ("pipelined", c_int32),
+                ("fused", c_int32), ("seeded", c_int32), ("chunk_max", c_int32), ("refresh", c_int32),
+                ("small_pairs", c_int32), ("num_sms", c_int32), ("world", c_int32), ("reserved", c_int32)]
 
 
 def _proto(name, res, args):

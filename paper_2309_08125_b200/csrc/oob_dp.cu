@@ -109,10 +109,15 @@ __global__ void k_wave_v1(DevGeom g, int l) {
 // One thread per (profile, template size n): argmin over S (strict <, smaller S wins),
 // then the split-tree backtrack (left child first => stages in pipeline order).
 __global__ void k_extract(DevGeom g, unsigned char *packed, size_t tpl_bytes, Pipe pp) {
-    if (pp.on) {                      // the pipelined waves' last cells (and, by monotonicity, all)
-        if (threadIdx.x == 0) pipe_wait(pp, g.L, g.L, 6);
-        __syncthreads();
+    __shared__ int s_err;
+    if (threadIdx.x == 0) {
+        s_err = 0;
+        if (pp.on) {                  // the pipelined waves' last cells (and, by monotonicity, all)
+            pipe_wait(pp, g.L, g.L, 6);
+            s_err = *(volatile int *)pp.err;   // a timed-out wait: the table may be wrong
+        }
     }
+    __syncthreads();
     const int p_cnt = g.n_hi - g.n_lo + 1;
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= p_cnt * g.P) return;
@@ -133,7 +138,8 @@ __global__ void k_extract(DevGeom g, unsigned char *packed, size_t tpl_bytes, Pi
         if (bestS < 0 || tot < best) { best = tot; bestS = S; }
     }
     const Cell4 c = d_load(g.CELL + pc + d_cell(g, bestS, 0, L, aW));
-    h->nodes = n; h->S = bestS; h->kstar = (int)d_kd(c.C1, bestS); h->status = 0;
+    h->nodes = n; h->S = bestS; h->kstar = (int)d_kd(c.C1, bestS);
+    h->status = s_err ? 2 : 0;        // 2: pipeline wait timed out (OOB_E_CUDA on the host)
     h->T1 = c.T1; h->T3 = c.T3; h->tstar = c.TS;
     h->T2 = __dmul_rn(c.C1, c.TS);
     h->iter = best;
@@ -163,7 +169,7 @@ __global__ void k_extract(DevGeom g, unsigned char *packed, size_t tpl_bytes, Pi
         const int s = (int)(arg >> 20);
         if (arg >= 0xFFFFFFFDu || k <= u || k >= v || s < 1 || s >= Sp || j >= d_num_dsplits(g, a) ||
             top + 2 > L + 1) {   // corrupt split (never for a valid table): flag the template, stop
-            h->status = 1;
+            h->status = h->status ? h->status : 1;
             break;
         }
         int a1, a2;
@@ -187,25 +193,59 @@ using namespace oob;
 
 namespace {
 
-// k_wave_w launch configurations: (TE cells per lane tile, threads per CTA)
-struct WCfg { int te, nt; };
-constexpr WCfg WCFGS[] = {{4, NTW}, {5, NTW}, {3, NTW}, {2, NTW}};
+constexpr int TE_W = 4;                    // k_wave_w register tile: TE cells per lane
 constexpr double SHARD_MIN_SPLITS = 2e7;   // wavefronts sharded across ranks (oob_dp_set_comm)
-constexpr int SEED_MIN_L = 6;      // waves seeded with proportional splits (k_fin)
+constexpr int SEED_MIN_L = 6;              // waves seeded with proportional splits (k_fin)
 constexpr int CTAS_PER_SM = WAVE_CTAS_PER_SM;   // k_wave_w: resident CTAs per SM (register bound; smem may allow fewer)
-constexpr int NWCFG = 4;
+
+// Plan-time switches (read once at oob_dp_plan_create; every OOB_DP_* variable is part of
+// the plan-cache key of oob_generate_templates).  All select variants with identical
+// results; the effective values are reported by oob_dp_plan_info (oob_dp_info.switches).
+struct Knobs {
+    int kernel = 2;            // OOB_DP_KERNEL=v1: thread-per-cell reference kernel (1)
+    int fuse_fin = 1;          // OOB_DP_FUSE=0: separate k_fin launch per wave
+    int pipe = 1;              // OOB_DP_PIPE=0: plain kernel boundaries between wavefronts
+    int seed_init = 1;         // OOB_DP_SEEDINIT=0: no proportional-split seeds
+    double seed_spo = 0.0;     // OOB_DP_SEEDSPO: seed waves with >= this many splits per W output
+    int seed_min_l = SEED_MIN_L;   // OOB_DP_SEEDMINL: first seeded wavefront
+    int small_pairs = 1;       // OOB_DP_SMALLPAIRS: layer splits per thread of an in-node cell
+    int chunk_max = 192;       // OOB_DP_CHMAX: streamed cells per unit (upper bound)
+    int units_per_cta = 0;     // OOB_DP_UPC: minimum queue units per CTA (chunk size)
+    int refresh = 1;           // OOB_DP_REFRESH=0: no per-unit filter refresh
+    double shard_min = SHARD_MIN_SPLITS;   // OOB_DP_SHARDMIN: waves with fewer splits run redundantly
+    long long spin_max = 1ll << 24;        // OOB_DP_PIPE_SPIN: polls before a pipeline wait times out
+    int debug = 0;             // OOB_DP_DEBUG: per-wave plan on stderr
+};
+
+Knobs read_knobs() {
+    Knobs k;
+    auto env = [](const char *n) { return std::getenv(n); };
+    if (const char *v = env("OOB_DP_KERNEL")) k.kernel = std::string(v) == "v1" ? 1 : 2;
+    if (const char *v = env("OOB_DP_FUSE")) k.fuse_fin = std::atoi(v) != 0;
+    if (const char *v = env("OOB_DP_PIPE")) k.pipe = std::atoi(v) != 0;
+    if (const char *v = env("OOB_DP_SEEDINIT")) k.seed_init = std::atoi(v) != 0;
+    if (const char *v = env("OOB_DP_SEEDSPO")) k.seed_spo = std::atof(v);
+    if (const char *v = env("OOB_DP_SEEDMINL")) k.seed_min_l = std::max(3, std::atoi(v));
+    if (const char *v = env("OOB_DP_SMALLPAIRS")) k.small_pairs = std::max(1, std::atoi(v));
+    if (const char *v = env("OOB_DP_CHMAX")) k.chunk_max = std::max(12, std::atoi(v));
+    if (const char *v = env("OOB_DP_UPC")) k.units_per_cta = std::max(0, std::atoi(v));
+    if (const char *v = env("OOB_DP_REFRESH")) k.refresh = std::atoi(v) != 0;
+    if (const char *v = env("OOB_DP_SHARDMIN")) k.shard_min = std::atof(v);
+    if (const char *v = env("OOB_DP_PIPE_SPIN")) k.spin_max = std::max(0ll, std::atoll(v));
+    if (env("OOB_DP_DEBUG")) k.debug = 1;
+    return k;
+}
 
 struct WaveHost {
-    int cfg = 0;                   // index into WCFGS
     int nents = 0, nunits = 0, nout = 0, cpr = 1;
-    size_t ents_off = 0, upre_off = 0, cb_off = 0;   // byte offsets in the blob's items region
+    size_t ents_off = 0, upre_off = 0, cb_off = 0;   // byte offsets in the geometry's items region
     std::vector<int32_t> ents;     // 4 ints per entry: (l1, nblocks, nchunks, chunk_off)
     std::vector<int32_t> upre;     // unit prefix per entry [nents + 1]
     std::vector<int32_t> cb;       // chunk row boundaries
     size_t smem = 0;
-    size_t ctr_off = 0;            // first unit counter of this wave (ints; two passes)
+    size_t ctr_off = 0;            // first unit counter of this wave (ints)
     size_t done_off = 0;           // per-range finished-CTA counters (fused finalize)
-    int seed_units = 0;            // units of the seeding pass (balanced splits), 0 = one pass
+    int max_row = 0;               // longest streamed W row (queue entry fields)
     int nsmall = 0;                // cells inside one node with S' >= 2 per range
     bool seed = false;             // accumulator seeded by k_fin (proportional + warm-start splits)
     double cost = 0.0;             // modelled issue cycles of the wave (all ranges, profiles)
@@ -218,37 +258,31 @@ int wlen_h(const Geometry &g, int l, int q) {
 }
 int wcells_h(const Geometry &g, int l) { return g.cells[l] - g.off[(size_t)l * g.A + (g.M - 1)]; }
 
-struct TileTab {
-    std::vector<int32_t> off, cnt;           // [L+1] flat tile list of a big side of length lb
-};
+// SMs of the current device (148 on B200; the CPU build box has no device)
+int device_sms() {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
+        return n;
+    cudaGetLastError();   // clear the sticky "no device" error of the query
+    return 148;
+}
 
 }  // namespace
 
 struct oob_dp_plan {
     Geometry g;
     int32_t P = 1;
+    Knobs kn;
     int kernel = 2;                      // 1 = v1 (thread per cell), 2 = tiled W kernel
-    int force_cfg = -1;
-    int units_per_cta = 0;               // OOB_DP_UPC: minimum queue units per CTA (chunk size)
-    int auto_cfgs = 2;                   // OOB_DP_AUTOCFGS: WCFGS entries the wave model chooses from
-    int seed_pass = 0;                   // OOB_DP_SEED=1 enables the seeding pass
-    int seed_init = 1;                   // OOB_DP_SEEDINIT=0: no proportional-split seeds
-    double seed_spo = 0.0;               // OOB_DP_SEEDSPO: seed waves with >= this many splits per W output
-    int small_pairs = 1;                 // OOB_DP_SMALLPAIRS: layer splits per thread of a small cell
-    int fuse_fin = 1;                    // OOB_DP_FUSE=0: separate k_fin launch per wave
-    int perm_order = 0;                  // OOB_DP_PERM=1: pseudo-random unit order
-    int rev_lanes = 0;                   // OOB_DP_REV=1: reversed lane <-> tile order
-    int chunk_max = 192;                 // OOB_DP_CHMAX: streamed cells per unit (upper bound)
-    int aux_first = 0;                   // OOB_DP_AUXFIRST: extra blocks first in k_wave_w's grid
-    int refresh = 1;                     // OOB_DP_REFRESH=0: no per-unit filter refresh
-    double shard_min = SHARD_MIN_SPLITS; // OOB_DP_SHARDMIN: wavefronts with fewer splits run redundantly
-    int seed_min_l = SEED_MIN_L;         // OOB_DP_SEEDMINL: first seeded wavefront
-    int pipe = 1;                        // OOB_DP_PIPE=0: plain kernel boundaries between wavefronts
+    int num_sms = 148;                   // SMs the wave grids were sized for
+    bool pipe_on = false;                // pipelined wavefronts (single-profile, unsharded)
     size_t pipe_cnt_off = 0;             // ints into the counter region: [3][L+2] + error word
     size_t geom_bytes = 0, ws_bytes = 0, tpl_bytes = 0;
-    std::vector<unsigned char> geom_blob;   // host image of the geometry region
-    size_t off_cells = 0, off_base = 0, off_off = 0, off_wofs = 0, off_pexp = 0, off_tiles = 0, off_tile_off = 0, off_tile_cnt = 0,
-           off_items = 0;
+    std::vector<unsigned char> geom_blob;   // host image of the device geometry (read-only)
+    std::vector<std::pair<int, void *>> dev_geom;   // plan-owned device copies, per device
+    size_t off_cells = 0, off_base = 0, off_off = 0, off_wofs = 0, off_pexp = 0, off_tiles = 0, off_tile_off = 0,
+           off_tile_cnt = 0, off_items = 0;
     size_t off_CELL = 0, off_SH = 0, off_ARG = 0, off_STK = 0, off_GACC = 0, off_GFILT = 0, off_CTR = 0;
     int64_t gacc_n = 0;
     void *comm = nullptr;                // ncclComm_t (single-profile sharding), world > 1
@@ -256,14 +290,11 @@ struct oob_dp_plan {
     size_t off_GPART = 0;                // [world][wave partial] gathered partial accumulators
     size_t ws_bytes_base = 0;
     size_t ctr_n = 0;
-    std::vector<int32_t> tiles;          // all TE's tables concatenated
-    TileTab tab[NWCFG];                  // per WCFGS entry (TE = 4, 5, 3, 2)
+    std::vector<int32_t> tiles;          // flat tile lists of TE_W cells
+    std::vector<int32_t> tile_off, tile_cnt;   // [L+1]
     std::vector<double> stream_steps;    // [L+1] cost-model steps of streaming a slab of length ls
     std::vector<WaveHost> waves;         // [L+1]
     size_t max_smem = 0;
-    int64_t launches = 0;
-    void *uploaded_to = nullptr;
-    void *gacc_ready = nullptr;
     int timing = 0;
     std::vector<cudaEvent_t> ev;
     int ev_used = 0;
@@ -277,36 +308,32 @@ static oob_status cuda_fail(cudaError_t e, const char *what) {
     return fail(OOB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-static int te_index(int te) { return te == 4 ? 0 : te == 5 ? 1 : te == 3 ? 2 : 3; }
-
 // Flat tile lists: for a big side of length lb, its W rows j = 1..min(Q, lb) cut into
 // ceil(len/TE) tiles of TE consecutive cells, in row order; 32 consecutive tiles form one
 // warp work unit of k_wave_w.
-static void build_tiles(oob_dp_plan *pl, int TE) {
+static void build_tiles(oob_dp_plan *pl) {
     const Geometry &g = pl->g;
-    TileTab &T = pl->tab[te_index(TE)];
-    T.off.assign(g.L + 1, 0);
-    T.cnt.assign(g.L + 1, 0);
+    pl->tile_off.assign(g.L + 1, 0);
+    pl->tile_cnt.assign(g.L + 1, 0);
     for (int lb = 1; lb <= g.L; ++lb) {
         const int J = std::min(Q_of(g, lb), lb);
-        T.off[lb] = (int32_t)pl->tiles.size();
+        pl->tile_off[lb] = (int32_t)pl->tiles.size();
         for (int j = 1; j <= J; ++j) {
             const int len = wlen_h(g, lb, j);
-            for (int e0 = 0; e0 < len; e0 += TE) pl->tiles.push_back((j << 16) | e0);
+            for (int e0 = 0; e0 < len; e0 += TE_W) pl->tiles.push_back((j << 16) | e0);
         }
-        T.cnt[lb] = (int32_t)pl->tiles.size() - T.off[lb];
+        pl->tile_cnt[lb] = (int32_t)pl->tiles.size() - pl->tile_off[lb];
     }
 }
 
-// Issue-cycle model of one k restricted to small-side rows [it_lo, it_hi): every unit
-// (32 lanes) walks its rows; a step costs TE splits (~20 instructions each) plus the load
-// and the merge (~24).
-static double k_cost(const oob_dp_plan *pl, int TE, int l, int l1, bool lt) {
+// Issue-cycle model of one k: every unit (32 lanes) walks its rows; a step costs TE splits
+// (~20 instructions each) plus the load and the merge (~24).
+static double k_cost(const oob_dp_plan *pl, int l, int l1, bool lt) {
     const int l2 = l - l1;
     const int ls = lt ? l2 : l1, lb = lt ? l1 : l2;       // streamed side, tiled side
     const double steps = pl->stream_steps[ls];             // rows + per-row tail/flush/setup
-    const double units = (pl->tab[te_index(TE)].cnt[lb] + 31) / 32;
-    return units * (steps * (TE * 20.0 + 24.0) + 400.0);
+    const double units = (pl->tile_cnt[lb] + 31) / 32;
+    return units * (steps * (TE_W * 20.0 + 24.0) + 400.0);
 }
 
 // Unit queue of wavefront l (identical for every range and profile): one entry per layer
@@ -314,9 +341,8 @@ static double k_cost(const oob_dp_plan *pl, int TE, int l, int l1, bool lt) {
 // totals early; an entry's small-side rows are cut into chunks of ~CH steps; a warp unit is
 // (entry, chunk, block of 32 big-side tiles).  `slots` = resident CTAs of the GPU: ranges
 // get several CTAs (sharing the range's queue) when there are fewer ranges than slots.
-static void build_wave(oob_dp_plan *pl, int l, int ci, int slots, WaveHost &wh, int CH = 96) {
+static void build_wave(oob_dp_plan *pl, int l, int slots, WaveHost &wh, int CH) {
     const Geometry &g = pl->g;
-    const int TE = WCFGS[ci].te;
     const int nr = g.L - l + 1;
     std::vector<int> order;
     for (int l1 = 1; l1 < l; ++l1) order.push_back(l1);
@@ -324,23 +350,25 @@ static void build_wave(oob_dp_plan *pl, int l, int ci, int slots, WaveHost &wh, 
     wh.ents.clear();
     wh.upre.assign(1, 0);
     wh.cb.clear();
+    wh.max_row = 0;
     double total = 0.0;
     for (int l1 : order) {
         const int l2 = l - l1;
         // tile the left child (stream the right) or the reverse, whichever the model finds
         // cheaper: tiling the bigger side fills the 32 lanes, streaming the longer rows cuts
         // the per-row overhead
-        const double cl = k_cost(pl, TE, l, l1, true), cr = k_cost(pl, TE, l, l1, false);
+        const double cl = k_cost(pl, l, l1, true), cr = k_cost(pl, l, l1, false);
         const bool lt = cl <= cr;
         const int ls = lt ? l2 : l1, lb = lt ? l1 : l2;
         const int JS = std::min(Q_of(g, ls), ls);
-        const int nblocks = (pl->tab[te_index(TE)].cnt[lb] + 31) / 32;
+        const int nblocks = (pl->tile_cnt[lb] + 31) / 32;
         const int coff = (int)wh.cb.size();
         int nchunks = 0, acc = 0, last = -1;
         for (int r = 1; r <= JS; ++r) {
             const int c = acc / CH;
             if (c != last) { wh.cb.push_back(r); ++nchunks; last = c; }
             acc += wlen_h(g, ls, r);
+            wh.max_row = std::max(wh.max_row, wlen_h(g, ls, r));
         }
         wh.cb.push_back(JS + 1);
         if (nchunks == 0 || nblocks == 0) { wh.cb.resize(coff); continue; }
@@ -348,7 +376,6 @@ static void build_wave(oob_dp_plan *pl, int l, int ci, int slots, WaveHost &wh, 
         wh.upre.push_back(wh.upre.back() + nblocks * nchunks);
         total += std::min(cl, cr);
     }
-    wh.cfg = ci;
     wh.nents = (int)wh.ents.size() / 4;
     wh.nunits = wh.upre.back();
     wh.nout = wcells_h(g, l);
@@ -356,7 +383,7 @@ static void build_wave(oob_dp_plan *pl, int l, int ci, int slots, WaveHost &wh, 
     wh.cpr = std::max(1, std::min(wh.nunits / 8, slots / std::max(1, ranges)));
     // acc[nout + dummy] (16 B) + filter (4 B) + base[L+2] (8 B) + cells[L+1] + outOff[L+2]
     // + upre[L+4] + ents[nents] (16 B)
-    const size_t nent = (size_t)(wh.nout + g.L + 2 * TE + 2);
+    const size_t nent = (size_t)(wh.nout + g.L + 2 * TE_W + 2);
     const size_t before_ring = nent * 16 + (nent + 3) / 4 * 16 + (size_t)wh.nents * 16 + (size_t)(g.L + 2) * 8 +
                                (size_t)(g.L + 1) * 4 + (size_t)(g.L + 2) * 4 + (size_t)(g.L + 4) * 4 +
                                2 * (size_t)(g.L + 1) * 4 + wh.cb.size() * 4;   // + tile tables, chunk bounds
@@ -378,6 +405,19 @@ static int small_tpc(const Geometry &g, int l, int per) {
     return t;
 }
 
+// Pipelined wavefronts (k_wave_w as programmatic dependent launches synchronised by
+// counters): only the fused single-pass, unsharded W kernel, and only when every wave's main
+// grid fits the resident CTA slots (a single profile); batched sweeps have far more CTAs
+// than slots and gain nothing from the overlap.
+static bool plan_pipe_on(const oob_dp_plan *pl) {
+    const Geometry &G = pl->g;
+    bool on = pl->kn.pipe && pl->kernel == 2 && pl->world == 1 && pl->kn.fuse_fin;
+    for (int l = 2; l <= G.L && on; ++l)
+        on = pl->waves[l].nents > 0 &&
+             (int64_t)pl->P * (G.L - l + 1) * pl->waves[l].cpr <= (int64_t)CTAS_PER_SM * pl->num_sms;
+    return on;
+}
+
 extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int32_t n_hi,
                                          int32_t num_profiles, oob_dp_plan **out) {
     if (!out) return fail(OOB_E_INVALID, "oob_dp_plan_create: out is NULL");
@@ -386,26 +426,12 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     if (!pl) return fail(OOB_E_NOMEM, "oob_dp_plan_create: out of memory");
     if (!build_geometry(L, M, n_lo, n_hi, pl->g)) { delete pl; return OOB_E_INVALID; }
     pl->P = num_profiles;
+    pl->kn = read_knobs();
+    pl->kernel = pl->kn.kernel;
+    pl->num_sms = device_sms();
     const Geometry &g = pl->g;
-    const char *kv = std::getenv("OOB_DP_KERNEL");
-    pl->kernel = (kv && std::string(kv) == "v1") ? 1 : 2;
-    if (const char *fc = std::getenv("OOB_DP_WCFG")) pl->force_cfg = std::atoi(fc);
-    if (const char *up = std::getenv("OOB_DP_UPC")) pl->units_per_cta = std::max(0, std::atoi(up));
-    if (const char *ac = std::getenv("OOB_DP_AUTOCFGS")) pl->auto_cfgs = std::max(1, std::min(NWCFG, std::atoi(ac)));
-    if (const char *sp = std::getenv("OOB_DP_SEED")) pl->seed_pass = std::atoi(sp) != 0;
-    if (const char *si = std::getenv("OOB_DP_SEEDINIT")) pl->seed_init = std::atoi(si) != 0;
-    if (const char *ss = std::getenv("OOB_DP_SEEDSPO")) pl->seed_spo = std::atof(ss);
-    if (const char *sp2 = std::getenv("OOB_DP_SMALLPAIRS")) pl->small_pairs = std::max(1, std::atoi(sp2));
-    if (const char *fu = std::getenv("OOB_DP_FUSE")) pl->fuse_fin = std::atoi(fu) != 0;
-    if (const char *po = std::getenv("OOB_DP_PERM")) pl->perm_order = std::atoi(po) != 0;
-    if (const char *rv = std::getenv("OOB_DP_REV")) pl->rev_lanes = std::atoi(rv) != 0;
-    if (const char *cm = std::getenv("OOB_DP_CHMAX")) pl->chunk_max = std::max(12, std::atoi(cm));
-    if (const char *af = std::getenv("OOB_DP_AUXFIRST")) pl->aux_first = std::atoi(af) != 0;
-    if (const char *rf = std::getenv("OOB_DP_REFRESH")) pl->refresh = std::atoi(rf) != 0;
-    if (const char *sm = std::getenv("OOB_DP_SHARDMIN")) pl->shard_min = std::atof(sm);
-    if (const char *sl = std::getenv("OOB_DP_SEEDMINL")) pl->seed_min_l = std::max(3, std::atoi(sl));
-    if (const char *pp = std::getenv("OOB_DP_PIPE")) pl->pipe = std::atoi(pp) != 0;
-    for (int ci = 0; ci < NWCFG; ++ci) build_tiles(pl, WCFGS[ci].te);
+    const int SMS = pl->num_sms;
+    build_tiles(pl);
     pl->stream_steps.assign(L + 1, 0.0);
     for (int ls = 1; ls <= L; ++ls) {
         const int JS = std::min(Q_of(pl->g, ls), ls);
@@ -413,37 +439,27 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     }
     pl->waves.assign(L + 1, WaveHost());
     size_t items_total = 0, gacc_max = 0, ctr_total = 0;
+    bool fits = true;                    // queue-entry fields and shared memory of k_wave_w
     for (int l = 2; l <= L; ++l) {
-        WaveHost best;
-        double best_t = 1e300;
-        for (int ci = 0; ci < NWCFG; ++ci) {
-            if (pl->force_cfg >= 0 ? ci != pl->force_cfg : ci >= pl->auto_cfgs) continue;
-            WaveHost wh;
-            // smaller chunks (more, shorter units) until every warp slot has ~4 units and every
-            // CTA has >= units_per_cta units of its range's queue (short tails per CTA)
-            // resident CTAs per SM: launch bounds (registers), then shared memory
-            int per_sm = CTAS_PER_SM;
-            for (int pass = 0; pass < 2; ++pass) {
-                for (int CH = pl->chunk_max;; CH /= 2) {
-                    build_wave(pl, l, ci, per_sm * 148, wh, CH);
-                    if (CH <= 12 || ((int64_t)wh.nunits * num_profiles * (L - l + 1) >= 4LL * per_sm * 148 * (NTW / 32) &&
-                                     wh.nunits >= pl->units_per_cta * wh.cpr))
-                        break;
-                }
-                const int by_smem = std::max<int>(1, (int)((228 * 1024) / (std::max<size_t>(wh.smem, 1) + 1024)));
-                const int ps = std::max(1, std::min(CTAS_PER_SM, by_smem));
-                if (ps == per_sm) break;
-                per_sm = ps;
-            }
-            const double warps_per_smsp = per_sm * (NTW / 32) / 4.0;
-            // issue efficiency saturates at ~4 resident warps per scheduler; TE = 5 (larger
-            // code, measured slower on B200) is kept as a forced option (OOB_DP_WCFG=1)
-            const double eff = std::min(1.0, warps_per_smsp / 4.0) * (WCFGS[ci].te == 5 ? 0.7 : 1.0);
-            const double t = wh.cost / (4.0 * 148.0 * eff);
-            if (t < best_t) { best_t = t; best = wh; }
-        }
-        pl->waves[l] = best;
         WaveHost &wh = pl->waves[l];
+        // smaller chunks (more, shorter units) until every warp slot has ~4 units and every
+        // CTA has >= units_per_cta units of its range's queue (short tails per CTA);
+        // resident CTAs per SM: launch bounds (registers), then shared memory
+        int per_sm = CTAS_PER_SM;
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int CH = pl->kn.chunk_max;; CH /= 2) {
+                build_wave(pl, l, per_sm * SMS, wh, CH);
+                if (CH <= 12 || ((int64_t)wh.nunits * num_profiles * (L - l + 1) >= 4LL * per_sm * SMS * (NTW / 32) &&
+                                 wh.nunits >= pl->kn.units_per_cta * wh.cpr))
+                    break;
+            }
+            const int by_smem = std::max<int>(1, (int)((228 * 1024) / (std::max<size_t>(wh.smem, 1) + 1024)));
+            const int ps = std::max(1, std::min(CTAS_PER_SM, by_smem));
+            if (ps == per_sm) break;
+            per_sm = ps;
+        }
+        // queue entries carry the accumulator entry in 16 bits and E', rl in 11 bits each
+        if (wh.nout + L + 2 * TE_W + 2 > 0xFFFF || wh.max_row + TE_W > 2047) fits = false;
         wh.ents_off = items_total;
         items_total += align_up(wh.ents.size() * sizeof(int32_t), 16);
         wh.upre_off = items_total;
@@ -457,46 +473,42 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
             int64_t wout = 0;
             for (int q = 2; q <= std::min(Q_of(g, l), l); ++q) wout += wlen_h(g, l, q);
             const double spo = wout ? (double)g.wave_splits[l] / ((double)(L - l + 1) * wout) : 0.0;
-            wh.seed = pl->seed_init && l >= pl->seed_min_l && spo >= pl->seed_spo;
+            wh.seed = pl->kn.seed_init && l >= pl->kn.seed_min_l && spo >= pl->kn.seed_spo;
         }
         wh.ctr_off = ctr_total;
-        ctr_total += 2 * (size_t)num_profiles * (L - l + 1);
+        ctr_total += (size_t)num_profiles * (L - l + 1);
         wh.done_off = ctr_total;
         ctr_total += 2 * (size_t)num_profiles * (L - l + 1);   // merged CTAs, claimed finalize shares
-        // seeding pass: the balanced entries' units (~4% of the wave) fill the global
-        // accumulator first, so that the main pass's flush filter rarely passes
-        wh.seed_units = 0;
-        if (l >= 24 && pl->seed_pass) {
-            const int target = std::max(1, wh.nunits / 25);
-            for (int e = 0; e < wh.nents && wh.seed_units < target; ++e) wh.seed_units = wh.upre[e + 1];
-            if (wh.seed_units >= wh.nunits) wh.seed_units = 0;
-        }
         pl->max_smem = std::max(pl->max_smem, wh.smem);
     }
     pl->pipe_cnt_off = ctr_total;
     ctr_total += 3 * (size_t)(L + 2) + 1;
     pl->ctr_n = ctr_total;
-    if (pl->max_smem > 227 * 1024) pl->kernel = 1;
-    if (std::getenv("OOB_DP_DEBUG")) {
+    if (pl->max_smem > 227 * 1024 || !fits) pl->kernel = 1;
+    pl->pipe_on = plan_pipe_on(pl);
+    if (pl->kn.debug) {
         for (int l = 2; l <= L; ++l) {
             const WaveHost &wh = pl->waves[l];
-            std::fprintf(stderr, "l=%d cfg=%d (TE=%d) ents=%d units=%d cpr=%d ctas=%lld smem=%zu cost=%.3g\n", l,
-                         wh.cfg, WCFGS[wh.cfg].te, wh.nents, wh.nunits, wh.cpr,
-                         (long long)wh.cpr * (L - l + 1) * num_profiles, wh.smem, wh.cost);
+            std::fprintf(stderr, "l=%d ents=%d units=%d cpr=%d ctas=%lld smem=%zu cost=%.3g seed=%d\n", l, wh.nents,
+                         wh.nunits, wh.cpr, (long long)wh.cpr * (L - l + 1) * num_profiles, wh.smem, wh.cost,
+                         (int)wh.seed);
         }
     }
 
+    // plan-owned device geometry (read-only): uploaded once per device by oob_dp_run
     size_t o = 0;
     pl->off_cells = o; o = align_up(o + sizeof(int32_t) * (L + 1), 256);
     pl->off_base = o;  o = align_up(o + sizeof(int64_t) * (L + 2), 256);
     pl->off_off = o;   o = align_up(o + sizeof(int32_t) * (size_t)(L + 1) * g.A, 256);
     pl->off_wofs = o;  o = align_up(o + sizeof(int32_t) * (size_t)(L + 1) * (L + 2), 256);
     pl->off_pexp = o;  o = align_up(o + sizeof(int32_t) * 3 * (size_t)(L + 2), 256);
-    pl->off_tiles = o; o = align_up(o + sizeof(int32_t) * pl->tiles.size(), 256);
-    pl->off_tile_off = o; o = align_up(o + sizeof(int32_t) * (L + 1) * NWCFG, 256);
-    pl->off_tile_cnt = o; o = align_up(o + sizeof(int32_t) * (L + 1) * NWCFG, 256);
+    pl->off_tiles = o; o = align_up(o + sizeof(int32_t) * std::max<size_t>(1, pl->tiles.size()), 256);
+    pl->off_tile_off = o; o = align_up(o + sizeof(int32_t) * (L + 1), 256);
+    pl->off_tile_cnt = o; o = align_up(o + sizeof(int32_t) * (L + 1), 256);
     pl->off_items = o;    o = align_up(o + items_total, 256);
     pl->geom_bytes = o;
+    // caller-owned workspace: tables, accumulators, counters (re-initialised every run)
+    o = 0;
     const size_t n = (size_t)g.table_cells * num_profiles;
     pl->off_CELL = o; o = align_up(o + 32 * (n + 16 + XR_CELLS), 256);   // + padding: row streams read ahead
     pl->off_SH = o; o = align_up(o + 16 * (n + 16 + XR_CELLS), 256);     // shadow lower bounds (+ padding)
@@ -522,7 +534,7 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
             if (l >= 3) {                       // produced by launch l-1's extra blocks
                 const int64_t nsd = wh.seed ? (int64_t)num_profiles * nr * wh.nout : 0;
                 ex[l] = (int32_t)((nsd + 255) / 256);
-                const int tpc = small_tpc(g, l, pl->small_pairs);
+                const int tpc = small_tpc(g, l, pl->kn.small_pairs);
                 const int64_t ns = (int64_t)num_profiles * nr * small_cells(g, l);
                 ex[(L + 2) + l] = (int32_t)((ns + (256 / tpc) - 1) / (256 / tpc));
             }
@@ -543,10 +555,8 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
         }
     }
     if (!pl->tiles.empty()) std::memcpy(b + pl->off_tiles, pl->tiles.data(), sizeof(int32_t) * pl->tiles.size());
-    for (int ti = 0; ti < NWCFG; ++ti) {
-        std::memcpy(b + pl->off_tile_off + sizeof(int32_t) * (L + 1) * ti, pl->tab[ti].off.data(), sizeof(int32_t) * (L + 1));
-        std::memcpy(b + pl->off_tile_cnt + sizeof(int32_t) * (L + 1) * ti, pl->tab[ti].cnt.data(), sizeof(int32_t) * (L + 1));
-    }
+    std::memcpy(b + pl->off_tile_off, pl->tile_off.data(), sizeof(int32_t) * (L + 1));
+    std::memcpy(b + pl->off_tile_cnt, pl->tile_cnt.data(), sizeof(int32_t) * (L + 1));
     for (int l = 2; l <= L; ++l) {
         const WaveHost &wh = pl->waves[l];
         if (!wh.ents.empty())
@@ -560,30 +570,61 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     return OOB_OK;
 }
 
-void oob::dp_plan_invalidate(oob_dp_plan *pl) {
-    pl->uploaded_to = nullptr;
-    pl->gacc_ready = nullptr;
-}
-
 extern "C" void oob_dp_plan_free(oob_dp_plan *pl) {
     if (!pl) return;
     for (auto e : pl->ev) cudaEventDestroy(e);
+    for (auto &dg : pl->dev_geom) {
+        int cur = 0;
+        if (cudaGetDevice(&cur) == cudaSuccess && cudaSetDevice(dg.first) == cudaSuccess) {
+            cudaFree(dg.second);
+            cudaSetDevice(cur);
+        }
+    }
     delete pl;
 }
 
-// Kernels one oob_dp_run enqueues (k_gacc_init only on a workspace's first run): k_base,
-// k_fin(in-node cells of wave 2), per wave k_wave_w (+ seeding pass) and, unless fused,
-// k_fin; k_extract.  v1: k_base, one kernel per wave, k_extract.
+// The plan's read-only device geometry on the current device (uploaded on first use).
+static oob_status plan_geometry(oob_dp_plan *pl, unsigned char **geo) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    for (auto &dg : pl->dev_geom)
+        if (dg.first == dev) { *geo = (unsigned char *)dg.second; return OOB_OK; }
+    int sms = 0;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    if (sms != pl->num_sms)
+        return fail(OOB_E_INVALID, "oob_dp_run: the plan was built for a device with " + std::to_string(pl->num_sms) +
+                                       " SMs, the current device has " + std::to_string(sms) +
+                                       " (create the plan with that device current)");
+    void *p = nullptr;
+    e = cudaMalloc(&p, pl->geom_bytes);
+    if (e != cudaSuccess) return fail(OOB_E_NOMEM, std::string("cudaMalloc plan geometry: ") + cudaGetErrorString(e));
+    e = cudaMemcpy(p, pl->geom_blob.data(), pl->geom_bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { cudaFree(p); return cuda_fail(e, "plan geometry upload"); }
+    if (pl->kernel == 2) {
+        const int sm = (int)std::max<size_t>(pl->max_smem, 48 * 1024);
+        e = cudaFuncSetAttribute(k_wave_w<TE_W>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        if (e != cudaSuccess) { cudaFree(p); return cuda_fail(e, "cudaFuncSetAttribute(k_wave_w)"); }
+    }
+    pl->dev_geom.emplace_back(dev, p);
+    *geo = (unsigned char *)p;
+    return OOB_OK;
+}
+
+// Kernels one oob_dp_run enqueues: k_init (accumulators + counters), k_base, k_fin
+// (in-node cells of wave 2), per wave k_wave_w and, unless fused, k_fin; k_extract.
+// v1: k_init, k_base, one kernel per wave, k_extract.
 static int64_t count_launches(const oob_dp_plan *pl) {
     const Geometry &G = pl->g;
-    if (pl->kernel == 1) return 2 + (G.L - 1);
-    int64_t n = 3;
+    if (pl->kernel == 1) return 3 + (G.L - 1);
+    int64_t n = 4;
     for (int l = 2; l <= G.L; ++l) {
         const WaveHost &wh = pl->waves[l];
-        const bool shard = pl->world > 1 && (double)G.wave_splits[l] * pl->P >= pl->shard_min;
+        const bool shard = pl->world > 1 && (double)G.wave_splits[l] * pl->P >= pl->kn.shard_min;
         const bool has = wh.nents > 0;
-        n += has ? (wh.seed_units > 0 ? 2 : 1) : 0;
-        n += (pl->fuse_fin && has && !shard && wh.seed_units == 0) ? 0 : 1;
+        n += has ? 1 : 0;
+        n += (pl->kn.fuse_fin && has && !shard) ? 0 : 1;
     }
     return n;
 }
@@ -601,6 +642,17 @@ extern "C" oob_status oob_dp_plan_info(const oob_dp_plan *pl, oob_dp_info *out) 
     out->packed_template_bytes = pl->tpl_bytes;
     out->packed_profile_bytes = pl->tpl_bytes * (size_t)(g.n_hi - g.n_lo + 1);
     out->packed_bytes = out->packed_profile_bytes * pl->P;
+    out->kernel = pl->kernel;
+    out->pipelined = pl->pipe_on ? 1 : 0;
+    out->fused = (pl->kernel == 2 && pl->kn.fuse_fin) ? 1 : 0;
+    out->seeded = 0;
+    for (int l = 2; l <= g.L; ++l) out->seeded += pl->waves[l].seed ? 1 : 0;
+    out->chunk_max = pl->kn.chunk_max;
+    out->refresh = pl->kn.refresh;
+    out->small_pairs = pl->kn.small_pairs;
+    out->num_sms = pl->num_sms;
+    out->world = pl->world;
+    out->reserved = 0;
     return OOB_OK;
 }
 
@@ -614,6 +666,7 @@ extern "C" oob_status oob_dp_set_comm(oob_dp_plan *pl, void *comm, int32_t world
     pl->rank = world > 1 ? rank : 0;
     pl->off_GPART = pl->ws_bytes_base;
     pl->ws_bytes = pl->ws_bytes_base + (world > 1 ? align_up(16 * (size_t)world * pl->gacc_n, 256) : 0);
+    pl->pipe_on = plan_pipe_on(pl);
     return OOB_OK;
 }
 
@@ -648,13 +701,12 @@ extern "C" oob_status oob_dp_kernel_time(oob_dp_plan *pl, double *ms_out, int64_
     return OOB_OK;
 }
 
-// k_fin: W winners of wave lw (lw >= 2, else none) + small cells of wave ls (0: none).
-// accumulator of wave l: two parity buffers (k_fin finalizes wave l-1 from one while it
-// seeds wave l into the other)
+// accumulator of wave l: three buffers (wave mod 3): k_fin / the fused finalize reads wave
+// l-1's while the seeds of wave l+1 fill another
 static ulonglong2 *gacc_of(const oob_dp_plan *pl, ulonglong2 *gacc, int l) {
     return gacc + (size_t)(l % 3) * (size_t)pl->gacc_n;
 }
-// global filter of wave l's accumulator (same parity and index)
+// global filter of wave l's accumulator (same buffer and index)
 static unsigned *gfilt_of(const oob_dp_plan *pl, ulonglong2 *gacc, int l) {
     return (unsigned *)((unsigned char *)gacc - pl->off_GACC + pl->off_GFILT) + (size_t)(l % 3) * (size_t)pl->gacc_n;
 }
@@ -662,8 +714,8 @@ static unsigned *gfilt_of(const oob_dp_plan *pl, ulonglong2 *gacc, int l) {
 // Finalize arguments for wave lw (0: none) and in-node cells + seeds of wave ls (0: none);
 // *nbsmall receives the blocks of the small-cell part.
 static FinArgs make_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglong2 *gacc, int lw, int ls, bool sharded,
-                        int64_t *nbsmall, int lsd = -1) {
-    if (lsd < 0) lsd = ls;                 // seeds of wave lsd (pipelined waves: two waves ahead)
+                        int64_t *nbsmall) {
+    const int lsd = ls;                 // seeds of the same wave as the in-node cells
     const Geometry &G = pl->g;
     FinArgs f;
     f.lw = lw;
@@ -685,7 +737,7 @@ static FinArgs make_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglong2 *ga
     f.GFS = gfilt_of(pl, gacc, lsd);
     f.ls = ls;
     f.nsmall = ls ? small_cells(G, ls) : 0;
-    f.tpc = ls ? small_tpc(G, ls, pl->small_pairs) : 32;
+    f.tpc = ls ? small_tpc(G, ls, pl->kn.small_pairs) : 32;
     const int64_t ns = ls ? (int64_t)pl->P * (G.L - ls + 1) * f.nsmall : 0;
     *nbsmall = (ns + (256 / f.tpc) - 1) / (256 / f.tpc);
     return f;
@@ -709,37 +761,32 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
     cudaStream_t stream = (cudaStream_t)stream_;
     const Geometry &G = pl->g;
     unsigned char *ws = (unsigned char *)d_ws;
+    unsigned char *geo = nullptr;
+    oob_status gs = plan_geometry(pl, &geo);
+    if (gs != OOB_OK) return gs;
     cudaError_t e;
-    if (pl->uploaded_to != d_ws) {
-        e = cudaMemcpyAsync(ws, pl->geom_blob.data(), pl->geom_bytes, cudaMemcpyHostToDevice, stream);
-        if (e != cudaSuccess) return cuda_fail(e, "geometry upload");
-        e = cudaStreamSynchronize(stream);
-        if (e != cudaSuccess) return cuda_fail(e, "geometry upload sync");
-        pl->uploaded_to = d_ws;
-        if (pl->kernel == 2) {
-            const int sm = (int)std::max<size_t>(pl->max_smem, 48 * 1024);
-            e = cudaFuncSetAttribute(k_wave_w<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-            if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(k_wave_w<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-            if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(k_wave_w<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-            if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(k_wave_w<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(k_wave_w)");
-        }
-    }
     DevGeom dg;
     dg.L = G.L; dg.M = G.M; dg.n_lo = G.n_lo; dg.n_hi = G.n_hi; dg.A = G.A; dg.P = pl->P;
     dg.C = G.table_cells;
-    dg.cells = (const int32_t *)(ws + pl->off_cells);
-    dg.base = (const int64_t *)(ws + pl->off_base);
-    dg.off = (const int32_t *)(ws + pl->off_off);
-    dg.wofs = (const int32_t *)(ws + pl->off_wofs);
+    dg.cells = (const int32_t *)(geo + pl->off_cells);
+    dg.base = (const int64_t *)(geo + pl->off_base);
+    dg.off = (const int32_t *)(geo + pl->off_off);
+    dg.wofs = (const int32_t *)(geo + pl->off_wofs);
     dg.CELL = (Cell4 *)(ws + pl->off_CELL);
     dg.SH = (float4 *)(ws + pl->off_SH);
     dg.ARG = (uint32_t *)(ws + pl->off_ARG);
     dg.STK = (uint64_t *)(ws + pl->off_STK);
 
+    ulonglong2 *gacc = (ulonglong2 *)(ws + pl->off_GACC);
+    int *ctr = (int *)(ws + pl->off_CTR);
+    {   // every run starts from a clean workspace state: accumulators, filters, counters
+        const int64_t nacc = pl->kernel == 2 ? 3 * pl->gacc_n : 0;
+        const int64_t nmax = std::max<int64_t>(nacc, (int64_t)pl->ctr_n + 1);
+        k_init<<<(unsigned)((nmax + 255) / 256), 256, 0, stream>>>(gacc, gfilt_of(pl, gacc, 0), nacc, ctr,
+                                                                  (int64_t)pl->ctr_n + 1);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "k_init launch");
+    }
     {   // K_base: grid.y = l
         int64_t maxn = (int64_t)G.L * G.M * pl->P;
         dim3 grid((unsigned)((maxn + 255) / 256), (unsigned)G.L);
@@ -756,32 +803,15 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
             pl->ev.push_back(ev);
         }
     }
-    ulonglong2 *gacc = (ulonglong2 *)(ws + pl->off_GACC);
-    // pipelined wavefronts: only the fused single-pass, unsharded W kernel
-    bool pipe_on = pl->pipe && pl->kernel == 2 && pl->world == 1 && pl->fuse_fin;
-    // ... and only when every wave's main grid fits the resident CTA slots (a single profile):
-    // batched sweeps have far more CTAs than slots and gain nothing from the overlap
-    for (int l = 2; l <= G.L && pipe_on; ++l)
-        pipe_on = pl->waves[l].nents > 0 && pl->waves[l].seed_units == 0 &&
-                  (int64_t)pl->P * (G.L - l + 1) * pl->waves[l].cpr <= (int64_t)CTAS_PER_SM * 148;
+    const bool pipe_on = pl->pipe_on;
     Pipe pp;
-    pp.cnt = (int *)(ws + pl->off_CTR) + pl->pipe_cnt_off;
-    pp.expc = (const int *)(ws + pl->off_pexp);
+    pp.cnt = ctr + pl->pipe_cnt_off;
+    pp.expc = (const int *)(geo + pl->off_pexp);
     pp.err = pp.cnt + 3 * (G.L + 2);
     pp.on = pipe_on ? 1 : 0;
-    if (pl->kernel == 2) {
-        if (pl->gacc_ready != d_ws && pl->gacc_n > 0) {   // finalize resets what it reads
-            k_gacc_init<<<(unsigned)((3 * pl->gacc_n + 255) / 256), 256, 0, stream>>>(gacc, gfilt_of(pl, gacc, 0),
-                                                                                     3 * pl->gacc_n);
-            e = cudaGetLastError();
-            if (e != cudaSuccess) return cuda_fail(e, "k_gacc_init launch");
-            pl->gacc_ready = d_ws;
-        }
-        e = cudaMemsetAsync(ws + pl->off_CTR, 0, 4 * pl->ctr_n + 4, stream);
-        if (e != cudaSuccess) return cuda_fail(e, "unit counter reset");
-        if (G.L >= 2 && (e = launch_fin(pl, dg, gacc, 0, 2, stream)) != cudaSuccess)
-            return cuda_fail(e, "k_fin launch");
-    }
+    pp.spin_max = pl->kn.spin_max;
+    if (pl->kernel == 2 && G.L >= 2 && (e = launch_fin(pl, dg, gacc, 0, 2, stream)) != cudaSuccess)
+        return cuda_fail(e, "k_fin launch");
     for (int l = 2; l <= G.L; ++l) {
         if (pl->kernel == 1) {
             int64_t n = (int64_t)(G.L - l + 1) * G.cells[l] * pl->P;
@@ -799,35 +829,36 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
         w.nranges = G.L - l + 1;
         w.cpr = wh.cpr;
         w.nents = wh.nents;
-        w.ents = (const int4 *)(ws + pl->off_items + wh.ents_off);
-        w.upre = (const int32_t *)(ws + pl->off_items + wh.upre_off);
-        w.cb = (const int32_t *)(ws + pl->off_items + wh.cb_off);
+        w.ents = (const int4 *)(geo + pl->off_items + wh.ents_off);
+        w.upre = (const int32_t *)(geo + pl->off_items + wh.upre_off);
+        w.cb = (const int32_t *)(geo + pl->off_items + wh.cb_off);
         w.ncb = (int)wh.cb.size();
-        w.ctr = (int *)(ws + pl->off_CTR) + wh.ctr_off;
+        w.ctr = ctr + wh.ctr_off;
+        w.nunits = wh.nunits;
+        w.seeded = wh.seed;
         w.nout = wh.nout;
         w.GACC = gacc_of(pl, gacc, l);
         w.GFILT = gfilt_of(pl, gacc, l);
-        w.tile_off = (const int32_t *)(ws + pl->off_tile_off) + (size_t)(G.L + 1) * te_index(WCFGS[wh.cfg].te);
-        w.tile_cnt = (const int32_t *)(ws + pl->off_tile_cnt) + (size_t)(G.L + 1) * te_index(WCFGS[wh.cfg].te);
-        w.tiles = (const int32_t *)(ws + pl->off_tiles);
+        w.tile_off = (const int32_t *)(geo + pl->off_tile_off);
+        w.tile_cnt = (const int32_t *)(geo + pl->off_tile_cnt);
+        w.tiles = (const int32_t *)(geo + pl->off_tiles);
         // shard only wavefronts whose work outweighs the all-gather (~10-20 us on NVLink);
         // short wavefronts run redundantly on every rank (identical results, no exchange)
-        const bool shard = pl->world > 1 && (double)G.wave_splits[l] * pl->P >= pl->shard_min;
+        const bool shard = pl->world > 1 && (double)G.wave_splits[l] * pl->P >= pl->kn.shard_min;
         w.rank = shard ? pl->rank : 0;
         w.world = shard ? pl->world : 1;
         const int64_t ctas = wh.nents > 0 ? (int64_t)pl->P * w.nranges * w.cpr : 0;
-        // fused finalize (OOB_DP_FUSE=1): unsharded, single-pass waves finalize in k_wave_w's
-        // last CTAs and run the next wave's in-node cells and seeds in extra blocks
-        const bool fused = pl->fuse_fin && ctas > 0 && !shard && wh.seed_units == 0;
+        // fused finalize (OOB_DP_FUSE=1): unsharded waves finalize in k_wave_w's last CTAs
+        // and run the next wave's in-node cells and seeds in extra blocks
+        const bool fused = pl->kn.fuse_fin && ctas > 0 && !shard;
         int64_t aux = 0;
         w.nbmain = (int)ctas;
-        w.aux_first = pl->aux_first;
-        w.refresh = pl->refresh && wh.cpr > 1;   // one CTA per range: its own filter is current
+        w.refresh = pl->kn.refresh && wh.cpr > 1;   // one CTA per range: its own filter is current
         // batched sweeps (one CTA per range, small shared memory, a larger L1): the exact
         // path's children are worth warming in L1 (cfg5 -2%; neutral to negative for cfg4)
         w.prefetch = wh.cpr == 1 && pl->P > 1;
         w.fin_inline = fused ? 1 : 0;
-        w.rdone = (int *)(ws + pl->off_CTR) + wh.done_off;
+        w.rdone = ctr + wh.done_off;
         w.rclaim = w.rdone + (size_t)pl->P * w.nranges;
         if (fused) {
             int64_t nbs = 0, nbw = 0;
@@ -838,39 +869,22 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
         if (pl->timing && (!pipe_on || l == 2)) cudaEventRecord(pl->ev[pl->ev_used], stream);
         w.pp = pp;
         if (ctas > 0) {
-            // pass 1 (optional): the seeding units; pass 2: the rest, from the seeded minima
-            for (int pass = wh.seed_units > 0 ? 0 : 1; pass < 2; ++pass) {
-                w.unit_lo = pass == 0 ? 0 : wh.seed_units;
-                w.unit_hi = pass == 0 ? wh.seed_units : wh.nunits;
-                w.seeded = (pass == 1 && wh.seed_units > 0) || wh.seed;
-                w.ctr = (int *)(ws + pl->off_CTR) + wh.ctr_off + (size_t)pass * pl->P * w.nranges;
-                w.perm_a = 1;
-                w.rev_lanes = pl->rev_lanes;
-                if (pl->perm_order) {   // a multiplier near n * 0.618 coprime to n
-                    const long long n = w.unit_hi - w.unit_lo;
-                    long long a = std::max<long long>(2, (long long)(n * 0.6180339887));
-                    while (n > 2 && std::gcd(a, n) != 1) ++a;
-                    w.perm_a = n > 2 ? a : 1;
-                }
-                const unsigned grid = (unsigned)(ctas + aux);
-                void (*kern)(DevGeom, WaveW) = WCFGS[wh.cfg].te == 2 ? k_wave_w<2> : WCFGS[wh.cfg].te == 3 ? k_wave_w<3>
-                                               : WCFGS[wh.cfg].te == 4 ? k_wave_w<4> : k_wave_w<5>;
-                if (pipe_on && l >= 3) {   // programmatic dependent of wave l-1 (counters, not the boundary)
-                    cudaLaunchConfig_t lc = {};
-                    lc.gridDim = dim3(grid);
-                    lc.blockDim = dim3(NTW);
-                    lc.dynamicSmemBytes = wh.smem;
-                    lc.stream = stream;
-                    cudaLaunchAttribute at[1];
-                    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-                    at[0].val.programmaticStreamSerializationAllowed = 1;
-                    lc.attrs = at;
-                    lc.numAttrs = 1;
-                    e = cudaLaunchKernelEx(&lc, kern, dg, w);
-                    if (e != cudaSuccess) return cuda_fail(e, "k_wave_w launch (pipelined)");
-                } else {
-                    kern<<<grid, NTW, wh.smem, stream>>>(dg, w);
-                }
+            const unsigned grid = (unsigned)(ctas + aux);
+            if (pipe_on && l >= 3) {   // programmatic dependent of wave l-1 (counters, not the boundary)
+                cudaLaunchConfig_t lc = {};
+                lc.gridDim = dim3(grid);
+                lc.blockDim = dim3(NTW);
+                lc.dynamicSmemBytes = wh.smem;
+                lc.stream = stream;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                at[0].val.programmaticStreamSerializationAllowed = 1;
+                lc.attrs = at;
+                lc.numAttrs = 1;
+                e = cudaLaunchKernelEx(&lc, k_wave_w<TE_W>, dg, w);
+                if (e != cudaSuccess) return cuda_fail(e, "k_wave_w launch (pipelined)");
+            } else {
+                k_wave_w<TE_W><<<grid, NTW, wh.smem, stream>>>(dg, w);
             }
         }
         if (pl->timing && (!pipe_on || l == G.L)) {
@@ -906,25 +920,3 @@ extern "C" int oob_dbg_flush_stats(int enable, unsigned long long *out4) {
     if (cudaMemcpyToSymbol(oob::g_flush_stats, z, sizeof(z)) != cudaSuccess) return 1;
     return cudaMemcpyToSymbol(oob::g_flush_stats_on, &enable, sizeof(int)) == cudaSuccess ? 0 : 1;
 }
-
-// Diagnostic (not part of the C ABI header): byte offsets of the cell, shadow and argmin
-// tables inside a plan's workspace (scripts/dbg_table.py).
-extern "C" int oob_dbg_offsets(const oob_dp_plan *pl, unsigned long long *out5) {   // [7]
-    if (!pl || !out5) return 1;
-    out5[0] = pl->off_CELL;
-    out5[1] = pl->off_SH;
-    out5[2] = pl->off_ARG;
-    out5[3] = pl->off_base;
-    out5[4] = pl->off_cells;
-    out5[5] = pl->off_off;
-    out5[6] = (unsigned long long)pl->g.A;
-    return 0;
-}
-
-#ifdef OOB_DBG_FILTER
-extern "C" int oob_dbg_filter(unsigned long long *out64) {
-    if (cudaMemcpyFromSymbol(out64, oob::g_dbg, sizeof(unsigned long long) * 256) != cudaSuccess) return 1;
-    unsigned long long z[256] = {0};
-    return cudaMemcpyToSymbol(oob::g_dbg, z, sizeof(z)) == cudaSuccess ? 0 : 1;
-}
-#endif

@@ -21,6 +21,8 @@
 
 #include "oob_internal.h"
 
+extern char **environ;
+
 namespace oob {
 
 static thread_local std::string g_last_error;
@@ -282,8 +284,13 @@ extern "C" oob_status oob_template_set_from_packed(const void *h_packed, const o
             const PackedHeader *h = (const PackedHeader *)(base + t * info->packed_template_bytes);
             const int32_t *st = (const int32_t *)(h + 1);
             if (h->S < 1 || h->S > info->L || h->status != 0) {
+                const std::string where = " (profile " + std::to_string(pr) + ", template " + std::to_string(i) + ")";
+                const int code = h->status;
                 delete s;
-                return fail(OOB_E_CUDA, "corrupt packed template (profile " + std::to_string(pr) + ", i " + std::to_string(i) + ")");
+                if (code == 2)
+                    return fail(OOB_E_CUDA, "wavefront pipeline wait timed out (GPU shared with other work?): "
+                                            "the DP table is incomplete" + where);
+                return fail(OOB_E_CUDA, "corrupt packed template" + where);
             }
             oob_template &tv = s->templates[t];
             tv.nodes = h->nodes; tv.num_stages = h->S; tv.kstar = h->kstar; tv.reserved = 0;
@@ -334,13 +341,13 @@ PlanCache &plan_cache() {
 std::string plan_key(int L, int M, int n_lo, int n_hi, int P, int dev) {
     std::string k = std::to_string(L) + "," + std::to_string(M) + "," + std::to_string(n_lo) + "," +
                     std::to_string(n_hi) + "," + std::to_string(P) + "," + std::to_string(dev);
-    static const char *knobs[] = {"OOB_DP_KERNEL", "OOB_DP_WCFG", "OOB_DP_AUTOCFGS", "OOB_DP_UPC", "OOB_DP_SEED",
-                                  "OOB_DP_SEEDINIT", "OOB_DP_SEEDSPO", "OOB_DP_SMALLPAIRS", "OOB_DP_FUSE",
-                                  "OOB_DP_PERM", "OOB_DP_REV"};
-    for (const char *n : knobs) {
-        const char *v = std::getenv(n);
-        k += std::string("|") + (v ? v : "");
-    }
+    // every plan-time switch: all OOB_DP_* variables of the environment (sorted), so a
+    // plan built under other settings is never reused
+    std::vector<std::string> kv;
+    for (char **e = environ; e && *e; ++e)
+        if (std::strncmp(*e, "OOB_DP_", 7) == 0) kv.emplace_back(*e);
+    std::sort(kv.begin(), kv.end());
+    for (const std::string &x : kv) k += "|" + x;
     return k;
 }
 oob_dp_plan *take_plan(const std::string &key) {
@@ -408,7 +415,6 @@ extern "C" oob_status oob_generate_templates(const oob_profile *const *profiles,
         st = oob_dp_plan_create(L, M, n_lo, n_hi, num_profiles, &plan);
         if (st != OOB_OK) return st;
     }
-    dp_plan_invalidate(plan);   // the workspace may be new memory at an old address
     struct Return {
         std::string key;
         oob_dp_plan *p;

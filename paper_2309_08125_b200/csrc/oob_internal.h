@@ -59,10 +59,6 @@ oob_status nccl_allgather_bytes(void *comm, const void *send, void *recv, size_t
                                 int world, void *stream);
 
 // ---------------------------------------------------------------- packed templates
-// Forget which workspace a plan's geometry / accumulators were initialised in (the next
-// oob_dp_run re-uploads them); used by the plan cache of oob_generate_templates.
-void dp_plan_invalidate(oob_dp_plan *pl);
-
 // Device output record, see oob_dp_run in oobleck_plan.h.
 struct PackedHeader {
     int32_t nodes, S, kstar, status;

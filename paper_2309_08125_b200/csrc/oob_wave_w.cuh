@@ -43,8 +43,9 @@ constexpr unsigned long long ACC_DIRTY = 1ull << 32;   // accumulator key word: 
 struct Pipe {
     int *cnt;              // [3][L+2]: seeds, in-node cells, finalize shares done per wave
     const int *expc;       // [3][L+2]: the counts that make each part ready
-    int *err;              // timeout flag
+    int *err;              // timeout flag (k_extract turns it into a template status: OOB_E_CUDA)
     int on;
+    long long spin_max;    // polls before a wait gives up (~200 ns each)
 };
 
 // Finalize / in-node work of one wavefront (k_fin, or k_wave_w's extra blocks and last CTAs).
@@ -71,11 +72,9 @@ struct WaveW {
     const int32_t *upre;   // [nents + 1] unit prefix: entry e owns units [upre[e], upre[e+1])
     const int32_t *cb;     // chunk row boundaries: rows [cb[off+c], cb[off+c+1])
     int ncb;               // entries of cb (staged in shared memory)
-    int *ctr;              // [P][nranges] unit counters of this pass (zeroed before the launch)
-    int unit_lo, unit_hi;  // this pass processes queue units [unit_lo, unit_hi)
-    int seeded;            // 1: start from the global accumulator (an earlier pass's minima)
-    long long perm_a;      // > 1: unit order permutation multiplier (coprime to the pass's unit count)
-    int rev_lanes;         // 1: lane i holds the block's tile 31 - i (diagnostic)
+    int *ctr;              // [P][nranges] unit counters (zeroed before the launch)
+    int nunits;            // units of the range's queue
+    int seeded;            // 1: start from the global accumulator (the seeds' minima)
     int rank, world;       // single-profile sharding: this rank takes units rank, rank+world, ...
     int nout;              // W-part cells of a slab of length l (W(1)..W(Q_l))
     ulonglong2 *GACC;      // global accumulator [P][nranges][nout]: {total bits, key}
@@ -87,7 +86,6 @@ struct WaveW {
     // the next wave (fa: nbw = 0; independent of this wave, they fill its tail); the last CTA
     // of each range (rdone counter) finalizes the range's W outputs of this wave (fw: lw = l)
     int nbmain;
-    int aux_first;             // 1: the extra blocks come first in the grid (start with the main work)
     int fin_inline;
     int *rdone;                // [P][nranges] CTAs of the range that have merged
     int *rclaim;               // [P][nranges] finalize shares claimed
@@ -266,16 +264,14 @@ __device__ __forceinline__ float split_lb(float TA, float TB, float TS, float TC
 // Candidate queue: the outputs whose slot bound passes the filter are not re-evaluated in
 // place (divergent, global-latency bound) but appended to a per-warp queue in shared memory
 // and re-evaluated by the whole warp, one output per lane, when the queue is full and at the
-// end of each unit.  An entry (24 B) names one output E' of one (tile, streamed row) pair:
+// end of each unit.  An entry (20 B) names one output E' of one (tile, streamed row) pair:
 //   x = tile cell index, y = streamed row's first cell index, z = key base kb,
-//   w = accumulator entry | E' << 13 | ncell << 20 | LT << 23 | rl << 24,
-//   v = the stage count the key does not carry (LT: rs, else S0).
+//   w = accumulator entry (16 bits) | ncell << 16 | LT << 19,
+//   v = (the stage count the key does not carry: LT: rs, else S0; 10 bits) | E' << 10 | rl << 21
+// (11 bits each: rows hold <= L <= 1023 cells, E' <= rl + TE - 2; the accumulator entries of
+// a wave, nout + dummies, are < 2^16 — oob_dp_plan_create falls back to k_wave_v1 otherwise).
 constexpr int XQ_CAP = 32;
-#ifndef OOB_XQ_PREFETCH
-#define OOB_XQ_PREFETCH 0   // L1 prefetch of the queued children: measured slower (cfg4 +2%)
-#endif
-constexpr bool XQ_PREFETCH = OOB_XQ_PREFETCH;
-constexpr int XQ_BYTES = XQ_CAP * 24;     // per warp
+constexpr int XQ_BYTES = XQ_CAP * 20;     // per warp
 
 // Exact evaluation of the queued outputs (warp-collective; lane i takes entry i): every
 // valid contribution t (tile cell t, streamed cell e = E' - t) in binary64 in the oracle's
@@ -294,10 +290,10 @@ __device__ __noinline__ void xq_flush(const uint4 *q4, const unsigned *q1, int c
     if (lane < count) {
         const uint4 en = q4[lane];
         const unsigned v = q1[lane];
-        const int idx = (int)(en.w & 8191u), Ep = (int)((en.w >> 13) & 127u), ncell = (int)((en.w >> 20) & 7u);
-        const bool lt = (en.w >> 23) & 1u;
-        const int rl = (int)(en.w >> 24);
-        const int rs = lt ? (int)v : (int)(en.z & 1023u), S0 = lt ? (int)(en.z & 1023u) : (int)v;
+        const int idx = (int)(en.w & 0xFFFFu), ncell = (int)((en.w >> 16) & 7u);
+        const bool lt = (en.w >> 19) & 1u;
+        const int v0 = (int)(v & 1023u), Ep = (int)((v >> 10) & 2047u), rl = (int)(v >> 21);
+        const int rs = lt ? v0 : (int)(en.z & 1023u), S0 = lt ? (int)(en.z & 1023u) : v0;
         unsigned long long bb = ACC_EMPTY;
         uint32_t bk = 0xFFFFFFFFu;
 #pragma unroll
@@ -368,83 +364,14 @@ __device__ __noinline__ int xq_push(unsigned mask, int base, unsigned bidx, int 
             mask &= mask - 1;
             const int slot = count + __popc(bal & lane_lt);
             q4[slot] = make_uint4(bidx, srow, kb,
-                                  (unsigned)(idx0 + Ep) | ((unsigned)Ep << 13) | ((unsigned)ncell << 20) |
-                                      (LT ? 1u << 23 : 0u) | ((unsigned)rl << 24));
-            q1[slot] = LT ? (unsigned)rs : (unsigned)S0;
-            if (XQ_PREFETCH) {   // warm L1 with the children the flush will load
-                const Cell4 *tp = CELL + bidx, *sp = CELL + srow + max(0, Ep - (TE - 1));
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(tp));
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(tp + TE - 1));
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(sp));
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(sp + TE - 1));
-            }
+                                  (unsigned)(idx0 + Ep) | ((unsigned)ncell << 16) | (LT ? 1u << 19 : 0u));
+            q1[slot] = (LT ? (unsigned)rs : (unsigned)S0) | ((unsigned)Ep << 10) | ((unsigned)rl << 21);
         }
         count += n;
     }
     return count;
 }
 
-#ifdef OOB_DBG_FILTER
-// Debug build: an output that did not pass must not hold a split that beats (or ties with a
-// smaller key) the accumulator entry; violations are recorded in g_dbg.
-__device__ unsigned long long g_dbg[256];
-template <int TE, bool LT>
-__device__ void dbg_check(const Cell4 *bp, int ncell, const Cell4 *srow, int rl, int Ep, int S0, int rs, uint32_t kb,
-                          unsigned acc_s, int idx, float mnv, float fv, const float (&TA)[TE], const float (&TB)[TE],
-                          const float (&TS)[TE], const float (&TC)[TE], const XRing &xr, int rb) {
-    unsigned long long cx, cy;
-    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(cx), "=l"(cy) : "r"(acc_s + 16u * (unsigned)idx) : "memory");
-    for (int t = 0; t < TE; ++t) {
-        const int e = Ep - t;
-        if (t >= ncell || e < 0 || e >= rl) continue;
-        const Cell4 tc = d_load(bp + t), sc = d_load(srow + e);
-        double tot;
-        uint32_t key;
-        if (LT) {
-            tot = split_total(tc.T1, tc.T3, tc.TS, __dadd_rn(tc.C1, (double)(3 * (rs + e))), sc.T1, sc.T3, sc.TS,
-                              __dadd_rn(sc.C1, (double)(4 * (S0 + t))));
-            key = kb + (uint32_t)t;
-        } else {
-            tot = split_total(sc.T1, sc.T3, sc.TS, __dadd_rn(sc.C1, (double)(3 * (S0 + t))), tc.T1, tc.T3, tc.TS,
-                              __dadd_rn(tc.C1, (double)(4 * (rs + e))));
-            key = kb + (uint32_t)e;
-        }
-        const unsigned long long tb = (unsigned long long)__double_as_longlong(tot);
-        if (lex_less(tb, key, cx, (uint32_t)cy)) {
-            const unsigned long long n = atomicAdd(&g_dbg[0], 1ull);
-            if (n < 7) {
-                unsigned long long *r = g_dbg + 1 + 9 * n;
-                r[0] = tb; r[1] = cx; r[2] = key | ((unsigned long long)(uint32_t)cy << 32);
-                r[3] = __float_as_uint(mnv) | ((unsigned long long)__float_as_uint(fv) << 32);
-                r[4] = (unsigned long long)t | ((unsigned long long)e << 16) | ((unsigned long long)Ep << 32);
-                r[5] = (unsigned long long)LT | ((unsigned long long)TE << 8) | ((unsigned long long)rl << 16) |
-                       ((unsigned long long)ncell << 32);
-                const float4 ts = LT ? make_float4(0, 0, 0, 0) : make_float4(0, 0, 0, 0);
-                (void)ts;
-                r[6] = (unsigned long long)idx | ((unsigned long long)S0 << 32);
-                r[7] = (unsigned long long)rs;
-                r[8] = (unsigned long long)(threadIdx.x & 31);
-                if (n < 3) {
-                    float *q = reinterpret_cast<float *>(g_dbg + 100 + 8 * n);
-                    float ta = 0, tb = 0, tsv = 0, tcv = 0;
-#pragma unroll
-                    for (int tt = 0; tt < TE; ++tt)
-                        if (tt == t) { ta = TA[tt]; tb = TB[tt]; tsv = TS[tt]; tcv = TC[tt]; }
-                    q[0] = ta; q[1] = tb; q[2] = tsv; q[3] = tcv;
-                    const float4 x = *xr_at(xr, rb + e);
-                    q[4] = x.x; q[5] = x.y; q[6] = x.z; q[7] = x.w;
-                    const float4 a = __ldcg(reinterpret_cast<const float4 *>(xr.src - (threadIdx.x & 31) * 16) + rb + e),
-                                 b = d_shadow(sc.T1, sc.T3, sc.TS, sc.C1);
-                    r[7] = (unsigned long long)rs | ((unsigned long long)xr.nb_ok << 16) | ((unsigned long long)xr.nb_iss << 32) |
-                           ((unsigned long long)rb << 48);
-                    q[8] = a.x; q[9] = a.y; q[10] = a.z; q[11] = a.w;
-                    q[12] = b.x; q[13] = b.y; q[14] = b.z; q[15] = b.w;
-                }
-            }
-        }
-    }
-}
-#endif
 
 // One step (streamed cell x, uniform factor fst: LT 3 S_R, else 4 s) of a lane's TE splits:
 // lower bounds into the ring slots (output E' = e + t lives in slot E' mod TE; its first
@@ -485,7 +412,7 @@ __device__ __forceinline__ void run_rows(XRing &xr, int64_t sidx, const int32_t 
                                          int l1, int L, const int *outOff, int nout, unsigned acc_s,
                                          unsigned filt_s, unsigned *gfr, uint4 *q4, unsigned *q1,
                                          const Cell4 *CELL) {
-    static_assert(32 % TE == 0 || TE == 3 || TE == 5, "TE");
+    static_assert(TE == 4, "the pending-output switch below covers TE = 4");
     int qn = 0;                                           // queued outputs (warp-uniform)
     const int S0 = rowB + e0;
     const float *filt = reinterpret_cast<const float *>(__cvta_shared_to_generic(filt_s));
@@ -527,12 +454,6 @@ __device__ __forceinline__ void run_rows(XRing &xr, int64_t sidx, const int32_t 
                 pm4 |= (mn[I] <= fb[I]) ? (1u << I) : 0u;
             }
             pmask |= pm4 << (blk - mbase);
-#ifdef OOB_DBG_FILTER
-            for (int I = 0; I < TE; ++I)
-                if (!((pmask >> (blk + I - mbase)) & 1))
-                    dbg_check<TE, LT>(CELL + bidx, ncell, CELL + srow, rl, blk + I, S0, rs, kb, acc_s, idx0 + blk + I,
-                                      mn[I], fr[blk + I], TA, TB, TS, TC, xr, rb);
-#endif
         }
         // tail block (rl % TE steps) and the pending outputs E' = rl .. rl + TE - 2
         {
@@ -895,8 +816,9 @@ __device__ __forceinline__ void fin_small_block(const DevGeom &g, const FinArgs 
 // for the previous wave), so "wave c ready" covers every shorter wave.  Every cell of a
 // wave is read only after its wave is ready (and the tables pad each wave to whole 32-byte
 // sectors plus the streams' read-ahead), so L1-cached loads never see a stale line.  Waits
-// are bounded; a timeout sets the error word and releases every later wait (the results
-// are then wrong and the parity tests fail, but the GPU never hangs).
+// are bounded; a timeout sets the error word and releases every later wait: the results
+// are then wrong, so k_extract marks every template (status 2) and oob_generate_templates /
+// oob_template_set_from_packed return OOB_E_CUDA; the GPU never hangs.
 __device__ __forceinline__ int ld_acquire(const int *p) {
     int v;
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -904,19 +826,20 @@ __device__ __forceinline__ int ld_acquire(const int *p) {
 }
 // one thread waits until the parts in `mask` (bit kind: 0 seeds, 1 in-node cells,
 // 2 finalize shares) of wave c are ready
-__device__ __noinline__ void pipe_wait_raw(int *cnt, const int *expc, int *err, int L, int c, int mask) {
+__device__ __noinline__ void pipe_wait_raw(int *cnt, const int *expc, int *err, int L, int c, int mask,
+                                           long long spin_max) {
     for (long long it = 0;; ++it) {
         bool ok = true;
         for (int kind = 0; kind < 3; ++kind)
             if ((mask >> kind) & 1) ok = ok && ld_acquire(cnt + kind * (L + 2) + c) >= expc[kind * (L + 2) + c];
         if (ok || *(volatile int *)err) break;
-        if (it > (1ll << 24)) { atomicExch(err, 1); break; }
+        if (it >= spin_max) { atomicExch(err, 1); break; }
         __nanosleep(200);
     }
     __threadfence();
 }
 __device__ __forceinline__ void pipe_wait(const Pipe &pp, int L, int c, int mask) {
-    if (pp.on && c >= 2) pipe_wait_raw(pp.cnt, pp.expc, pp.err, L, c, mask);
+    if (pp.on && c >= 2) pipe_wait_raw(pp.cnt, pp.expc, pp.err, L, c, mask, pp.spin_max);
 }
 // the calling block has finished writing its part of wave c (all threads reach this)
 __device__ __forceinline__ void pipe_signal(const Pipe &pp, int L, int kind, int c) {
@@ -945,12 +868,11 @@ template <int TE>
 __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, WaveW w) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_last;
-    // block order: aux_first ? [extra blocks][main CTAs] : [main CTAs][extra blocks]
-    const int naux = (int)gridDim.x - w.nbmain;
-    const int bid = w.aux_first ? (int)blockIdx.x - naux : (int)blockIdx.x;   // main CTA index
+    // block order: [main CTAs][extra blocks]
+    const int bid = (int)blockIdx.x;          // main CTA index
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // the next wave may start (pipeline)
-    if (bid < 0 || bid >= w.nbmain) {         // next wave's seeds and in-node cells
-        const int ab = w.aux_first ? (int)blockIdx.x : (int)blockIdx.x - w.nbmain;
+    if (bid >= w.nbmain) {                    // next wave's seeds and in-node cells
+        const int ab = (int)blockIdx.x - w.nbmain;
         if (ab < w.fa.nbseed) {
             // seeds of wave l+1 read cells of waves <= l-1 and reuse wave l-1's accumulator buffer
             if (threadIdx.x == 0) pipe_wait(w.pp, L_of(g), w.fa.lseed - 2, 7);
@@ -1038,18 +960,16 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
         if (i < w.nents) sents[i] = w.ents[i];
     }
     __syncthreads();
-    const int nunits = w.unit_hi;
+    const int nunits = w.nunits;
     const unsigned acc_s = (unsigned)__cvta_generic_to_shared(acc);
     const unsigned filt_s = (unsigned)__cvta_generic_to_shared(filt);
     int *gctr = w.ctr + pr;
 
     for (;;) {
         int un = 0;
-        if (lane == 0) un = w.unit_lo + w.rank + w.world * atomicAdd(gctr, 1);
+        if (lane == 0) un = w.rank + w.world * atomicAdd(gctr, 1);
         un = __shfl_sync(0xFFFFFFFFu, un, 0);
         if (un >= nunits) break;
-        if (w.perm_a > 1)    // visit the queue in a pseudo-random order (a permutation of the pass's units)
-            un = w.unit_lo + (int)(((long long)(un - w.unit_lo) * w.perm_a) % (nunits - w.unit_lo));
         int lo = 0, hi = w.nents - 1;                // entry: upre[ei] <= un < upre[ei+1]
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
@@ -1079,7 +999,7 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
         const int lb = ltiled ? l1 : l2;
         const int us = ltiled ? k : u;                             // small slab start
         const int ub = ltiled ? u : k;
-        const int ti = blk * 32 + (w.rev_lanes ? 31 - lane : lane);
+        const int ti = blk * 32 + lane;
         const bool has = ti < stcnt[lb];
         const int32_t code = has ? w.tiles[stoff[lb] + ti] : 0;
         const int rowB = has ? (code >> 16) : 1;
@@ -1202,12 +1122,16 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
     }
 }
 
-__global__ void k_gacc_init(ulonglong2 *gacc, unsigned *gfilt, int64_t n) {
+// Start of every run: empty accumulators and filters (the finalize resets what it reads,
+// but a run that failed part-way, or another plan's run in the same workspace, leaves
+// entries behind) and zero counters (unit counters, pipeline counters, error word).
+__global__ void k_init(ulonglong2 *gacc, unsigned *gfilt, int64_t nacc, int *ctr, int64_t nctr) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) {
+    if (i < nacc) {
         gacc[i] = make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull);
         gfilt[i] = FILT_EMPTY;
     }
+    if (i < nctr) ctr[i] = 0;
 }
 
 }  // namespace oob

@@ -82,24 +82,62 @@ def test_batched_profiles_vs_oracle(planner):
         _assert_same(ts.templates(i), want, f"cfg5 profile {i}")
 
 
-@pytest.mark.parametrize("fuse", ["default", "0", "1", "pipe0"])
+CFG4_VARIANTS = {"default": ({}, {"pipelined": 1, "fused": 1}),
+                 "fuse0": ({"OOB_DP_FUSE": "0"}, {"pipelined": 0, "fused": 0}),
+                 "pipe0": ({"OOB_DP_PIPE": "0"}, {"pipelined": 0, "fused": 1})}
+
+
+@pytest.mark.parametrize("variant", sorted(CFG4_VARIANTS))
 @pytest.mark.parametrize("mode", ["real", "dyadic"])
-def test_cfg4_full_vs_golden(planner, mode, fuse, monkeypatch):
+def test_cfg4_full_vs_golden(planner, mode, variant, monkeypatch):
     """Full template set of the north-star config (96 layers, 512 x 8 GPUs, f=4, n0=3)
-    vs the C oracle's output stored by scripts/make_golden.py; with the finalize fused into
-    k_wave_w (OOB_DP_FUSE=1, pipelined wavefronts by default), as separate k_fin launches
-    (0), and fused without the wavefront pipeline (pipe0)."""
-    if fuse == "pipe0":
-        monkeypatch.setenv("OOB_DP_PIPE", "0")
-    elif fuse != "default":
-        monkeypatch.setenv("OOB_DP_FUSE", fuse)
+    vs the C oracle's output stored by scripts/make_golden.py: pipelined wavefronts with the
+    finalize fused into k_wave_w (default), separate k_fin launches (fuse0), and fused
+    without the wavefront pipeline (pipe0).  The plan's reported switches prove the variant
+    ran (every OOB_DP_* variable is part of the plan-cache key)."""
+    env, want_sw = CFG4_VARIANTS[variant]
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     rec = load_golden("cfg4", mode)
     if rec is None:
         pytest.skip(f"tests/golden/cfg4_{mode}.json not generated")
     cfg = CONFIGS["cfg4"]
+    info = planner.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, 1).info
+    for k, v in want_sw.items():
+        assert getattr(info, k) == v, (variant, k)
     prof = config_profiles(cfg, mode)[0]
     ts = _gpu_set(planner, [prof], (cfg.L, cfg.M, cfg.N, cfg.f, cfg.n0))
     _assert_same(ts.templates(0), rec["profiles"][0]["templates"], "cfg4")
+
+
+def test_pipeline_timeout_is_an_error(planner, monkeypatch):
+    """A pipelined wait that times out (OOB_DP_PIPE_SPIN=0: give up after one poll) must
+    surface as OOB_E_CUDA, never as a template set built from an incomplete table."""
+    from paper_2309_08125_b200._lib import OOB_E_CUDA, OobError
+    monkeypatch.setenv("OOB_DP_PIPE_SPIN", "0")
+    cfg = CONFIGS["cfg4"]
+    assert planner.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, 1).info.pipelined == 1
+    prof = config_profiles(cfg, "real")[0]
+    with pytest.raises(OobError) as e:
+        _gpu_set(planner, [prof], (cfg.L, cfg.M, cfg.N, cfg.f, cfg.n0))
+    assert e.value.status == OOB_E_CUDA and "timed out" in str(e.value)
+
+
+def test_long_rows_queue_fields(planner, monkeypatch):
+    """L = 150, 20-node templates: streamed W rows of up to 131 cells and wide accumulators
+    (the candidate-queue entry fields must not overflow).  The tiled W kernel must
+    equal the thread-per-cell kernel (k_wave_v1) on every template, and the oracle on the
+    smallest ones."""
+    L, M, N, f, n0 = 150, 8, 21, 1, 1
+    prof = random_profile(150150, L, M, "lognormal")
+    assert planner.DPPlan(L, M, n0, 20, 1).info.kernel == 2
+    got = _gpu_set(planner, [prof], (L, M, N, f, n0)).templates(0)
+    monkeypatch.setenv("OOB_DP_KERNEL", "v1")
+    assert planner.DPPlan(L, M, n0, 20, 1).info.kernel == 1
+    ref = _gpu_set(planner, [prof], (L, M, N, f, n0)).templates(0)
+    _assert_same(got, ref, "L=150 W kernel vs v1")
+    want, _ = coracle.template_set(prof.fwd_ms, prof.bwd_ms, M, n0, 2)
+    _assert_same(got[:2], want, "L=150 small templates vs oracle")
 
 
 def test_cfg4_sampled_templates_vs_oracle(planner):
@@ -152,41 +190,35 @@ def test_edge_cases(planner):
     assert e.value.status == OOB_E_INFEASIBLE
 
 
-@pytest.mark.parametrize("key", ["cfg2", "cfg3"])
-def test_v1_kernel_still_matches(planner, key, monkeypatch):
-    """The simple thread-per-cell kernel (OOB_DP_KERNEL=v1) stays parity-green too."""
-    monkeypatch.setenv("OOB_DP_KERNEL", "v1")
-    cfg = CONFIGS[key]
-    prof = config_profiles(cfg, "real")[0]
-    ts = _gpu_set(planner, [prof], (cfg.L, cfg.M, cfg.N, cfg.f, cfg.n0))
-    want, _ = coracle.template_set(prof.fwd_ms, prof.bwd_ms, cfg.M, cfg.n0, cfg.n_max)
-    _assert_same(ts.templates(0), want, key + " v1")
-
-
 VARIANTS = [
-    {"OOB_DP_WCFG": "1"},            # TE = 5 register tile
-    {"OOB_DP_WCFG": "2"},            # TE = 3
-    {"OOB_DP_WCFG": "3"},            # TE = 2
-    {"OOB_DP_FUSE": "0"},            # separate k_fin launches
-    {"OOB_DP_FUSE": "1"},            # finalize + next wave's in-node cells inside k_wave_w
-    {"OOB_DP_SEEDSPO": "1000"},      # only waves with >= 1000 splits per output seeded
-    {"OOB_DP_SEEDINIT": "0"},        # no seeds
-    {"OOB_DP_SMALLPAIRS": "4"},      # fewer threads per in-node cell
-    {"OOB_DP_PIPE": "0"},            # plain kernel boundaries between wavefronts
-    {"OOB_DP_PIPE": "0", "OOB_DP_SEEDINIT": "0"},
-    {"OOB_DP_CHMAX": "24"},          # short units: many per range, long queues
-    {"OOB_DP_AUXFIRST": "1"},        # extra blocks first in the grid (finalize waits bounded)
+    ({"OOB_DP_KERNEL": "v1"}, {"kernel": 1}),                  # thread-per-cell reference kernel
+    ({"OOB_DP_FUSE": "0"}, {"fused": 0, "pipelined": 0}),      # separate k_fin launches
+    ({"OOB_DP_FUSE": "1"}, {"fused": 1}),                      # finalize + next wave's in-node cells inside k_wave_w
+    ({"OOB_DP_SEEDSPO": "1000"}, {}),                          # only waves with >= 1000 splits per output seeded
+    ({"OOB_DP_SEEDINIT": "0"}, {"seeded": 0}),                 # no seeds
+    ({"OOB_DP_SMALLPAIRS": "4"}, {"small_pairs": 4}),          # fewer threads per in-node cell
+    ({"OOB_DP_PIPE": "0"}, {"pipelined": 0, "fused": 1}),      # plain kernel boundaries between wavefronts
+    ({"OOB_DP_PIPE": "0", "OOB_DP_SEEDINIT": "0"}, {"pipelined": 0, "seeded": 0}),
+    ({"OOB_DP_CHMAX": "24"}, {"chunk_max": 24}),               # short units: many per range, long queues
+    ({"OOB_DP_REFRESH": "0"}, {"refresh": 0}),                 # no per-unit filter refresh
 ]
 
 
-@pytest.mark.parametrize("env", VARIANTS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+@pytest.mark.parametrize("variant", VARIANTS, ids=lambda v: ",".join(f"{k}={x}" for k, x in v[0].items()))
 @pytest.mark.parametrize("key", ["cfg2", "cfg3"])
-def test_kernel_variants_match(planner, key, env, monkeypatch):
-    """Alternative W-kernel configurations and finalize / seeding modes (plan-time switches)
-    all give the oracle's template sets."""
+def test_kernel_variants_match(planner, key, variant, monkeypatch):
+    """Alternative kernels and finalize / seeding / pipeline modes (plan-time switches) all
+    give the oracle's template sets.  The plan's reported switches prove each variant ran."""
+    env, want_sw = variant
+    cfg = CONFIGS[key]
+    base = planner.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, 1).info
     for k, v in env.items():
         monkeypatch.setenv(k, v)
-    cfg = CONFIGS[key]
+    info = planner.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, 1).info
+    for k, v in want_sw.items():
+        assert getattr(info, k) == v, (env, k, getattr(info, k))
+    if "OOB_DP_SEEDSPO" in env:
+        assert info.seeded < base.seeded
     for mode in ("real", "dyadic"):
         prof = config_profiles(cfg, mode)[0]
         ts = _gpu_set(planner, [prof], (cfg.L, cfg.M, cfg.N, cfg.f, cfg.n0))

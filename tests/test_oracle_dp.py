@@ -235,3 +235,70 @@ def test_node_sizes_spec():
     with pytest.raises(ValueError):
         node_sizes(3, 1, 2)
     assert node_sizes(512, 4, 3, L=96) == list(range(3, 97))    # reading R4 (cap at L)
+
+
+# ------------------------------------------------------------------ tie-rule pins (readings R6, R8)
+def _cd_profile(cd):
+    """Profile with F+B = cd[l][d-1] exactly (F = B = c/2; dyadic values, exact sums)."""
+    import numpy as np
+    c = np.asarray(cd, dtype=np.float64)
+    return c / 2.0, c / 2.0
+
+
+def _both_oracles(fwd, bwd, M, n):
+    py = TemplateDP(fwd, bwd, M).template(n)
+    c, _ = coracle.template_set(fwd, bwd, M, n, n)
+    assert c[0] == py
+    return py
+
+
+def test_s_tie_smaller_s_wins():
+    """Reading R8 ("smaller S"): L=2, M=2, n=1, per-layer F+B on 1 GPU
+    = 1 and on 2 GPUs = 1.125 (both layers).
+      S=1: one stage (0,2) on 2 GPUs, t = 2.25: T1 = T3 = 2.25, T2 = (4-1+0-1) 2.25 = 4.5,
+           total 9.
+      S=2: stages (0,1),(1,2) on 1 GPU each, times (1,1): T1 = 2, k* = 0, T2 = (8-2+0-1) 1
+           = 5, T3 = 2, total 9.
+    Equal totals: the smaller S wins -> one stage.  (Larger-S-wins would return S=2.)"""
+    fwd, bwd = _cd_profile([[1, 1.125], [1, 1.125]])
+    assert closed_form([2.25])[0] == 9.0 and closed_form([1.0, 1.0])[0] == 9.0
+    t = _both_oracles(fwd, bwd, 2, 1)
+    assert (t["S"], t["total"]) == (1, 9.0)
+    assert t["stages"] == [(0, 2, 2, 0, 0)]
+
+
+def test_device_split_order_smaller_m_wins():
+    """Reading R6 (smaller k, then m, then s): L=2, M=3, n=1; layer 0 costs
+    F+B = 2 on 1 or 2 GPUs, layer 1 costs 1 on 1 or 2 GPUs, both cost 10 on 3 GPUs.
+    W(1) with S'=2 splits only at k=1 into (I(m), I(3-m)):
+      m=1: stage times (2, 1) on (1, 2) GPUs: T1 = 3, k* = 0, T2 = 5*2 = 10, T3 = 3 -> 16;
+      m=2: stage times (2, 1) on (2, 1) GPUs -> 16 as well.
+    S=1 (one stage on 3 GPUs) costs 4*20 = 80.  The tie goes to m=1: stage 0 gets 1 GPU
+    (offset 0), stage 1 gets 2 GPUs (offset 1).  (Reversed m order returns (2 GPUs, 1 GPU).)"""
+    fwd, bwd = _cd_profile([[2, 2, 10], [1, 1, 10]])
+    assert closed_form([2.0, 1.0])[0] == 16.0
+    t = _both_oracles(fwd, bwd, 3, 1)
+    assert (t["S"], t["total"]) == (2, 16.0)
+    assert t["stages"] == [(0, 1, 1, 0, 0), (1, 2, 2, 0, 1)]
+
+
+def test_node_split_order_smaller_j_wins():
+    """Reading R6 for whole-node splits W(q) -> (W(j), W(q-j)), smaller j first.  L=5, M=2,
+    n=3, integer F+B (columns d=1, d=2): [[3,3],[1,1],[2,3],[3,2],[1,1]].  Two partitions
+    tie at total 51 (closed form, Eq.1-3 / P:381-386):
+      (0,1)x1, (1,3)x1 on node 0; (3,4)x2 on node 1; (4,5)x2 on node 2 — stage times
+        3, 3, 2, 1: k* = 0, T1 = 9, T2 = (16-4+0-1)*3 = 33, T3 = 9, total 51;
+      (0,1)x2 on node 0; (1,2)x1, (2,3)x1 on node 1; (3,5)x2 on node 2 — stage times
+        3, 1, 2, 3: k* = 0, T1 = 9, T2 = 33, T3 = 9, total 51.
+    The first is reached with the smaller j at the layer split k=3 (node split (W(1), W(2))),
+    the second with (W(2), W(1)): the oracle keeps the smaller j."""
+    cd = [[3, 3], [1, 1], [2, 3], [3, 2], [1, 1]]
+    fwd, bwd = _cd_profile(cd)
+    first = [(0, 1, 1, 0, 0), (1, 3, 1, 0, 1), (3, 4, 2, 1, 0), (4, 5, 2, 2, 0)]
+    second = [(0, 1, 2, 0, 0), (1, 2, 1, 1, 0), (2, 3, 1, 1, 1), (3, 5, 2, 2, 0)]
+    for st in (first, second):
+        times = [stage_time(fwd, bwd, u, v, d) for (u, v, d, _, _) in st]
+        assert closed_form(times)[0] == 51.0
+    t = _both_oracles(fwd, bwd, 2, 3)
+    assert t["total"] == 51.0
+    assert t["stages"] == first
