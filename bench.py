@@ -48,65 +48,91 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi sampling of SM clock + throttle reasons during the timed region."""
+    """SM clock + clock-event (throttle) reasons of this rank's GPU, sampled DURING the timed
+    region: NVML polled every ~2 ms from a thread (nvidia-smi -lms as a fallback)."""
 
-    def __init__(self, index: int):
-        self.index = index
-        self.samples = []
-        self._proc = None
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []          # (sm_mhz, reasons bitmask)
+        self.sm_max = None
+        self._stop = threading.Event()
         self._thr = None
+        self._h = None
+        self._nvml = None
+
+    def _handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        self._nvml = pynvml
+        try:   # the physical GPU behind torch's device index (CUDA_VISIBLE_DEVICES remaps)
+            import torch
+            uuid = str(torch.cuda.get_device_properties(self.device).uuid)
+            return pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        except Exception:
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.device]) if vis and vis.split(",")[0].isdigit() else self.device
+            return pynvml.nvmlDeviceGetHandleByIndex(idx)
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
-            self._proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                           "--format=csv,noheader,nounits", "-lms", "100"],
-                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self._proc = None
-            return self
+            self._h = self._handle()
+            nv = self._nvml
+            self.sm_max = float(nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM))
 
-        def pump():
-            for line in self._proc.stdout:
-                parts = [x.strip() for x in line.split(",")]
-                if len(parts) >= 7:
-                    self.samples.append(parts)
-        self._thr = threading.Thread(target=pump, daemon=True)
+            def poll():
+                while not self._stop.is_set():
+                    try:
+                        mhz = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                        rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                        self.samples.append((float(mhz), int(rs)))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+        except Exception:
+            self._h = None
+
+            def poll():   # fallback: nvidia-smi every 20 ms
+                q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active")
+                try:
+                    proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                             "--format=csv,noheader,nounits", "-lms", "20"],
+                                            stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                except OSError:
+                    return
+                for line in proc.stdout:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) >= 3 and parts[0].replace(".", "").isdigit():
+                        self.sm_max = float(parts[1])
+                        self.samples.append((float(parts[0]), int(parts[2], 16)))
+                    if self._stop.is_set():
+                        break
+                proc.terminate()
+        self._thr = threading.Thread(target=poll, daemon=True)
         self._thr.start()
+        time.sleep(0.01)
         return self
 
     def __exit__(self, *a):
-        if self._proc:
-            self._proc.terminate()
-            try:
-                self._proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self._proc.kill()
+        self._stop.set()
         if self._thr:
-            self._thr.join(timeout=2)
+            self._thr.join(timeout=5)
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for s in self.samples:
-            for n, v in zip(names, s[3:7]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": self.sm_max, "reasons": ["unsampled"], "samples": 0}
+        reasons = sorted(n for n, bit in self.REASONS.items() if any(r & bit for _, r in self.samples))
+        return {"sm_mhz": statistics.median(m for m, _ in self.samples), "sm_max_mhz": self.sm_max,
+                "reasons": reasons, "samples": len(self.samples),
+                "source": "nvml" if self._h is not None else "nvidia-smi"}
 
 
 def cpu_oracle_sample(cfg, prof, n_hi_sample: int):
-    """Time the C oracle on templates n0..n_hi_sample of the workload profile (a bounded
-    sample: the full cfg4 set takes ~5 min single-threaded).  Returns a dict in cells/s of
-    the FULL workload, projected from the oracle's measured split rate (splits are the
-    per-unit cost of the recursion), plus the raw sample numbers."""
+    """Time the C oracle (oracle/c, one thread, as it stands) on templates n0..n_hi_sample of
+    the workload profile: a bounded sample of the workload (the full cfg4 set takes minutes
+    single-threaded).  Returns the raw sample numbers and the oracle's split rate."""
     from oracle import coracle
     t0 = time.perf_counter()
     _, (cells, splits) = coracle.template_set(prof.fwd_ms, prof.bwd_ms, cfg.M, cfg.n0, n_hi_sample)
@@ -115,13 +141,16 @@ def cpu_oracle_sample(cfg, prof, n_hi_sample: int):
 
 
 def run_reference(args, cfg):
+    """The reference arm: the oracle (the only reference this paper-only tier has) timed on
+    the host cores, on rank 0 only; it loads nothing from paper_2309_08125_b200/."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2309_08125_b200.planner import dp_info  # geometry counts only (no GPU work)
-    info = dp_info(cfg.L, cfg.M, cfg.n0, cfg.n_max, 1)
+    from oracle.count import universe
+    from workloads import config_profiles
+    cells_full, splits_full = universe(cfg.L, cfg.M, cfg.n_max)
     prof = config_profiles(cfg, "real")[0]
-    n_s = min(cfg.n_max, cfg.n0 + args.ref_sample_sizes - 1)
+    n_s = cfg.n_max if args.ref_full else min(cfg.n_max, cfg.n0 + args.ref_sample_sizes - 1)
     for _ in range(args.warmup):
         cpu_oracle_sample(cfg, prof, n_s)
     rates, secs = [], []
@@ -131,20 +160,27 @@ def run_reference(args, cfg):
         rates.append(last["splits_per_s"])
         secs.append(last["seconds"])
     sps = statistics.median(rates)
-    full_s = info.splits_per_profile / sps
-    value = info.cells_per_profile / full_s
-    sample = (f"C oracle (oracle/c, 1 thread) on {cfg.key} templates n={cfg.n0}..{n_s} "
-              f"({last['cells']} cells, {last['splits']} splits, {statistics.median(secs):.2f} s/step); "
-              f"cells/s of the full set projected from the measured split rate")
+    full = n_s == cfg.n_max
+    full_s = statistics.median(secs) if full else splits_full / sps
+    value = cells_full / full_s
+    if full:
+        sample = (f"C oracle (oracle/c, 1 thread) on the FULL {cfg.key} template set n={cfg.n0}..{cfg.n_max} "
+                  f"({last['cells']} cells, {last['splits']} splits, {statistics.median(secs):.2f} s/step)")
+    else:
+        sample = (f"C oracle (oracle/c, 1 thread) on the bounded sample {cfg.key} templates n={cfg.n0}..{n_s} "
+                  f"({last['cells']} cells, {last['splits']} splits, {statistics.median(secs):.2f} s/step); "
+                  f"value = cells/s of the full set PROJECTED from the sample's split rate "
+                  f"({splits_full} splits, oracle/count.py)")
     line = {"metric": METRIC, "value": value, "unit": "cells/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": statistics.median(secs) * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.key, "label": cfg.label, "L": cfg.L, "M": cfg.M, "N": cfg.N,
                        "f": cfg.f, "n0": cfg.n0, "sizes": [cfg.n0, cfg.n_max]},
-            "cpu_baseline": {"value": value, "unit": "cells/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "cells/s", "cores": 1, "kind": "oracle", "sample": sample,
+                             "projected": not full, "host_cpu": _cpu_model(), "host_cores": os.cpu_count()},
             "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "full_set_seconds_projected": full_s}
+            "full_set_seconds" + ("" if full else "_projected"): full_s}
     print(json.dumps(line), flush=True)
 
 
@@ -162,6 +198,8 @@ def main():
                     help="N > 1: all ranks plan ONE profile, wavefronts split across GPUs (strong scaling)")
     ap.add_argument("--ref-sample-sizes", type=int, default=5,
                     help="reference arm / cpu_baseline: number of template sizes in the sample")
+    ap.add_argument("--ref-full", action="store_true",
+                    help="reference arm: time the oracle on the full template set (minutes for cfg4)")
     args = ap.parse_args()
     cfg = CONFIGS[args.workload]
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
@@ -200,9 +238,10 @@ def main():
 
     shard = args.shard_profile and world > 1 and cfg.key != "cfg5"
     plan = planner.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, P)
-    comm = None
+    # the library's own NCCL communicator (torch.distributed only bootstraps its unique id):
+    # per-wavefront partial argmins (--shard-profile) or the packed template sets (batched)
+    comm = planner.NcclComm(world, rank, local) if world > 1 else None
     if shard:   # single-profile wavefront sharding: NCCL all-gather of partial argmins per wavefront
-        comm = planner.NcclComm(world, rank, local)
         plan.set_comm(comm)
     info = plan.info
     dev = torch.device("cuda", local)
@@ -217,7 +256,7 @@ def main():
     def step():
         plan.run(fwd.data_ptr(), bwd.data_ptr(), ws.data_ptr(), ws.numel(), packed.data_ptr(), sptr)
         if world > 1 and not shard:   # one NCCL all-gather assembles every rank's packed template sets
-            odist.allgather_packed(packed, info.packed_bytes)
+            odist.allgather_packed(packed, info.packed_bytes, comm=comm, stream=sptr)
 
     for _ in range(args.warmup):
         step()
@@ -291,22 +330,27 @@ def main():
     # e2e: through the public C ABI with host buffers (H2D of the profiles, D2H + host
     # template-set build inside the timed region), workspace preallocated by torch.
     hprofs = [planner.Profile.from_arrays(p.fwd_ms, p.bwd_ms) for p in profs]
-    e2e_ws = torch.empty(info.workspace_bytes + (4 << 20) + info.packed_bytes + 2 * 8 * cfg.L * cfg.M * P + (1 << 20),
-                         dtype=torch.uint8, device=dev)
+    e2e_ws = torch.empty(info.workspace_bytes + (world + 2) * info.packed_bytes + 2 * 8 * cfg.L * cfg.M * P * world +
+                         (8 << 20), dtype=torch.uint8, device=dev)
 
-    h_fwd = torch.from_numpy(np.stack([p.fwd_ms for p in profs])).pin_memory()
-    h_bwd = torch.from_numpy(np.stack([p.bwd_ms for p in profs])).pin_memory()
+    # the e2e call: every rank passes the job's profiles (all ranks' blocks, or the one
+    # sharded profile) and the library's communicator; each rank plans its share and gets
+    # the whole template set
+    if world > 1 and not shard:
+        if cfg.key == "cfg5":
+            all_profs = [random_profile(cfg.seed + i, cfg.L, cfg.M, "lognormal")
+                         for i in range(P * world if args.profiles_per_rank else cfg.num_profiles)]
+        else:
+            from workloads import gpt_profile
+            all_profs = [gpt_profile(cfg, cfg.seed + 1000 * i) for i in range(P * world)]
+        e2e_profs = [planner.Profile.from_arrays(p.fwd_ms, p.bwd_ms) for p in all_profs]
+    else:
+        e2e_profs = hprofs
 
     def e2e_step():
-        if shard:   # public DPPlan API: pinned H2D, sharded DP, D2H + host template set
-            fwd.copy_(h_fwd, non_blocking=True)
-            bwd.copy_(h_bwd, non_blocking=True)
-            plan.run(fwd.data_ptr(), bwd.data_ptr(), ws.data_ptr(), ws.numel(), packed.data_ptr(), sptr)
-            return plan.template_set(packed.cpu().numpy())
-        ts = planner.generate_templates(hprofs, nodes=cfg.N, gpus_per_node=cfg.M, f=cfg.f, n0=cfg.n0,
-                                        device=local, stream=sptr, workspace=e2e_ws.data_ptr(),
-                                        workspace_bytes=e2e_ws.numel())
-        return ts
+        return planner.generate_templates(e2e_profs, nodes=cfg.N, gpus_per_node=cfg.M, f=cfg.f, n0=cfg.n0,
+                                          device=local, stream=sptr, workspace=e2e_ws.data_ptr(),
+                                          workspace_bytes=e2e_ws.numel(), comm=comm)
 
     for _ in range(2):
         e2e_step()
@@ -322,7 +366,8 @@ def main():
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_s = float(e2e_s[0])
     e2e = {"value": cells_step / e2e_s, "unit": "cells/s",
-           "h2d_bytes_per_step": 2 * 8 * cfg.L * cfg.M * P, "d2h_bytes_per_step": int(info.packed_bytes),
+           "h2d_bytes_per_step": 2 * 8 * cfg.L * cfg.M * P,
+           "d2h_bytes_per_step": int(info.packed_bytes) * (world if world > 1 and not shard else 1),
            "planning_latency_ms": e2e_s * 1e3}
     # full-plan latency: template set (e2e) + instantiation/batch distribution at N
     t0 = time.perf_counter()

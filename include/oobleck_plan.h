@@ -79,6 +79,9 @@ typedef struct {
     void *workspace;            /* optional caller-owned device memory (NULL: library
                                    allocates and frees it inside the call) */
     size_t workspace_bytes;     /* size of `workspace` (>= oob_dp_plan_info.workspace_bytes) */
+    void *comm;                 /* optional ncclComm_t of `world` ranks (oob_nccl_comm_create),
+                                   borrowed; NULL or world <= 1: this GPU only */
+    int32_t world, rank;        /* ranks of `comm` and this process's rank */
 } oob_plan_opts;
 
 /* ------------------------------------------------------------------ errors */
@@ -117,8 +120,15 @@ oob_status oob_node_sizes(int32_t nodes, int32_t f, int32_t n0, int32_t layers,
  * argmin over S in n..min(L, nM) of the memoized recursion T(S, 0, L, W(n))
  * (Eqs.1-4).  Runs on the GPU (sm_100a): host arrays are copied to the device, the DP
  * wavefronts run, the packed templates are copied back.  `profiles` are num_profiles
- * handles with identical L and M (batched sweep).  Errors: OOB_E_INVALID, OOB_E_INFEASIBLE,
- * OOB_E_CUDA, OOB_E_NOMEM. */
+ * handles with identical L and M (batched sweep).
+ * Multi-GPU (opts.comm with world > 1; every rank calls with the same profiles and options
+ * on its own device, and every rank receives the whole template set, bit-identical to one
+ * GPU): num_profiles == 1 splits each large wavefront's W-cell work across the ranks (one
+ * all-gather of partial argmins per such wavefront, see oob_dp_set_comm); num_profiles > 1
+ * gives rank r the contiguous block of profiles [r*B + min(r, E), ...) (B = num/world,
+ * E = num%world, the first E ranks one extra), planned independently, then one
+ * ncclAllGather of the packed blocks.  Errors: OOB_E_INVALID, OOB_E_INFEASIBLE,
+ * OOB_E_CUDA, OOB_E_NCCL, OOB_E_NOMEM. */
 oob_status oob_generate_templates(const oob_profile *const *profiles, int32_t num_profiles,
                                   const oob_plan_opts *opts, oob_template_set **out);
 int32_t oob_template_set_profiles(const oob_template_set *s);
@@ -204,6 +214,23 @@ oob_status oob_nccl_unique_id(void *id_out);
 oob_status oob_nccl_comm_create(const void *id, int32_t world, int32_t rank, int32_t device, void **comm_out);
 void oob_nccl_comm_destroy(void *comm);
 oob_status oob_dp_set_comm(oob_dp_plan *plan, void *comm, int32_t world, int32_t rank);
+/* ncclAllGather of `bytes_per_rank` bytes per rank: d_recv[r * bytes_per_rank ...] receives
+ * rank r's d_send (device buffers, enqueued on `stream`).  Used to assemble packed
+ * template sets of batched sweeps.  Errors: OOB_E_INVALID, OOB_E_NCCL. */
+oob_status oob_nccl_allgather(void *comm, const void *d_send, void *d_recv, size_t bytes_per_rank,
+                              void *stream);
+/* Virtual shards (test mode of the single-profile sharding on ONE GPU):
+ * oob_dp_set_virtual_shards(plan, world) makes the plan split each large wavefront's units
+ * across `world` virtual ranks exactly as oob_dp_set_comm does; oob_dp_run_virtual then
+ * runs every virtual rank on the current device — per wavefront each rank's k_wave_w over
+ * its own workspace d_ws[r] (>= info.workspace_bytes after the call; re-read it), then
+ * device copies in place of the all-gather, then each rank's finalize — and writes rank r's
+ * packed templates to d_packed[r].  Every rank's output must equal a 1-GPU run.  world = 1
+ * restores a plain plan.  Errors: OOB_E_INVALID, OOB_E_NOMEM, OOB_E_CUDA. */
+oob_status oob_dp_set_virtual_shards(oob_dp_plan *plan, int32_t world);
+oob_status oob_dp_run_virtual(oob_dp_plan *plan, const double *d_fwd, const double *d_bwd,
+                              void *const *d_workspace, size_t workspace_bytes,
+                              void *const *d_packed, void *stream);
 
 /* Build a template set from a HOST copy of the packed output (d_packed copied back). */
 oob_status oob_template_set_from_packed(const void *h_packed, const oob_dp_info *info,

@@ -42,7 +42,7 @@ class OobPlanOpts(ctypes.Structure):
     _fields_ = [("nodes", c_int32), ("gpus_per_node", c_int32), ("f", c_int32), ("n0", c_int32),
                 ("gpu_mem_bytes", c_int64), ("util", c_double), ("samples_per_gpu", c_int32),
                 ("device", c_int32), ("stream", c_void_p), ("workspace", c_void_p),
-                ("workspace_bytes", c_size_t)]
+                ("workspace_bytes", c_size_t), ("comm", c_void_p), ("world", c_int32), ("rank", c_int32)]
 
 
 class OobDpInfo(ctypes.Structure):
@@ -89,6 +89,9 @@ _proto("oob_nccl_unique_id", ctypes.c_int, [c_void_p])
 _proto("oob_nccl_comm_create", ctypes.c_int, [c_void_p, c_int32, c_int32, c_int32, P(c_void_p)])
 _proto("oob_nccl_comm_destroy", None, [c_void_p])
 _proto("oob_dp_set_comm", ctypes.c_int, [c_void_p, c_void_p, c_int32, c_int32])
+_proto("oob_nccl_allgather", ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_size_t, c_void_p])
+_proto("oob_dp_set_virtual_shards", ctypes.c_int, [c_void_p, c_int32])
+_proto("oob_dp_run_virtual", ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p])
 _proto("oob_instantiate", ctypes.c_int, [c_void_p, c_int32, c_int32, c_int32, c_int64, c_int32, c_int64,
                                          c_void_p, c_void_p, c_int32, P(c_int32), P(c_double), P(c_double),
                                          P(c_int64), P(c_int64)])
@@ -105,7 +108,7 @@ EXPORTED = [
     "oob_dp_plan_info", "oob_dp_run", "oob_dp_set_timing", "oob_dp_kernel_time",
     "oob_template_set_from_packed", "oob_instantiate", "oob_count_sets", "oob_distribute_batch",
     "oob_recommend_batch", "oob_nccl_unique_id", "oob_nccl_comm_create", "oob_nccl_comm_destroy",
-    "oob_dp_set_comm",
+    "oob_dp_set_comm", "oob_nccl_allgather", "oob_dp_set_virtual_shards", "oob_dp_run_virtual",
 ]
 NCCL_ID_BYTES = 128
 

@@ -60,3 +60,11 @@ extern "C" oob_status oob_nccl_comm_create(const void *id, int32_t world, int32_
 extern "C" void oob_nccl_comm_destroy(void *comm) {
     if (comm) ncclCommDestroy((ncclComm_t)comm);
 }
+
+extern "C" oob_status oob_nccl_allgather(void *comm, const void *d_send, void *d_recv, size_t bytes_per_rank,
+                                         void *stream) {
+    if (!comm || !d_send || !d_recv) return fail(OOB_E_INVALID, "oob_nccl_allgather: NULL argument");
+    ncclResult_t r = ncclAllGather(d_send, d_recv, bytes_per_rank, ncclInt8, (ncclComm_t)comm, (cudaStream_t)stream);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather (packed template sets)");
+    return OOB_OK;
+}

@@ -106,9 +106,22 @@ __global__ void k_wave_v1(DevGeom g, int l) {
 }
 
 // ------------------------------------------------------------------ K_extract
-// One thread per (profile, template size n): argmin over S (strict <, smaller S wins),
-// then the split-tree backtrack (left child first => stages in pipeline order).
+// One warp per (profile, template size n).  Choice of S: the lanes evaluate
+// S = n + lane, n + lane + 32, ... and the warp takes the lexicographic minimum of
+// (total, S) — the oracle's "first strictly smaller total" scan in ascending S (smaller S
+// wins ties, reading R8).  Backtrack: the split tree level by level, the warp expanding a
+// level's nodes in parallel; a node carries the index of its first stage (its left child
+// keeps it, its right child starts s stages later), so every leaf (S' = 1) writes its stage
+// record straight into pipeline order.  Frontier: two buffers of <= L + 1 nodes in shared
+// memory (dynamic, 2 x (L+1) x 16 bytes per warp).
+struct XNode {
+    uint64_t key;      // Sp | u << 10 | v << 20 | a << 30 | node << 41 | goff << 51 (goff < 64)
+    int32_t first;     // stage index of the node's first stage
+    int32_t pad;
+};
+
 __global__ void k_extract(DevGeom g, unsigned char *packed, size_t tpl_bytes, Pipe pp) {
+    extern __shared__ __align__(16) unsigned char xsm[];
     __shared__ int s_err;
     if (threadIdx.x == 0) {
         s_err = 0;
@@ -118,8 +131,9 @@ __global__ void k_extract(DevGeom g, unsigned char *packed, size_t tpl_bytes, Pi
         }
     }
     __syncthreads();
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int p_cnt = g.n_hi - g.n_lo + 1;
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.x * (blockDim.x >> 5) + wib;
     if (t >= p_cnt * g.P) return;
     const int p = t / p_cnt;
     const int n = g.n_lo + t % p_cnt;
@@ -128,62 +142,99 @@ __global__ void k_extract(DevGeom g, unsigned char *packed, size_t tpl_bytes, Pi
     const int aW = (g.M - 1) + n - 1;
     PackedHeader *h = reinterpret_cast<PackedHeader *>(packed + (size_t)t * tpl_bytes);
     int32_t *st = reinterpret_cast<int32_t *>(h + 1);
-    int bestS = -1;
-    double best = 0.0;
+    // argmin over S: lexicographic (total, S)
     const int Smax = min(L, n * g.M);
-    for (int S = n; S <= Smax; ++S) {
+    double best = __longlong_as_double(0x7ff0000000000000LL);
+    int bestS = 0x7FFFFFFF;
+    for (int S = n + lane; S <= Smax; S += 32) {
         const Cell4 c = d_load(g.CELL + pc + d_cell(g, S, 0, L, aW));
         const double T2 = __dmul_rn(c.C1, c.TS);      // (4S - S + k* - 1) t*, Eq.2
         const double tot = __dadd_rn(__dadd_rn(c.T1, T2), c.T3);
-        if (bestS < 0 || tot < best) { best = tot; bestS = S; }
+        if (tot < best || (tot == best && S < bestS)) { best = tot; bestS = S; }
     }
-    const Cell4 c = d_load(g.CELL + pc + d_cell(g, bestS, 0, L, aW));
-    h->nodes = n; h->S = bestS; h->kstar = (int)d_kd(c.C1, bestS);
-    h->status = s_err ? 2 : 0;        // 2: pipeline wait timed out (OOB_E_CUDA on the host)
-    h->T1 = c.T1; h->T3 = c.T3; h->tstar = c.TS;
-    h->T2 = __dmul_rn(c.C1, c.TS);
-    h->iter = best;
-    h->pad = 0.0;
-    // explicit DFS stack in the workspace (<= L pending entries): packed
-    // Sp | u<<10 | v<<20 | a<<30 | node<<41 | goff<<51
-    uint64_t *stk = g.STK + (size_t)t * (size_t)(L + 1);
+    for (int d = 16; d >= 1; d >>= 1) {
+        const double ob = __shfl_xor_sync(0xFFFFFFFFu, best, d);
+        const int os = __shfl_xor_sync(0xFFFFFFFFu, bestS, d);
+        if (ob < best || (ob == best && os < bestS)) { best = ob; bestS = os; }
+    }
+    int status = s_err ? 2 : 0;       // 2: pipeline wait timed out (OOB_E_CUDA on the host)
+    if (lane == 0) {
+        const Cell4 c = d_load(g.CELL + pc + d_cell(g, bestS, 0, L, aW));
+        h->nodes = n; h->S = bestS; h->kstar = (int)d_kd(c.C1, bestS);
+        h->T1 = c.T1; h->T3 = c.T3; h->tstar = c.TS;
+        h->T2 = __dmul_rn(c.C1, c.TS);
+        h->iter = best;
+        h->pad = 0.0;
+    }
     auto pack = [](int Sp, int u, int v, int a, int node, int goff) -> uint64_t {
         return (uint64_t)Sp | ((uint64_t)u << 10) | ((uint64_t)v << 20) | ((uint64_t)a << 30) |
                ((uint64_t)node << 41) | ((uint64_t)goff << 51);
     };
-    int top = 0, ns = 0;
-    stk[top++] = pack(bestS, 0, L, aW, 0, 0);
-    while (top > 0) {
-        const uint64_t e = stk[--top];
-        const int Sp = (int)(e & 1023u), u = (int)((e >> 10) & 1023u), v = (int)((e >> 20) & 1023u);
-        const int a = (int)((e >> 30) & 2047u), node = (int)((e >> 41) & 1023u), goff = (int)((e >> 51) & 63u);
-        if (Sp == 1) {
-            int32_t *r = st + 5 * ns;
-            r[0] = u; r[1] = v; r[2] = d_is_whole(g, a) ? g.M : d_alloc_n(g, a); r[3] = node; r[4] = goff;
-            ++ns;
-            continue;
+    XNode *fr[2];
+    fr[0] = reinterpret_cast<XNode *>(xsm) + (size_t)wib * 2 * (L + 1);
+    fr[1] = fr[0] + (L + 1);
+    int cnt = 1, cur = 0;
+    if (lane == 0) fr[0][0] = XNode{pack(bestS, 0, L, aW, 0, 0), 0, 0};
+    __syncwarp();
+    bool bad = false;
+    while (cnt > 0) {
+        int next = 0;
+        for (int i0 = 0; i0 < cnt; i0 += 32) {
+            const int i = i0 + lane;
+            XNode c0{0, 0, 0}, c1{0, 0, 0};
+            int nout = 0;
+            if (i < cnt) {
+                const XNode nd = fr[cur][i];
+                const uint64_t e = nd.key;
+                const int Sp = (int)(e & 1023u), u = (int)((e >> 10) & 1023u), v = (int)((e >> 20) & 1023u);
+                const int a = (int)((e >> 30) & 2047u), node = (int)((e >> 41) & 1023u), goff = (int)((e >> 51) & 63u);
+                if (Sp == 1) {
+                    if (nd.first < L) {
+                        int32_t *r = st + 5 * nd.first;
+                        r[0] = u; r[1] = v; r[2] = d_is_whole(g, a) ? g.M : d_alloc_n(g, a); r[3] = node; r[4] = goff;
+                    } else {
+                        bad = true;
+                    }
+                } else {
+                    const uint32_t arg = g.ARG[pc + d_cell(g, Sp, u, v - u, a)];
+                    const int k = u + (int)(arg & 1023u) + 1;
+                    const int j = (int)((arg >> 10) & 1023u);
+                    const int s = (int)(arg >> 20);
+                    if (arg >= 0xFFFFFFFDu || k <= u || k >= v || s < 1 || s >= Sp || j >= d_num_dsplits(g, a)) {
+                        bad = true;           // corrupt split (never for a valid table)
+                    } else {
+                        int a1, a2;
+                        d_dsplit(g, a, j, a1, a2);
+                        const bool wsplit = d_is_whole(g, a) && d_alloc_n(g, a) >= 2;
+                        c0 = XNode{pack(s, u, k, a1, node, wsplit ? 0 : goff), nd.first, 0};
+                        c1 = XNode{wsplit ? pack(Sp - s, k, v, a2, node + d_alloc_n(g, a1), 0)
+                                          : pack(Sp - s, k, v, a2, node, goff + d_alloc_n(g, a1)),
+                                   nd.first + s, 0};
+                        nout = 2;
+                    }
+                }
+            }
+            // compact the children into the next frontier
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, nout > 0);
+            const int pos = next + 2 * __popc(bal & ((1u << lane) - 1u));
+            if (nout > 0 && pos + 1 <= L) {
+                fr[cur ^ 1][pos] = c0;
+                fr[cur ^ 1][pos + 1] = c1;
+            } else if (nout > 0) {
+                bad = true;
+            }
+            next += 2 * __popc(bal);
         }
-        const uint32_t arg = g.ARG[pc + d_cell(g, Sp, u, v - u, a)];
-        const int k = u + (int)(arg & 1023u) + 1;
-        const int j = (int)((arg >> 10) & 1023u);
-        const int s = (int)(arg >> 20);
-        if (arg >= 0xFFFFFFFDu || k <= u || k >= v || s < 1 || s >= Sp || j >= d_num_dsplits(g, a) ||
-            top + 2 > L + 1) {   // corrupt split (never for a valid table): flag the template, stop
-            h->status = h->status ? h->status : 1;
-            break;
-        }
-        int a1, a2;
-        d_dsplit(g, a, j, a1, a2);
-        const bool wsplit = d_is_whole(g, a) && d_alloc_n(g, a) >= 2;
-        // push right, then left (popped first => stages come out in pipeline order)
-        stk[top++] = wsplit ? pack(Sp - s, k, v, a2, node + d_alloc_n(g, a1), 0)
-                            : pack(Sp - s, k, v, a2, node, goff + d_alloc_n(g, a1));
-        stk[top++] = pack(s, u, k, a1, node, wsplit ? 0 : goff);
+        __syncwarp();
+        cnt = min(next, L + 1);
+        cur ^= 1;
     }
-    for (int i = ns; i < L; ++i) {
+    if (__any_sync(0xFFFFFFFFu, bad) && !status) status = 1;
+    for (int i = bestS + lane; i < L; i += 32) {
         int32_t *r = st + 5 * i;
         r[0] = r[1] = r[2] = r[3] = r[4] = -1;
     }
+    if (lane == 0) h->status = status;
 }
 
 }  // namespace oob
@@ -283,7 +334,7 @@ struct oob_dp_plan {
     std::vector<std::pair<int, void *>> dev_geom;   // plan-owned device copies, per device
     size_t off_cells = 0, off_base = 0, off_off = 0, off_wofs = 0, off_pexp = 0, off_tiles = 0, off_tile_off = 0,
            off_tile_cnt = 0, off_items = 0;
-    size_t off_CELL = 0, off_SH = 0, off_ARG = 0, off_STK = 0, off_GACC = 0, off_GFILT = 0, off_CTR = 0;
+    size_t off_CELL = 0, off_SH = 0, off_ARG = 0, off_GACC = 0, off_GFILT = 0, off_CTR = 0;
     int64_t gacc_n = 0;
     void *comm = nullptr;                // ncclComm_t (single-profile sharding), world > 1
     int rank = 0, world = 1;
@@ -513,7 +564,6 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     pl->off_CELL = o; o = align_up(o + 32 * (n + 16 + XR_CELLS), 256);   // + padding: row streams read ahead
     pl->off_SH = o; o = align_up(o + 16 * (n + 16 + XR_CELLS), 256);     // shadow lower bounds (+ padding)
     pl->off_ARG = o; o = align_up(o + 4 * n, 256);
-    pl->off_STK = o; o = align_up(o + 8 * (size_t)num_profiles * (n_hi - n_lo + 1) * (L + 1), 256);
     pl->gacc_n = (int64_t)gacc_max;
     pl->off_GACC = o; o = align_up(o + 3 * 16 * gacc_max, 256);   // three buffers (wave mod 3)
     pl->off_GFILT = o; o = align_up(o + 3 * 4 * gacc_max, 256);   // their filters
@@ -602,6 +652,14 @@ static oob_status plan_geometry(oob_dp_plan *pl, unsigned char **geo) {
     if (e != cudaSuccess) return fail(OOB_E_NOMEM, std::string("cudaMalloc plan geometry: ") + cudaGetErrorString(e));
     e = cudaMemcpy(p, pl->geom_blob.data(), pl->geom_bytes, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) { cudaFree(p); return cuda_fail(e, "plan geometry upload"); }
+    {
+        const size_t xs = 2 * 2 * (size_t)(pl->g.L + 1) * sizeof(XNode);
+        if (xs > 48 * 1024 && (e = cudaFuncSetAttribute(k_extract, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xs)) !=
+                                  cudaSuccess) {
+            cudaFree(p);
+            return cuda_fail(e, "cudaFuncSetAttribute(k_extract)");
+        }
+    }
     if (pl->kernel == 2) {
         const int sm = (int)std::max<size_t>(pl->max_smem, 48 * 1024);
         e = cudaFuncSetAttribute(k_wave_w<TE_W>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
@@ -753,46 +811,64 @@ static cudaError_t launch_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglon
     return cudaGetLastError();
 }
 
-extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const double *d_bwd,
-                                 void *d_ws, size_t ws_bytes, void *d_packed, void *stream_) {
-    if (!pl || !d_fwd || !d_bwd || !d_ws || !d_packed)
-        return fail(OOB_E_INVALID, "oob_dp_run: NULL argument");
-    if (ws_bytes < pl->ws_bytes) return fail(OOB_E_NOMEM, "oob_dp_run: workspace too small");
-    cudaStream_t stream = (cudaStream_t)stream_;
+// One rank's state of a run: its workspace (tables, accumulators, counters) and output.
+struct RankRun {
+    unsigned char *ws;
+    unsigned char *packed;
+    int rank;
+    DevGeom dg;
+    ulonglong2 *gacc;
+    int *ctr;
+    Pipe pp;
+};
+
+// The template set for `nr` local rank contexts on the current device and stream.
+// nr = 1: one GPU (world = 1) or this process's rank of an NCCL-sharded plan; nr = world > 1
+// with comm = NULL: virtual shards — every rank's kernels run on this device, one after the
+// other per wavefront, and the all-gather of the partial argmins is a set of device copies
+// (the sharded algorithm, checkable on one GPU).
+static oob_status run_ranks(oob_dp_plan *pl, const double *d_fwd, const double *d_bwd, RankRun *rr, int nr,
+                            cudaStream_t stream) {
     const Geometry &G = pl->g;
-    unsigned char *ws = (unsigned char *)d_ws;
     unsigned char *geo = nullptr;
     oob_status gs = plan_geometry(pl, &geo);
     if (gs != OOB_OK) return gs;
     cudaError_t e;
-    DevGeom dg;
-    dg.L = G.L; dg.M = G.M; dg.n_lo = G.n_lo; dg.n_hi = G.n_hi; dg.A = G.A; dg.P = pl->P;
-    dg.C = G.table_cells;
-    dg.cells = (const int32_t *)(geo + pl->off_cells);
-    dg.base = (const int64_t *)(geo + pl->off_base);
-    dg.off = (const int32_t *)(geo + pl->off_off);
-    dg.wofs = (const int32_t *)(geo + pl->off_wofs);
-    dg.CELL = (Cell4 *)(ws + pl->off_CELL);
-    dg.SH = (float4 *)(ws + pl->off_SH);
-    dg.ARG = (uint32_t *)(ws + pl->off_ARG);
-    dg.STK = (uint64_t *)(ws + pl->off_STK);
-
-    ulonglong2 *gacc = (ulonglong2 *)(ws + pl->off_GACC);
-    int *ctr = (int *)(ws + pl->off_CTR);
-    {   // every run starts from a clean workspace state: accumulators, filters, counters
-        const int64_t nacc = pl->kernel == 2 ? 3 * pl->gacc_n : 0;
-        const int64_t nmax = std::max<int64_t>(nacc, (int64_t)pl->ctr_n + 1);
-        k_init<<<(unsigned)((nmax + 255) / 256), 256, 0, stream>>>(gacc, gfilt_of(pl, gacc, 0), nacc, ctr,
-                                                                  (int64_t)pl->ctr_n + 1);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return cuda_fail(e, "k_init launch");
-    }
-    {   // K_base: grid.y = l
-        int64_t maxn = (int64_t)G.L * G.M * pl->P;
-        dim3 grid((unsigned)((maxn + 255) / 256), (unsigned)G.L);
-        k_base<<<grid, 256, 0, stream>>>(dg, d_fwd, d_bwd);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return cuda_fail(e, "k_base launch");
+    const bool pipe_on = pl->pipe_on;
+    for (int i = 0; i < nr; ++i) {
+        RankRun &R = rr[i];
+        DevGeom &dg = R.dg;
+        dg.L = G.L; dg.M = G.M; dg.n_lo = G.n_lo; dg.n_hi = G.n_hi; dg.A = G.A; dg.P = pl->P;
+        dg.C = G.table_cells;
+        dg.cells = (const int32_t *)(geo + pl->off_cells);
+        dg.base = (const int64_t *)(geo + pl->off_base);
+        dg.off = (const int32_t *)(geo + pl->off_off);
+        dg.wofs = (const int32_t *)(geo + pl->off_wofs);
+        dg.CELL = (Cell4 *)(R.ws + pl->off_CELL);
+        dg.SH = (float4 *)(R.ws + pl->off_SH);
+        dg.ARG = (uint32_t *)(R.ws + pl->off_ARG);
+        R.gacc = (ulonglong2 *)(R.ws + pl->off_GACC);
+        R.ctr = (int *)(R.ws + pl->off_CTR);
+        R.pp.cnt = R.ctr + pl->pipe_cnt_off;
+        R.pp.expc = (const int *)(geo + pl->off_pexp);
+        R.pp.err = R.pp.cnt + 3 * (G.L + 2);
+        R.pp.on = pipe_on ? 1 : 0;
+        R.pp.spin_max = pl->kn.spin_max;
+        {   // every run starts from a clean workspace state: accumulators, filters, counters
+            const int64_t nacc = pl->kernel == 2 ? 3 * pl->gacc_n : 0;
+            const int64_t nmax = std::max<int64_t>(nacc, (int64_t)pl->ctr_n + 1);
+            k_init<<<(unsigned)((nmax + 255) / 256), 256, 0, stream>>>(R.gacc, gfilt_of(pl, R.gacc, 0), nacc, R.ctr,
+                                                                      (int64_t)pl->ctr_n + 1);
+            if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_init launch");
+        }
+        {   // K_base: grid.y = l
+            int64_t maxn = (int64_t)G.L * G.M * pl->P;
+            dim3 grid((unsigned)((maxn + 255) / 256), (unsigned)G.L);
+            k_base<<<grid, 256, 0, stream>>>(dg, d_fwd, d_bwd);
+            if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_base launch");
+        }
+        if (pl->kernel == 2 && G.L >= 2 && (e = launch_fin(pl, dg, R.gacc, 0, 2, stream)) != cudaSuccess)
+            return cuda_fail(e, "k_fin launch");
     }
     if (pl->timing) {
         size_t need = 2 * (size_t)(G.L - 1) + pl->ev_used;
@@ -803,72 +879,63 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
             pl->ev.push_back(ev);
         }
     }
-    const bool pipe_on = pl->pipe_on;
-    Pipe pp;
-    pp.cnt = ctr + pl->pipe_cnt_off;
-    pp.expc = (const int *)(geo + pl->off_pexp);
-    pp.err = pp.cnt + 3 * (G.L + 2);
-    pp.on = pipe_on ? 1 : 0;
-    pp.spin_max = pl->kn.spin_max;
-    if (pl->kernel == 2 && G.L >= 2 && (e = launch_fin(pl, dg, gacc, 0, 2, stream)) != cudaSuccess)
-        return cuda_fail(e, "k_fin launch");
     for (int l = 2; l <= G.L; ++l) {
         if (pl->kernel == 1) {
             int64_t n = (int64_t)(G.L - l + 1) * G.cells[l] * pl->P;
             if (n == 0) continue;
             if (pl->timing) cudaEventRecord(pl->ev[pl->ev_used], stream);
-            k_wave_v1<<<(unsigned)((n + 127) / 128), 128, 0, stream>>>(dg, l);
+            for (int i = 0; i < nr; ++i) k_wave_v1<<<(unsigned)((n + 127) / 128), 128, 0, stream>>>(rr[i].dg, l);
             if (pl->timing) { cudaEventRecord(pl->ev[pl->ev_used + 1], stream); pl->ev_used += 2; }
-            e = cudaGetLastError();
-            if (e != cudaSuccess) return cuda_fail(e, "k_wave_v1 launch");
+            if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_wave_v1 launch");
             continue;
         }
         const WaveHost &wh = pl->waves[l];
-        WaveW w;
-        w.l = l;
-        w.nranges = G.L - l + 1;
-        w.cpr = wh.cpr;
-        w.nents = wh.nents;
-        w.ents = (const int4 *)(geo + pl->off_items + wh.ents_off);
-        w.upre = (const int32_t *)(geo + pl->off_items + wh.upre_off);
-        w.cb = (const int32_t *)(geo + pl->off_items + wh.cb_off);
-        w.ncb = (int)wh.cb.size();
-        w.ctr = ctr + wh.ctr_off;
-        w.nunits = wh.nunits;
-        w.seeded = wh.seed;
-        w.nout = wh.nout;
-        w.GACC = gacc_of(pl, gacc, l);
-        w.GFILT = gfilt_of(pl, gacc, l);
-        w.tile_off = (const int32_t *)(geo + pl->off_tile_off);
-        w.tile_cnt = (const int32_t *)(geo + pl->off_tile_cnt);
-        w.tiles = (const int32_t *)(geo + pl->off_tiles);
         // shard only wavefronts whose work outweighs the all-gather (~10-20 us on NVLink);
         // short wavefronts run redundantly on every rank (identical results, no exchange)
         const bool shard = pl->world > 1 && (double)G.wave_splits[l] * pl->P >= pl->kn.shard_min;
-        w.rank = shard ? pl->rank : 0;
-        w.world = shard ? pl->world : 1;
-        const int64_t ctas = wh.nents > 0 ? (int64_t)pl->P * w.nranges * w.cpr : 0;
+        const int64_t ctas = wh.nents > 0 ? (int64_t)pl->P * (G.L - l + 1) * wh.cpr : 0;
         // fused finalize (OOB_DP_FUSE=1): unsharded waves finalize in k_wave_w's last CTAs
         // and run the next wave's in-node cells and seeds in extra blocks
         const bool fused = pl->kn.fuse_fin && ctas > 0 && !shard;
-        int64_t aux = 0;
-        w.nbmain = (int)ctas;
-        w.refresh = pl->kn.refresh && wh.cpr > 1;   // one CTA per range: its own filter is current
-        // batched sweeps (one CTA per range, small shared memory, a larger L1): the exact
-        // path's children are worth warming in L1 (cfg5 -2%; neutral to negative for cfg4)
-        w.prefetch = wh.cpr == 1 && pl->P > 1;
-        w.fin_inline = fused ? 1 : 0;
-        w.rdone = ctr + wh.done_off;
-        w.rclaim = w.rdone + (size_t)pl->P * w.nranges;
-        if (fused) {
-            int64_t nbs = 0, nbw = 0;
-            w.fa = make_fin(pl, dg, gacc, 0, l < G.L ? l + 1 : 0, false, &nbs);
-            w.fw = make_fin(pl, dg, gacc, l, 0, false, &nbw);
-            aux = w.fa.nbseed + nbs;
-        }
         if (pl->timing && (!pipe_on || l == 2)) cudaEventRecord(pl->ev[pl->ev_used], stream);
-        w.pp = pp;
-        if (ctas > 0) {
+        for (int i = 0; i < nr && ctas > 0; ++i) {
+            RankRun &R = rr[i];
+            WaveW w;
+            w.l = l;
+            w.nranges = G.L - l + 1;
+            w.cpr = wh.cpr;
+            w.nents = wh.nents;
+            w.ents = (const int4 *)(geo + pl->off_items + wh.ents_off);
+            w.upre = (const int32_t *)(geo + pl->off_items + wh.upre_off);
+            w.cb = (const int32_t *)(geo + pl->off_items + wh.cb_off);
+            w.ncb = (int)wh.cb.size();
+            w.ctr = R.ctr + wh.ctr_off;
+            w.nunits = wh.nunits;
+            w.seeded = wh.seed;
+            w.nout = wh.nout;
+            w.GACC = gacc_of(pl, R.gacc, l);
+            w.GFILT = gfilt_of(pl, R.gacc, l);
+            w.tile_off = (const int32_t *)(geo + pl->off_tile_off);
+            w.tile_cnt = (const int32_t *)(geo + pl->off_tile_cnt);
+            w.tiles = (const int32_t *)(geo + pl->off_tiles);
+            w.rank = shard ? R.rank : 0;
+            w.world = shard ? pl->world : 1;
+            int64_t aux = 0;
+            w.nbmain = (int)ctas;
+            w.refresh = pl->kn.refresh && wh.cpr > 1;   // one CTA per range: its own filter is current
+            // batched sweeps (one CTA per range, small shared memory, a larger L1): the exact
+            // path's children are worth warming in L1 (cfg5 -2%; neutral to negative for cfg4)
+            w.prefetch = wh.cpr == 1 && pl->P > 1;
+            w.fin_inline = fused ? 1 : 0;
+            w.rdone = R.ctr + wh.done_off;
+            w.rclaim = w.rdone + (size_t)pl->P * w.nranges;
+            if (fused) {
+                int64_t nbs = 0, nbw = 0;
+                w.fa = make_fin(pl, R.dg, R.gacc, 0, l < G.L ? l + 1 : 0, false, &nbs);
+                w.fw = make_fin(pl, R.dg, R.gacc, l, 0, false, &nbw);
+                aux = w.fa.nbseed + nbs;
+            }
+            w.pp = R.pp;
             const unsigned grid = (unsigned)(ctas + aux);
             if (pipe_on && l >= 3) {   // programmatic dependent of wave l-1 (counters, not the boundary)
                 cudaLaunchConfig_t lc = {};
@@ -881,34 +948,82 @@ extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const dou
                 at[0].val.programmaticStreamSerializationAllowed = 1;
                 lc.attrs = at;
                 lc.numAttrs = 1;
-                e = cudaLaunchKernelEx(&lc, k_wave_w<TE_W>, dg, w);
+                e = cudaLaunchKernelEx(&lc, k_wave_w<TE_W>, R.dg, w);
                 if (e != cudaSuccess) return cuda_fail(e, "k_wave_w launch (pipelined)");
             } else {
-                k_wave_w<TE_W><<<grid, NTW, wh.smem, stream>>>(dg, w);
+                k_wave_w<TE_W><<<grid, NTW, wh.smem, stream>>>(R.dg, w);
             }
+            if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_wave_w launch");
         }
         if (pl->timing && (!pipe_on || l == G.L)) {
             cudaEventRecord(pl->ev[pl->ev_used + 1], stream);
             pl->ev_used += 2;
         }
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return cuda_fail(e, "k_wave_w launch");
-        if (shard) {   // one all-gather of the wave's partial argmins (every rank finalizes all)
-            const size_t bytes = 16 * (size_t)pl->P * w.nranges * w.nout;
-            oob_status st = nccl_allgather_bytes(pl->comm, gacc_of(pl, gacc, l), ws + pl->off_GPART,
-                                                 bytes, 16 * (size_t)pl->gacc_n, pl->world, stream);
-            if (st != OOB_OK) return st;
+        if (shard) {   // all-gather of the wave's partial argmins (every rank finalizes all)
+            const size_t bytes = 16 * (size_t)pl->P * (G.L - l + 1) * wh.nout;
+            if (pl->comm) {
+                oob_status st = nccl_allgather_bytes(pl->comm, gacc_of(pl, rr[0].gacc, l), rr[0].ws + pl->off_GPART,
+                                                     bytes, 16 * (size_t)pl->gacc_n, pl->world, stream);
+                if (st != OOB_OK) return st;
+            } else {   // virtual shards: rank r's partial into slot r of every rank's gather buffer
+                for (int d = 0; d < nr; ++d)
+                    for (int r = 0; r < nr; ++r) {
+                        e = cudaMemcpyAsync(rr[d].ws + pl->off_GPART + (size_t)rr[r].rank * bytes,
+                                            gacc_of(pl, rr[r].gacc, l), bytes, cudaMemcpyDeviceToDevice, stream);
+                        if (e != cudaSuccess) return cuda_fail(e, "virtual-shard gather copy");
+                    }
+            }
         }
-        if (!fused && (e = launch_fin(pl, dg, gacc, l, l < G.L ? l + 1 : 0, stream, shard)) != cudaSuccess)
-            return cuda_fail(e, "k_fin launch");
+        for (int i = 0; i < nr && !fused; ++i)
+            if ((e = launch_fin(pl, rr[i].dg, rr[i].gacc, l, l < G.L ? l + 1 : 0, stream, shard)) != cudaSuccess)
+                return cuda_fail(e, "k_fin launch");
     }
-    {
-        int n = (G.n_hi - G.n_lo + 1) * pl->P;
-        k_extract<<<(n + 63) / 64, 64, 0, stream>>>(dg, (unsigned char *)d_packed, pl->tpl_bytes, pp);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return cuda_fail(e, "k_extract launch");
+    for (int i = 0; i < nr; ++i) {
+        // one warp per template; 2 warps per block (frontier: 2 x (L+1) nodes of 16 B per warp)
+        const int n = (G.n_hi - G.n_lo + 1) * pl->P;
+        const size_t xs = 2 * 2 * (size_t)(G.L + 1) * sizeof(XNode);
+        k_extract<<<(n + 1) / 2, 64, xs, stream>>>(rr[i].dg, rr[i].packed, pl->tpl_bytes, rr[i].pp);
+        if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_extract launch");
     }
     return OOB_OK;
+}
+
+extern "C" oob_status oob_dp_run(oob_dp_plan *pl, const double *d_fwd, const double *d_bwd,
+                                 void *d_ws, size_t ws_bytes, void *d_packed, void *stream_) {
+    if (!pl || !d_fwd || !d_bwd || !d_ws || !d_packed)
+        return fail(OOB_E_INVALID, "oob_dp_run: NULL argument");
+    if (ws_bytes < pl->ws_bytes) return fail(OOB_E_NOMEM, "oob_dp_run: workspace too small");
+    if (pl->world > 1 && !pl->comm)
+        return fail(OOB_E_INVALID, "oob_dp_run: plan has virtual shards; use oob_dp_run_virtual");
+    RankRun r{(unsigned char *)d_ws, (unsigned char *)d_packed, pl->rank, {}, nullptr, nullptr, {}};
+    return run_ranks(pl, d_fwd, d_bwd, &r, 1, (cudaStream_t)stream_);
+}
+
+extern "C" oob_status oob_dp_set_virtual_shards(oob_dp_plan *pl, int32_t world) {
+    if (!pl || world < 1 || world > 64) return fail(OOB_E_INVALID, "oob_dp_set_virtual_shards: bad argument");
+    if (world > 1 && pl->kernel != 2)
+        return fail(OOB_E_INVALID, "oob_dp_set_virtual_shards: sharding needs the W-kernel path");
+    pl->comm = nullptr;
+    pl->world = world;
+    pl->rank = 0;
+    pl->off_GPART = pl->ws_bytes_base;
+    pl->ws_bytes = pl->ws_bytes_base + (world > 1 ? align_up(16 * (size_t)world * pl->gacc_n, 256) : 0);
+    pl->pipe_on = plan_pipe_on(pl);
+    return OOB_OK;
+}
+
+extern "C" oob_status oob_dp_run_virtual(oob_dp_plan *pl, const double *d_fwd, const double *d_bwd,
+                                         void *const *d_ws, size_t ws_bytes, void *const *d_packed, void *stream_) {
+    if (!pl || !d_fwd || !d_bwd || !d_ws || !d_packed)
+        return fail(OOB_E_INVALID, "oob_dp_run_virtual: NULL argument");
+    if (pl->comm) return fail(OOB_E_INVALID, "oob_dp_run_virtual: plan has an NCCL communicator");
+    if (ws_bytes < pl->ws_bytes) return fail(OOB_E_NOMEM, "oob_dp_run_virtual: workspace too small");
+    std::vector<RankRun> rr((size_t)pl->world);
+    for (int r = 0; r < pl->world; ++r) {
+        if (!d_ws[r] || !d_packed[r]) return fail(OOB_E_INVALID, "oob_dp_run_virtual: NULL workspace or output");
+        rr[r] = RankRun{(unsigned char *)d_ws[r], (unsigned char *)d_packed[r], r, {}, nullptr, nullptr, {}};
+    }
+    return run_ranks(pl, d_fwd, d_bwd, rr.data(), pl->world, (cudaStream_t)stream_);
 }
 
 // Diagnostic (not part of the C ABI header): enable/read the flush counters of k_wave_w.
@@ -919,4 +1034,20 @@ extern "C" int oob_dbg_flush_stats(int enable, unsigned long long *out4) {
     unsigned long long z[4] = {0, 0, 0, 0};
     if (cudaMemcpyToSymbol(oob::g_flush_stats, z, sizeof(z)) != cudaSuccess) return 1;
     return cudaMemcpyToSymbol(oob::g_flush_stats_on, &enable, sizeof(int)) == cudaSuccess ? 0 : 1;
+}
+
+// Diagnostic (not part of the C ABI header; -DOOB_TIMELINE builds only): read and reset the
+// per-wave timeline of k_wave_w (6 x u64 per wave, see g_tl).
+extern "C" int oob_dbg_timeline(unsigned long long *out, int nwaves) {
+#ifdef OOB_TIMELINE
+    if (nwaves > 1024) return 1;
+    if (out && cudaMemcpyFromSymbol(out, oob::g_tl, sizeof(unsigned long long) * 6 * nwaves) != cudaSuccess) return 1;
+    static unsigned long long init[1024][6];
+    for (int i = 0; i < 1024; ++i)
+        for (int j = 0; j < 6; ++j) init[i][j] = (j == 0 || j == 1 || j == 4) ? ~0ull : 0ull;
+    return cudaMemcpyToSymbol(oob::g_tl, init, sizeof(init)) == cudaSuccess ? 0 : 1;
+#else
+    (void)out; (void)nwaves;
+    return 2;
+#endif
 }

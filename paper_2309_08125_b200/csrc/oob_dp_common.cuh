@@ -31,7 +31,6 @@ struct DevGeom {
     Cell4 *CELL;              // [P*C]
     float4 *SH;               // [P*C] shadow lower bounds (filter only)
     uint32_t *ARG;            // [P*C]
-    uint64_t *STK;            // [P*p*(L+1)] backtrack stacks
 };
 
 __device__ __forceinline__ bool d_is_whole(const DevGeom &g, int a) { return a >= g.M - 1; }

@@ -409,11 +409,33 @@ extern "C" oob_status oob_generate_templates(const oob_profile *const *profiles,
     int dev = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess)
         return fail(OOB_E_CUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
-    const std::string key = plan_key(L, M, n_lo, n_hi, num_profiles, dev);
+    // multi-GPU: with a communicator of world > 1, one profile is planned by
+    // every rank with its wavefronts split across the ranks; a batch of profiles is split into
+    // contiguous blocks (rank r plans its block) and one all-gather assembles every rank's
+    // packed template sets.  Every rank passes the same profiles and receives the whole set.
+    const int world = (opts->comm && opts->world > 1) ? opts->world : 1;
+    const int rank = world > 1 ? opts->rank : 0;
+    if (world > 1 && (rank < 0 || rank >= world)) return fail(OOB_E_INVALID, "opts.rank out of range");
+    const bool shard_one = world > 1 && num_profiles == 1;
+    int first = 0, count = num_profiles, per_rank = num_profiles;
+    if (world > 1 && !shard_one) {
+        const int base = num_profiles / world, extra = num_profiles % world;
+        first = rank * base + std::min(rank, extra);
+        count = base + (rank < extra ? 1 : 0);
+        per_rank = base + (extra ? 1 : 0);
+    }
+    const int plan_P = std::max(1, count);
+    std::string key = plan_key(L, M, n_lo, n_hi, plan_P, dev);
+    if (shard_one) key += "|comm" + std::to_string((uintptr_t)opts->comm) + "," + std::to_string(world) + "," +
+                          std::to_string(rank);
     oob_dp_plan *plan = take_plan(key);
     if (!plan) {
-        st = oob_dp_plan_create(L, M, n_lo, n_hi, num_profiles, &plan);
+        st = oob_dp_plan_create(L, M, n_lo, n_hi, plan_P, &plan);
         if (st != OOB_OK) return st;
+        if (shard_one && (st = oob_dp_set_comm(plan, opts->comm, world, rank)) != OOB_OK) {
+            oob_dp_plan_free(plan);
+            return st;
+        }
     }
     struct Return {
         std::string key;
@@ -424,12 +446,15 @@ extern "C" oob_status oob_generate_templates(const oob_profile *const *profiles,
     oob_dp_plan_info(plan, &info);
 
     const size_t prof_bytes = sizeof(double) * (size_t)L * M;
-    size_t own_bytes = align_up_host(2 * prof_bytes * num_profiles) + align_up_host(info.packed_bytes);
+    const size_t gather_bytes = (world > 1 && !shard_one) ? (size_t)world * per_rank * info.packed_profile_bytes : 0;
+    size_t own_bytes = align_up_host(2 * prof_bytes * plan_P) + align_up_host(std::max<size_t>(
+                                                                   info.packed_bytes, (size_t)per_rank * info.packed_profile_bytes)) +
+                       align_up_host(gather_bytes);
     void *ws = opts->workspace;
     size_t ws_bytes = opts->workspace_bytes;
     void *own = nullptr;
     if (!ws) ws_bytes = 0;
-    // inputs + packed output live after the DP workspace (caller's or ours)
+    // inputs + packed output (+ the gathered sets) live after the DP workspace (caller's or ours)
     size_t need = align_up_host(info.workspace_bytes) + own_bytes;
     if (!ws || ws_bytes < need) {
         if (ws && ws_bytes > 0 && ws_bytes < need)
@@ -442,20 +467,46 @@ extern "C" oob_status oob_generate_templates(const oob_profile *const *profiles,
     std::unique_ptr<void, void (*)(void *)> own_guard(own, [](void *q) { if (q) cudaFree(q); });
     unsigned char *wsb = (unsigned char *)ws;
     double *d_fwd = (double *)(wsb + align_up_host(info.workspace_bytes));
-    double *d_bwd = d_fwd + (size_t)L * M * num_profiles;
-    unsigned char *d_packed = (unsigned char *)d_fwd + align_up_host(2 * prof_bytes * num_profiles);
-    // H2D of the profile costs (one copy per array per profile)
-    for (int i = 0; i < num_profiles; ++i) {
-        e = cudaMemcpyAsync(d_fwd + (size_t)i * L * M, profiles[i]->fwd.data(), prof_bytes, cudaMemcpyHostToDevice, stream);
+    double *d_bwd = d_fwd + (size_t)L * M * plan_P;
+    unsigned char *d_packed = (unsigned char *)d_fwd + align_up_host(2 * prof_bytes * plan_P);
+    unsigned char *d_gather = d_packed + align_up_host(std::max<size_t>(info.packed_bytes,
+                                                                        (size_t)per_rank * info.packed_profile_bytes));
+    // H2D of this rank's profile costs (one copy per array per profile; a rank without
+    // profiles plans a copy of profile 0 and discards it)
+    for (int i = 0; i < plan_P; ++i) {
+        const oob_profile *pf = profiles[count > 0 ? first + i : 0];
+        e = cudaMemcpyAsync(d_fwd + (size_t)i * L * M, pf->fwd.data(), prof_bytes, cudaMemcpyHostToDevice, stream);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(d_bwd + (size_t)i * L * M, profiles[i]->bwd.data(), prof_bytes, cudaMemcpyHostToDevice, stream);
+            e = cudaMemcpyAsync(d_bwd + (size_t)i * L * M, pf->bwd.data(), prof_bytes, cudaMemcpyHostToDevice, stream);
         if (e != cudaSuccess) return fail(OOB_E_CUDA, std::string("H2D profile: ") + cudaGetErrorString(e));
     }
     st = oob_dp_run(plan, d_fwd, d_bwd, ws, info.workspace_bytes, d_packed, stream);
     if (st != OOB_OK) return st;
-    std::vector<unsigned char> host(info.packed_bytes);
-    e = cudaMemcpyAsync(host.data(), d_packed, info.packed_bytes, cudaMemcpyDeviceToHost, stream);
+    if (world == 1 || shard_one) {
+        std::vector<unsigned char> host(info.packed_bytes);
+        e = cudaMemcpyAsync(host.data(), d_packed, info.packed_bytes, cudaMemcpyDeviceToHost, stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) return fail(OOB_E_CUDA, std::string("DP run / D2H: ") + cudaGetErrorString(e));
+        return oob_template_set_from_packed(host.data(), &info, out);
+    }
+    // batched sweep across ranks: one NCCL all-gather of the per-rank blocks (padded to
+    // per_rank profiles), then the blocks in rank order are the profiles in order
+    const size_t blk = (size_t)per_rank * info.packed_profile_bytes;
+    st = nccl_allgather_bytes(opts->comm, d_packed, d_gather, blk, gather_bytes, world, stream);
+    if (st != OOB_OK) return st;
+    std::vector<unsigned char> host(gather_bytes);
+    e = cudaMemcpyAsync(host.data(), d_gather, gather_bytes, cudaMemcpyDeviceToHost, stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-    if (e != cudaSuccess) return fail(OOB_E_CUDA, std::string("DP run / D2H: ") + cudaGetErrorString(e));
-    return oob_template_set_from_packed(host.data(), &info, out);
+    if (e != cudaSuccess) return fail(OOB_E_CUDA, std::string("DP run / all-gather / D2H: ") + cudaGetErrorString(e));
+    std::vector<unsigned char> whole((size_t)num_profiles * info.packed_profile_bytes);
+    for (int r = 0, pos = 0; r < world; ++r) {
+        const int cnt = num_profiles / world + (r < num_profiles % world ? 1 : 0);
+        std::memcpy(whole.data() + (size_t)pos * info.packed_profile_bytes, host.data() + (size_t)r * blk,
+                    (size_t)cnt * info.packed_profile_bytes);
+        pos += cnt;
+    }
+    oob_dp_info all = info;
+    all.num_profiles = num_profiles;
+    all.packed_bytes = whole.size();
+    return oob_template_set_from_packed(whole.data(), &all, out);
 }

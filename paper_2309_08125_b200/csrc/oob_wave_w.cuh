@@ -34,7 +34,10 @@
 namespace oob {
 
 constexpr int NTW = 256;                                          // threads per k_wave_w CTA
-constexpr int WAVE_CTAS_PER_SM = 2;                               // register budget: 128 per thread
+#ifndef OOB_WAVE_MINB
+#define OOB_WAVE_MINB 2
+#endif
+constexpr int WAVE_CTAS_PER_SM = OOB_WAVE_MINB;                   // register budget: 65536 / (256 x this)
 constexpr unsigned long long ACC_EMPTY = 0x7FEFFFFFFFFFFFFFull;   // DBL_MAX: "no split yet"
 constexpr double D_INF = __builtin_huge_val();
 constexpr unsigned long long ACC_DIRTY = 1ull << 32;   // accumulator key word: improved by this CTA
@@ -159,6 +162,24 @@ __device__ __forceinline__ int c_ipart(int M, int l) {
 // with -DOOB_FLUSH_STATS (scripts/flush_stats.py), enabled by oob_dbg_flush_stats
 __device__ unsigned long long g_flush_stats[4];
 __device__ int g_flush_stats_on;
+
+// diagnostic timeline (compiled in with -DOOB_TIMELINE, scripts/timeline.py): per wave the
+// global-timer ns of [0] first main-CTA start, [1] first CTA past its prologue waits, [2] last
+// CTA done with its units, [3] last CTA done (finalize included), [4] first aux block start,
+// [5] last aux block end
+#ifdef OOB_TIMELINE
+__device__ unsigned long long g_tl[1024][6];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define OOB_TL_MIN(l, i) atomicMin(&g_tl[l][i], gtime())
+#define OOB_TL_MAX(l, i) atomicMax(&g_tl[l][i], gtime())
+#else
+#define OOB_TL_MIN(l, i) ((void)0)
+#define OOB_TL_MAX(l, i) ((void)0)
+#endif
 
 // ---------------------------------------------------------------- exact filter (fast path)
 // A split's binary64 total is bounded from below by a binary32 expression of the children's
@@ -494,6 +515,45 @@ __device__ __forceinline__ void run_rows(XRing &xr, int64_t sidx, const int32_t 
     if (qn) xq_flush<TE>(q4, q1, qn, CELL, acc_s, filt_s, gfr);
     asm volatile("cp.async.wait_group 0;" ::: "memory");   // no copy of this chunk outlives the unit
     __syncwarp();
+}
+
+// One warp unit (out of line: the kernel's outer state stays out of the step loop's
+// registers): start the streamed chunk's ring, load the register tile (shadow lower bounds
+// of TE big-side cells; +inf beyond the row, so a sentinel's bound never passes), refresh
+// the filter entries of the outputs [olo, ohi) the unit can touch from the range's global
+// filter (minima the range's other CTAs found), then run the rows.
+template <int TE, bool LT>
+__device__ __noinline__ void run_unit(const float4 *__restrict__ SH, const Cell4 *CELL, int64_t sidx, const int32_t *wls,
+                                      int r_lo, int r_hi, int64_t bidx, int ncell, int rowB, int e0, int l1, int L,
+                                      const int *outOff, int nout, unsigned acc_s, unsigned filt_s, unsigned *gfr,
+                                      unsigned char *wsm, int olo, int ohi) {
+    const int lane = threadIdx.x & 31;
+    uint4 *q4 = reinterpret_cast<uint4 *>(wsm + XR_BYTES);         // this warp's candidate queue
+    unsigned *q1 = reinterpret_cast<unsigned *>(q4 + XQ_CAP);
+    XRing xr;                                            // rows r_lo.. are contiguous
+    xr_start(xr, reinterpret_cast<float4 *>(wsm), SH + sidx, lane);
+    float TA[TE], TB[TE], TS[TE], TC[TE];
+#pragma unroll
+    for (int t = 0; t < TE; ++t) {
+        const float inf = __int_as_float(0x7f800000);
+        float4 c = make_float4(inf, inf, inf, inf);
+        if (t < ncell) c = __ldg(SH + bidx + t);
+        TA[t] = c.x;
+        TB[t] = LT ? c.y : c.w;
+        TS[t] = c.z;
+        TC[t] = (float)((LT ? 4 : 3) * (rowB + e0 + t));
+    }
+    unsigned *filt = reinterpret_cast<unsigned *>(__cvta_shared_to_generic(filt_s));
+    for (int i0 = olo + lane; i0 < ohi; i0 += 128) {   // 4 loads in flight per lane
+        unsigned gv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) gv[j] = i0 + 32 * j < ohi ? __ldcg(gfr + i0 + 32 * j) : 0xFFFFFFFFu;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (gv[j] < filt[i0 + 32 * j]) atomicMin(filt + i0 + 32 * j, gv[j]);
+    }
+    run_rows<TE, LT>(xr, sidx, wls, r_lo, r_hi, TA, TB, TS, TC, bidx, ncell, rowB, e0, l1, L, outOff, nout, acc_s, filt_s,
+                     gfr, q4, q1, CELL);
 }
 
 // Per-wave finalize + small cells.  Blocks [0, nbw): one thread per (profile, range, W-part
@@ -873,6 +933,7 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // the next wave may start (pipeline)
     if (bid >= w.nbmain) {                    // next wave's seeds and in-node cells
         const int ab = (int)blockIdx.x - w.nbmain;
+        if (threadIdx.x == 0) OOB_TL_MIN(w.l, 4);
         if (ab < w.fa.nbseed) {
             // seeds of wave l+1 read cells of waves <= l-1 and reuse wave l-1's accumulator buffer
             if (threadIdx.x == 0) pipe_wait(w.pp, L_of(g), w.fa.lseed - 2, 7);
@@ -886,6 +947,7 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
             fin_small_block(g, w.fa, (int64_t)ab - w.fa.nbseed);
             pipe_signal(w.pp, L_of(g), 1, w.fa.ls);
         }
+        if (threadIdx.x == 0) OOB_TL_MAX(w.l, 5);
         return;
     }
     const int l = w.l;
@@ -917,10 +979,12 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
     unsigned *gfilt = w.GFILT + (size_t)pr * nout;
     __shared__ int s_rdy;                      // every wave <= s_rdy is ready (pipeline)
     if (tid == 0) {
+        OOB_TL_MIN(l, 0);
         if (w.seeded) pipe_wait(w.pp, L, l, 1);   // this wave's seeds (launch l-1's extra blocks)
         // the accumulator buffer's previous user (wave l-3) has finalized: wave l-2 ready
         pipe_wait(w.pp, L, l - 2, 6);
         s_rdy = w.pp.on ? max(1, l - 2) : L;
+        OOB_TL_MIN(l, 1);
     }
     __syncthreads();
     // accumulator from the seeds, filter from the range's global filter (F of the seeds and
@@ -1010,10 +1074,6 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
         // the streamed chunk's first batches are in flight while the tile and the filter load
         const int64_t sidx = pc + sbase[ls] + (int64_t)us * scells[ls] + d_wofs(g, ls, r_lo);
         unsigned char *wsm = reinterpret_cast<unsigned char *>(rings) + (size_t)(tid >> 5) * (XR_BYTES + XQ_BYTES);
-        uint4 *q4 = reinterpret_cast<uint4 *>(wsm + XR_BYTES);         // this warp's candidate queue
-        unsigned *q1 = reinterpret_cast<unsigned *>(q4 + XQ_CAP);
-        XRing xr;                                            // rows r_lo.. are contiguous
-        xr_start(xr, reinterpret_cast<float4 *>(wsm), g.SH + sidx, lane);
         if (w.prefetch) {   // warm L1 with the binary64 cells the exact path may load
             const Cell4 *tp = g.CELL + pc + sbase[lb] + (int64_t)ub * scells[lb] + (has ? d_wofs(g, lb, rowB) : 0) + e0;
             asm volatile("prefetch.global.L1 [%0];" ::"l"(tp));
@@ -1022,48 +1082,30 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
             asm volatile("prefetch.global.L1 [%0];" ::"l"(sp0));
             asm volatile("prefetch.global.L1 [%0];" ::"l"(sp0 + 4));
         }
-        // register tile: shadow lower bounds of TE big-side cells (+inf beyond the row: every
-        // bound of a sentinel is +inf and never passes)
         const int64_t bidx = pc + sbase[lb] + (int64_t)ub * scells[lb] + (has ? wb0 : d_wofs(g, lb, 1)) + e0;
-        float TA[TE], TB[TE], TS[TE], TC[TE];
-#pragma unroll
-        for (int t = 0; t < TE; ++t) {
-            const float inf = __int_as_float(0x7f800000);
-            float4 c = make_float4(inf, inf, inf, inf);
-            if (t < ncell) c = __ldg(g.SH + bidx + t);
-            TA[t] = c.x;
-            TB[t] = ltiled ? c.y : c.w;
-            TS[t] = c.z;
-            TC[t] = (float)((ltiled ? 4 : 3) * (rowB + e0 + t));
-        }
-        if (w.refresh) {   // refresh the filter of the outputs this unit can touch (rows q = rowB + rs) from the
-            // range's global filter: minima other CTAs found since this CTA last looked
+        int olo = 0, ohi = 0;   // outputs of the parent rows q = rowB + rs this unit can touch
+        if (w.refresh) {
             const int tb0 = blk * 32, tb1 = min(blk * 32 + 31, stcnt[lb] - 1);
             const int rmin = w.tiles[stoff[lb] + tb0] >> 16, rmax = w.tiles[stoff[lb] + tb1] >> 16;
-            const int olo = outOff[min(rmin + r_lo, L + 1)], ohi = outOff[min(rmax + r_hi, L + 1)];
-            for (int i0 = olo + lane; i0 < ohi; i0 += 128) {   // 4 loads in flight per lane
-                unsigned gv[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) gv[j] = i0 + 32 * j < ohi ? __ldcg(gfilt + i0 + 32 * j) : 0xFFFFFFFFu;
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (gv[j] < filt[i0 + 32 * j]) atomicMin(filt + i0 + 32 * j, gv[j]);
-            }
+            olo = outOff[min(rmin + r_lo, L + 1)];
+            ohi = outOff[min(rmax + r_hi, L + 1)];
         }
         if (ltiled)
-            run_rows<TE, true>(xr, sidx, g.wofs + ls * (L + 2), r_lo, r_hi, TA, TB, TS, TC, bidx, ncell, rowB, e0, l1, L, outOff, nout,
-                               acc_s, filt_s, gfilt, q4, q1, g.CELL);
+            run_unit<TE, true>(g.SH, g.CELL, sidx, g.wofs + ls * (L + 2), r_lo, r_hi, bidx, ncell, rowB, e0, l1, L,
+                               outOff, nout, acc_s, filt_s, gfilt, wsm, olo, ohi);
         else
-            run_rows<TE, false>(xr, sidx, g.wofs + ls * (L + 2), r_lo, r_hi, TA, TB, TS, TC, bidx, ncell, rowB, e0, l1, L, outOff,
-                                nout, acc_s, filt_s, gfilt, q4, q1, g.CELL);
+            run_unit<TE, false>(g.SH, g.CELL, sidx, g.wofs + ls * (L + 2), r_lo, r_hi, bidx, ncell, rowB, e0, l1, L,
+                                outOff, nout, acc_s, filt_s, gfilt, wsm, olo, ohi);
     }
     __syncthreads();
+    if (tid == 0) OOB_TL_MAX(l, 2);
     // merge into the range's global accumulator (L2-coherent loads; a stale value is an
     // upper bound of the current one, so the CAS loop stays exact).  Loads are batched so
     // their latencies overlap.
     if (w.cpr == 1 && w.fin_inline && w.world == 1) {   // the range's only CTA: finalize from shared memory
         fin_w_range<NTW>(g, w.fw, pr, tid, 0, 1, acc);
         pipe_signal(w.pp, L, 2, l);
+        if (tid == 0) OOB_TL_MAX(l, 3);
         return;
     }
     ulonglong2 *ga = w.GACC + ((size_t)p * w.nranges + u) * nout;
@@ -1120,6 +1162,7 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
             }
         }
     }
+    if (tid == 0) OOB_TL_MAX(l, 3);
 }
 
 // Start of every run: empty accumulators and filters (the finalize resets what it reads,

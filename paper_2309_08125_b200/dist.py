@@ -4,8 +4,9 @@ The path partitions into independent template DPs — one per profile instance o
 sweep (BASELINE cfg5) — so profiles are sharded in contiguous blocks across ranks with no
 collective inside the DP; one all-gather of the fixed-size packed template sets
 (include/oobleck_plan.h, `oob_dp_run` output layout) assembles the whole set on every rank.
-torch.distributed provides the process group (NCCL over NVLink on the GPU box; gloo in the
-CPU tests); the bytes gathered are the library's packed output, unchanged.
+On GPUs the all-gather is the library's own NCCL communicator (oob_nccl_allgather over
+NVLink; torch.distributed only bootstraps it); the CPU tests use a gloo process group.  The
+bytes gathered are the library's packed output, unchanged.
 """
 from __future__ import annotations
 
@@ -23,11 +24,13 @@ def shard(num_profiles: int, world: int, rank: int) -> tuple[int, int]:
     return first, base + (1 if rank < extra else 0)
 
 
-def allgather_packed(packed: torch.Tensor, per_rank_bytes: int, group=None) -> torch.Tensor:
+def allgather_packed(packed: torch.Tensor, per_rank_bytes: int, group=None, comm=None,
+                     stream: int = 0) -> torch.Tensor:
     """All-gather every rank's packed template sets (uint8, `per_rank_bytes` each; a rank
     with fewer profiles pads with zeros) into one [world * per_rank_bytes] tensor, rank
-    order.  NCCL: one all_gather_into_tensor; gloo: all_gather into a list."""
-    world = dist.get_world_size(group)
+    order.  With `comm` (planner.NcclComm, device tensors): one ncclAllGather through the
+    library; otherwise the process group's all_gather (gloo, CPU tests)."""
+    world = comm.world if comm is not None else dist.get_world_size(group)
     if packed.dtype != torch.uint8 or packed.dim() != 1:
         raise ValueError("packed must be a 1-D uint8 tensor")
     if packed.numel() > per_rank_bytes:
@@ -37,8 +40,8 @@ def allgather_packed(packed: torch.Tensor, per_rank_bytes: int, group=None) -> t
         pad[: packed.numel()] = packed
         packed = pad
     out = torch.empty(world * per_rank_bytes, dtype=torch.uint8, device=packed.device)
-    if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(out, packed, group=group)
+    if comm is not None:
+        comm.allgather(packed.data_ptr(), out.data_ptr(), per_rank_bytes, stream)
     else:
         dist.all_gather(list(out.view(world, per_rank_bytes).unbind(0)), packed, group=group)
     return out

@@ -112,14 +112,18 @@ class TemplateSet:
 def generate_templates(profiles, nodes: int, gpus_per_node: int, f: int, n0: int = 0,
                        gpu_mem_bytes: int = 0, util: float = 0.8, samples_per_gpu: int = 1,
                        device: int = -1, stream: int = 0, workspace: int = 0,
-                       workspace_bytes: int = 0) -> TemplateSet:
-    """oob_generate_templates: host profiles in, template set out (H2D + GPU DP + D2H)."""
+                       workspace_bytes: int = 0, comm: "NcclComm | None" = None) -> TemplateSet:
+    """oob_generate_templates: host profiles in, template set out (H2D + GPU DP + D2H).
+    With `comm` (an NcclComm of world > 1, every rank passing the same profiles): one
+    profile is sharded per wavefront across the ranks, a batch of profiles in contiguous
+    blocks with one all-gather; every rank gets the whole set."""
     profs = [p if isinstance(p, Profile) else Profile.from_arrays(*p) for p in profiles]
     arr = (ctypes.c_void_p * len(profs))(*[p._h for p in profs])
     opts = OobPlanOpts(nodes=nodes, gpus_per_node=gpus_per_node, f=f, n0=n0,
                        gpu_mem_bytes=gpu_mem_bytes, util=util, samples_per_gpu=samples_per_gpu,
                        device=device, stream=stream or None, workspace=workspace or None,
-                       workspace_bytes=workspace_bytes)
+                       workspace_bytes=workspace_bytes, comm=comm.handle if comm is not None else None,
+                       world=comm.world if comm is not None else 1, rank=comm.rank if comm is not None else 0)
     h = ctypes.c_void_p()
     check(lib.oob_generate_templates(arr, len(profs), ctypes.byref(opts), ctypes.byref(h)))
     ts = TemplateSet(h)
@@ -150,6 +154,19 @@ class DPPlan:
             check(lib.oob_dp_set_comm(self._h, comm.handle, comm.world, comm.rank))
             self._comm = comm
         check(lib.oob_dp_plan_info(self._h, ctypes.byref(self.info)))
+
+    def set_virtual_shards(self, world: int) -> None:
+        """oob_dp_set_virtual_shards: the sharded algorithm with `world` virtual ranks on
+        this GPU (test mode); refreshes `info` (per-rank workspace grows)."""
+        check(lib.oob_dp_set_virtual_shards(self._h, world))
+        check(lib.oob_dp_plan_info(self._h, ctypes.byref(self.info)))
+
+    def run_virtual(self, d_fwd: int, d_bwd: int, d_workspaces, workspace_bytes: int, d_packed,
+                    stream: int = 0) -> None:
+        """oob_dp_run_virtual: every virtual rank r on this device (workspace / output r)."""
+        ws = (ctypes.c_void_p * len(d_workspaces))(*d_workspaces)
+        pk = (ctypes.c_void_p * len(d_packed))(*d_packed)
+        check(lib.oob_dp_run_virtual(self._h, d_fwd, d_bwd, ws, workspace_bytes, pk, stream or None))
 
     def set_timing(self, enable: bool) -> None:
         check(lib.oob_dp_set_timing(self._h, 1 if enable else 0))
@@ -196,6 +213,10 @@ class NcclComm:
         h = ctypes.c_void_p()
         check(lib.oob_nccl_comm_create(idb, world, rank, device, ctypes.byref(h)))
         self.handle, self.world, self.rank = h, world, rank
+
+    def allgather(self, d_send: int, d_recv: int, bytes_per_rank: int, stream: int = 0) -> None:
+        """oob_nccl_allgather: d_recv[r * bytes_per_rank:] <- rank r's d_send (device)."""
+        check(lib.oob_nccl_allgather(self.handle, d_send, d_recv, bytes_per_rank, stream or None))
 
     def __del__(self):
         if getattr(self, "handle", None) and lib is not None:

@@ -254,6 +254,49 @@ def test_cfg5_full_sweep_sampled(planner):
         _assert_same(ts.templates(i)[:4], want, f"cfg5 profile {i} sizes 1..4")
 
 
+def _virtual_run(planner, cfg, profs, world):
+    """oob_dp_run_virtual with `world` virtual ranks: every rank's packed output."""
+    import torch
+    plan = planner.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, len(profs))
+    plan.set_virtual_shards(world)
+    info = plan.info
+    assert info.world == world and info.pipelined == 0
+    fwd = torch.tensor(np.stack([p.fwd_ms for p in profs]), dtype=torch.float64, device="cuda")
+    bwd = torch.tensor(np.stack([p.bwd_ms for p in profs]), dtype=torch.float64, device="cuda")
+    ws = [torch.empty(info.workspace_bytes, dtype=torch.uint8, device="cuda") for _ in range(world)]
+    pk = [torch.zeros(info.packed_bytes, dtype=torch.uint8, device="cuda") for _ in range(world)]
+    plan.run_virtual(fwd.data_ptr(), bwd.data_ptr(), [w.data_ptr() for w in ws], info.workspace_bytes,
+                     [p.data_ptr() for p in pk], torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    return [plan.template_set(p.cpu().numpy()) for p in pk]
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_virtual_shards_cfg3_every_wave(planner, world, monkeypatch):
+    """Single-profile sharding checked on ONE GPU (SURVEY §4 "virtual shards"): every
+    wavefront's W units split across `world` virtual ranks (OOB_DP_SHARDMIN=0: all waves),
+    the partial argmins exchanged by device copies, every rank finalizing the whole wave —
+    every rank's template set equals the oracle's."""
+    monkeypatch.setenv("OOB_DP_SHARDMIN", "0")
+    cfg = CONFIGS["cfg3"]
+    prof = config_profiles(cfg, "real")[0]
+    want, _ = coracle.template_set(prof.fwd_ms, prof.bwd_ms, cfg.M, cfg.n0, cfg.n_max)
+    for r, ts in enumerate(_virtual_run(planner, cfg, [prof], world)):
+        _assert_same(ts.templates(0), want, f"cfg3 virtual rank {r}/{world}")
+
+
+def test_virtual_shards_cfg4_golden(planner):
+    """The launch configuration bench.py --shard-profile uses (large waves sharded, default
+    threshold), 4 virtual ranks, full cfg4 set vs the oracle's stored output."""
+    rec = load_golden("cfg4", "real")
+    if rec is None:
+        pytest.skip("tests/golden/cfg4_real.json not generated")
+    cfg = CONFIGS["cfg4"]
+    prof = config_profiles(cfg, "real")[0]
+    for r, ts in enumerate(_virtual_run(planner, cfg, [prof], 4)):
+        _assert_same(ts.templates(0), rec["profiles"][0]["templates"], f"cfg4 virtual rank {r}/4")
+
+
 def _shard_worker(rank, world, port, q):
     import os
     import torch
