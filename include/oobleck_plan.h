@@ -179,7 +179,7 @@ typedef struct {
     int32_t chunk_max, refresh, small_pairs;
     int32_t num_sms;                /* SMs of the device the plan was built for */
     int32_t world;                  /* ranks sharing the wavefronts (oob_dp_set_comm) */
-    int32_t reserved;
+    int32_t warp_waves;             /* batched wavefronts run one warp per (profile, range) */
 } oob_dp_info;
 
 oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int32_t n_hi,
@@ -240,7 +240,8 @@ oob_status oob_template_set_from_packed(const void *h_packed, const oob_dp_info 
  * Best plan for `nodes` available nodes: enumerate every X with
  * sum x_i n_i = N' and sum x_i >= f+1 (Eq.5), distribute the batch for each (Eq.6), and
  * keep the highest throughput B / max_i iteration_ms(N_b,i) (iteration_ms = T1 +
- * (N_b - S + k* - 1) t* + T3); ties: fewer pipelines, then lexicographically
+ * max(0, N_b - S + k* - 1) t* + T3, reading R30); Eq.6 ties (equal T_i): the
+ * minimizer with the smallest iteration time (R29); ties: fewer pipelines, then lexicographically
  * smallest counts.
  *  counts_out   : caller-owned int32 [oob_template_count] — x_i per template
  *  nb_out       : caller-owned int64 [max_pipelines] — N_b per pipeline, pipelines ordered
@@ -260,6 +261,23 @@ oob_status oob_instantiate(const oob_template_set *set, int32_t profile, int32_t
                            double *throughput_out, double *iter_ms_out,
                            int64_t *num_feasible_out, int64_t *recommended_batch_out);
 
+/* Plans for every node count N' = n_min .. n_max in one call (the instantiation for any
+ * number of surviving nodes).  Per N' (index k = N' - n_min): counts_out
+ * [k * template_count + i] = x_i of the chosen plan, throughput_out[k] (samples per ms),
+ * upper_bound_out[k] = a CERTIFIED upper bound of the best throughput of any plan on N'
+ * nodes (equal to throughput_out when exact_out[k] = 1: Eq.5 enumerated exhaustively,
+ * <= max_enumerated sets), status_out[k] = OOB_OK, OOB_E_INFEASIBLE (N' < (f+1) n0 or no
+ * set) or OOB_E_BATCH (B not distributable).  Above max_enumerated the knapsack candidates
+ * of every N' (one set of DPs over 0..n_max) are scored exactly in decreasing order of their
+ * own relaxation bound until none can beat the best; the bound of N' is
+ * B / min_j max(a_j + t*_j, a_j + K t*_j n_j / N') with a_j = T1 + T3 - (S - k* + 1) t*
+ * (DESIGN.md §8).  Caller-owned outputs of (n_max - n_min + 1) entries.  Errors:
+ * OOB_E_INVALID. */
+oob_status oob_instantiate_all(const oob_template_set *set, int32_t profile, int32_t n_min,
+                               int32_t n_max, int32_t f, int64_t global_batch, int32_t microbatch,
+                               int64_t max_enumerated, int32_t *counts_out, double *throughput_out,
+                               double *upper_bound_out, int32_t *exact_out, int32_t *status_out);
+
 /* Number of X satisfying Eq.5's Requirements 1-2 for sizes n_lo..n_hi (saturating). */
 oob_status oob_count_sets(int32_t n_lo, int32_t n_hi, int32_t nodes, int32_t f,
                           int64_t *count_out);
@@ -275,6 +293,63 @@ oob_status oob_distribute_batch(const double *per_microbatch_ms, int32_t x,
                                 int64_t global_batch, int32_t microbatch, int64_t *nb_out,
                                 double *objective_out, int64_t *recommended_batch_out);
 int64_t oob_recommend_batch(int32_t x, int32_t microbatch, int64_t global_batch);
+
+/* ------------------------------------------------------------------ dynamic reconfiguration
+ * An execution state: pipelines instantiated from a template set, each an ordered
+ * list of node ids (template stage i runs on the pipeline's node stages[i].node), with the
+ * Eq.6 microbatches of every pipeline.  On node failures (oob_exec_fail) the affected
+ * pipelines are repaired by the three steps of PAPER §5.1 — simple
+ * reinstantiation from the template of the surviving node count; borrowing nodes from
+ * pipelines that can yield (more than n0 nodes), largest first, the donor giving its last
+ * node; merging with the smallest other pipeline (Appendix B guarantees a template of the
+ * merged size) — processed in ascending surviving size; if whole pipelines failed and fewer
+ * than f+1 remain, the survivors are instantiated afresh (oob_instantiate's plan).  Then the
+ * batch is redistributed (§5.2, Eq.6, global batch unchanged), the copy plan of missing
+ * layers is built (every (node, layer) newly needed, from the surviving previous owner with
+ * the fewest transfers so far, ties: lowest node id) and the per-layer synchronisation
+ * groups of §6.1 follow from the pipelines.  Readings R21-R28.
+ * The template set is borrowed and must outlive the state.  Errors of oob_exec_fail:
+ * OOB_E_INVALID (unknown or already failed node), OOB_E_INFEASIBLE (fewer than (f+1) n0
+ * survivors: checkpoint and exit; or a layer with no surviving copy, P:257-263;
+ * or a merged size above the largest template), OOB_E_BATCH (the pipelines are rebuilt but B
+ * cannot be distributed over them; *recommended_batch_out is set). */
+typedef struct oob_exec oob_exec;
+enum { OOB_ACT_REINSTANTIATE = 1, OOB_ACT_BORROW = 2, OOB_ACT_MERGE = 3, OOB_ACT_REMOVE = 4, OOB_ACT_REPLAN = 5 };
+/* reinstantiate: pipeline a (index before the call) -> template of `nodes` nodes;
+ * borrow: one node from pipeline a to pipeline b; merge: pipeline b's nodes appended to a;
+ * remove: pipeline a lost every node; replan: a = new pipeline count. */
+typedef struct {
+    int32_t kind, a, b, nodes;
+} oob_action;
+typedef struct {
+    int32_t layer, donor, receiver, reserved;
+    int64_t bytes;                  /* layer_bytes[layer] given at creation (0 if none) */
+} oob_transfer;
+
+/* counts: caller [template_count] pipelines per template size n_lo + i; node_ids: the
+ * sum(counts_i * n_i) nodes, assigned in order (template order, pipelines consecutive);
+ * layer_bytes: [L] model-state bytes per layer or NULL.  Errors: OOB_E_INVALID,
+ * OOB_E_INFEASIBLE (fewer than f+1 pipelines), OOB_E_BATCH. */
+oob_status oob_exec_create(const oob_template_set *set, int32_t profile, int32_t f,
+                           int64_t global_batch, int32_t microbatch, const int32_t *counts,
+                           const int32_t *node_ids, int32_t num_nodes, const int64_t *layer_bytes,
+                           oob_exec **out);
+void oob_exec_free(oob_exec *state);
+int32_t oob_exec_num_pipelines(const oob_exec *state);
+/* nodes_out: caller [max_nodes] (may be NULL); *nb = the pipeline's microbatches. */
+oob_status oob_exec_pipeline(const oob_exec *state, int32_t i, int32_t *nodes_out, int32_t max_nodes,
+                             int32_t *num_nodes, int64_t *nb);
+oob_status oob_exec_fail(oob_exec *state, const int32_t *failed, int32_t num_failed,
+                         int64_t *recommended_batch_out);
+/* actions and copy transfers of the last oob_exec_fail, in the order they were taken */
+int32_t oob_exec_num_actions(const oob_exec *state);
+oob_status oob_exec_action(const oob_exec *state, int32_t i, oob_action *out);
+int32_t oob_exec_num_transfers(const oob_exec *state);
+oob_status oob_exec_transfer(const oob_exec *state, int32_t i, oob_transfer *out);
+/* Sync group of `layer` (§6.1): for every pipeline p, the stage holding the layer —
+ * entries (pipelines_out[k], stages_out[k]), *count = number of pipelines. */
+oob_status oob_exec_sync_group(const oob_exec *state, int32_t layer, int32_t *pipelines_out,
+                               int32_t *stages_out, int32_t max_entries, int32_t *count);
 
 #ifdef __cplusplus
 }

@@ -10,8 +10,14 @@ definition is (small inputs only).
   every integer assignment N_{b,i} >= 1 with sum N_{b,i} b = B (reading R18); T_i is the
   pipeline's per-microbatch steady cost t* (reading R19).
 * `recommend_batch`: smallest distributable B' >= B.
-* `iteration_ms`: T1 + (N_b - S + k* - 1) t* + T3 (Eq.2 with the real N_b).
+* `iteration_ms`: T1 + max(0, N_b - S + k* - 1) t* + T3 (Eq.2 with the real N_b; SPEC S:131;
+  reading R30 for N_b below the pipeline fill).
 * `select_plan_brute`: max-throughput plan over all feasible sets.
+* `distribute_for_plan`: Eq.6 for a plan's pipelines; Eq.6 can have several minimizers
+  (pipelines with equal T_i), and the distributor exists to balance the pipelines'
+  execution, so among the minimizers the one with the smallest plan iteration
+  time max_i iteration_ms(N_b,i) is taken, remaining ties giving the larger count to the
+  lower pipeline index (reading R29).
 """
 from __future__ import annotations
 
@@ -79,6 +85,27 @@ def distribute_batch_brute(T, B: int, b: int):
     return best
 
 
+def distribute_for_plan(pipes, B: int, b: int):
+    """Reading R29: (nb, iteration time) of the Eq.6 minimizer with the smallest plan
+    iteration time (pipes: template dicts); raises ValueError if not distributable."""
+    x = len(pipes)
+    if B % b != 0 or B // b < x:
+        raise ValueError("infeasible distribution")
+    T = [t["tstar"] for t in pipes]
+    cands = [(variance_objective(nb, T), nb) for nb in compositions(B // b, x)]
+    best_obj = min(o for o, _ in cands)
+    tol = 1e-12 * (B // b * max(T)) ** 2        # rounding of a sum of squares of size (K T)^2
+    best = None
+    for o, nb in cands:
+        if o > best_obj + tol:
+            continue
+        it = max(iteration_ms(t, n) for t, n in zip(pipes, nb))
+        key = (it, tuple(-n for n in nb))
+        if best is None or key < best[0]:
+            best = (key, nb, it)
+    return best[1], best[2]
+
+
 def recommend_batch(x: int, b: int, B: int) -> int:
     Bp = max(B, x * b)
     if Bp % b:
@@ -87,8 +114,10 @@ def recommend_batch(x: int, b: int, B: int) -> int:
 
 
 def iteration_ms(tpl, Nb: int) -> float:
+    """Eq.2 with the real N_b; with fewer microbatches than the pipeline's fill (N_b <
+    S - k* + 1) the steady phase T2 is empty, not negative (reading R30)."""
     S = tpl["S"]
-    return (tpl["T1"] + float(Nb - S + tpl["kstar"] - 1) * tpl["tstar"]) + tpl["T3"]
+    return (tpl["T1"] + float(max(0, Nb - S + tpl["kstar"] - 1)) * tpl["tstar"]) + tpl["T3"]
 
 
 def select_plan_brute(templates, Nprime: int, f: int, B: int, b: int):
@@ -101,10 +130,9 @@ def select_plan_brute(templates, Nprime: int, f: int, B: int, b: int):
         for i, cnt in enumerate(X):
             pipes += [templates[i]] * cnt
         try:
-            nb, _ = distribute_batch_brute([t["tstar"] for t in pipes], B, b)
+            nb, it = distribute_for_plan(pipes, B, b)
         except ValueError:
             continue
-        it = max(iteration_ms(t, n) for t, n in zip(pipes, nb))
         thr = B / it
         key = (-thr, sum(X), X)
         if best is None or key < best[0]:

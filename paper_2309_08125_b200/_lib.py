@@ -53,7 +53,19 @@ class OobDpInfo(ctypes.Structure):
                 ("packed_template_bytes", c_size_t), ("packed_profile_bytes", c_size_t),
                 ("packed_bytes", c_size_t), ("kernel", c_int32), ("pipelined", c_int32),
                 ("fused", c_int32), ("seeded", c_int32), ("chunk_max", c_int32), ("refresh", c_int32),
-                ("small_pairs", c_int32), ("num_sms", c_int32), ("world", c_int32), ("reserved", c_int32)]
+                ("small_pairs", c_int32), ("num_sms", c_int32), ("world", c_int32), ("warp_waves", c_int32)]
+
+
+class OobAction(ctypes.Structure):
+    _fields_ = [("kind", c_int32), ("a", c_int32), ("b", c_int32), ("nodes", c_int32)]
+
+
+class OobTransfer(ctypes.Structure):
+    _fields_ = [("layer", c_int32), ("donor", c_int32), ("receiver", c_int32), ("reserved", c_int32),
+                ("bytes", c_int64)]
+
+
+OOB_ACT_REINSTANTIATE, OOB_ACT_BORROW, OOB_ACT_MERGE, OOB_ACT_REMOVE, OOB_ACT_REPLAN = 1, 2, 3, 4, 5
 
 
 def _proto(name, res, args):
@@ -96,9 +108,22 @@ _proto("oob_instantiate", ctypes.c_int, [c_void_p, c_int32, c_int32, c_int32, c_
                                          c_void_p, c_void_p, c_int32, P(c_int32), P(c_double), P(c_double),
                                          P(c_int64), P(c_int64)])
 _proto("oob_count_sets", ctypes.c_int, [c_int32, c_int32, c_int32, c_int32, P(c_int64)])
+_proto("oob_instantiate_all", ctypes.c_int, [c_void_p, c_int32, c_int32, c_int32, c_int32, c_int64, c_int32, c_int64,
+                                             c_void_p, c_void_p, c_void_p, c_void_p, c_void_p])
 _proto("oob_distribute_batch", ctypes.c_int, [c_void_p, c_int32, c_int64, c_int32, c_void_p, P(c_double),
                                               P(c_int64)])
 _proto("oob_recommend_batch", c_int64, [c_int32, c_int32, c_int64])
+_proto("oob_exec_create", ctypes.c_int, [c_void_p, c_int32, c_int32, c_int64, c_int32, c_void_p, c_void_p, c_int32,
+                                         c_void_p, P(c_void_p)])
+_proto("oob_exec_free", None, [c_void_p])
+_proto("oob_exec_num_pipelines", c_int32, [c_void_p])
+_proto("oob_exec_pipeline", ctypes.c_int, [c_void_p, c_int32, c_void_p, c_int32, P(c_int32), P(c_int64)])
+_proto("oob_exec_fail", ctypes.c_int, [c_void_p, c_void_p, c_int32, P(c_int64)])
+_proto("oob_exec_num_actions", c_int32, [c_void_p])
+_proto("oob_exec_action", ctypes.c_int, [c_void_p, c_int32, P(OobAction)])
+_proto("oob_exec_num_transfers", c_int32, [c_void_p])
+_proto("oob_exec_transfer", ctypes.c_int, [c_void_p, c_int32, P(OobTransfer)])
+_proto("oob_exec_sync_group", ctypes.c_int, [c_void_p, c_int32, c_void_p, c_void_p, c_int32, P(c_int32)])
 
 EXPORTED = [
     "oob_last_error", "oob_status_string", "oob_load_profile", "oob_profile_from_arrays",
@@ -109,6 +134,8 @@ EXPORTED = [
     "oob_template_set_from_packed", "oob_instantiate", "oob_count_sets", "oob_distribute_batch",
     "oob_recommend_batch", "oob_nccl_unique_id", "oob_nccl_comm_create", "oob_nccl_comm_destroy",
     "oob_dp_set_comm", "oob_nccl_allgather", "oob_dp_set_virtual_shards", "oob_dp_run_virtual",
+    "oob_instantiate_all", "oob_exec_create", "oob_exec_free", "oob_exec_num_pipelines", "oob_exec_pipeline", "oob_exec_fail",
+    "oob_exec_num_actions", "oob_exec_action", "oob_exec_num_transfers", "oob_exec_transfer", "oob_exec_sync_group",
 ]
 NCCL_ID_BYTES = 128
 

@@ -265,6 +265,9 @@ struct Knobs {
     int refresh = 1;           // OOB_DP_REFRESH=0: no per-unit filter refresh
     double shard_min = SHARD_MIN_SPLITS;   // OOB_DP_SHARDMIN: waves with fewer splits run redundantly
     long long spin_max = 1ll << 24;        // OOB_DP_PIPE_SPIN: polls before a pipeline wait times out
+    int fin_wait = 1;          // OOB_DP_FINWAIT=0: merged CTAs exit, the range's last one finalizes alone
+    int warp_units = 96;       // OOB_DP_WARPMAX: batched waves with <= this many units per range run one
+                               // warp per (profile, range) (0: never)
     int debug = 0;             // OOB_DP_DEBUG: per-wave plan on stderr
 };
 
@@ -283,6 +286,8 @@ Knobs read_knobs() {
     if (const char *v = env("OOB_DP_REFRESH")) k.refresh = std::atoi(v) != 0;
     if (const char *v = env("OOB_DP_SHARDMIN")) k.shard_min = std::atof(v);
     if (const char *v = env("OOB_DP_PIPE_SPIN")) k.spin_max = std::max(0ll, std::atoll(v));
+    if (const char *v = env("OOB_DP_FINWAIT")) k.fin_wait = std::atoi(v) != 0;
+    if (const char *v = env("OOB_DP_WARPMAX")) k.warp_units = std::max(0, std::atoi(v));
     if (env("OOB_DP_DEBUG")) k.debug = 1;
     return k;
 }
@@ -299,6 +304,7 @@ struct WaveHost {
     int max_row = 0;               // longest streamed W row (queue entry fields)
     int nsmall = 0;                // cells inside one node with S' >= 2 per range
     bool seed = false;             // accumulator seeded by k_fin (proportional + warm-start splits)
+    bool warp = false;             // one warp per (profile, range) (k_wave_w warp mode)
     double cost = 0.0;             // modelled issue cycles of the wave (all ranges, profiles)
 };
 
@@ -434,7 +440,7 @@ static void build_wave(oob_dp_plan *pl, int l, int slots, WaveHost &wh, int CH) 
     wh.cpr = std::max(1, std::min(wh.nunits / 8, slots / std::max(1, ranges)));
     // acc[nout + dummy] (16 B) + filter (4 B) + base[L+2] (8 B) + cells[L+1] + outOff[L+2]
     // + upre[L+4] + ents[nents] (16 B)
-    const size_t nent = (size_t)(wh.nout + g.L + 2 * TE_W + 2);
+    const size_t nent = (size_t)(wh.nout + g.L + 2 * TE_W + 2) * (wh.warp ? NTW / 32 : 1);
     const size_t before_ring = nent * 16 + (nent + 3) / 4 * 16 + (size_t)wh.nents * 16 + (size_t)(g.L + 2) * 8 +
                                (size_t)(g.L + 1) * 4 + (size_t)(g.L + 2) * 4 + (size_t)(g.L + 4) * 4 +
                                2 * (size_t)(g.L + 1) * 4 + wh.cb.size() * 4;   // + tile tables, chunk bounds
@@ -464,7 +470,7 @@ static bool plan_pipe_on(const oob_dp_plan *pl) {
     const Geometry &G = pl->g;
     bool on = pl->kn.pipe && pl->kernel == 2 && pl->world == 1 && pl->kn.fuse_fin;
     for (int l = 2; l <= G.L && on; ++l)
-        on = pl->waves[l].nents > 0 &&
+        on = pl->waves[l].nents > 0 && !pl->waves[l].warp &&
              (int64_t)pl->P * (G.L - l + 1) * pl->waves[l].cpr <= (int64_t)CTAS_PER_SM * pl->num_sms;
     return on;
 }
@@ -508,6 +514,15 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
             const int ps = std::max(1, std::min(CTAS_PER_SM, by_smem));
             if (ps == per_sm) break;
             per_sm = ps;
+        }
+        // batched sweeps: short waves (few units per range) one warp per (profile, range)
+        if (num_profiles > 1 && pl->kn.fuse_fin && wh.nunits <= pl->kn.warp_units) {
+            WaveHost ww = wh;
+            ww.warp = true;
+            build_wave(pl, l, per_sm * SMS, ww, pl->kn.chunk_max);
+            ww.warp = true;
+            ww.cpr = 1;
+            if (ww.smem <= 113 * 1024) wh = ww;
         }
         // queue entries carry the accumulator entry in 16 bits and E', rl in 11 bits each
         if (wh.nout + L + 2 * TE_W + 2 > 0xFFFF || wh.max_row + TE_W > 2047) fits = false;
@@ -679,7 +694,7 @@ static int64_t count_launches(const oob_dp_plan *pl) {
     int64_t n = 4;
     for (int l = 2; l <= G.L; ++l) {
         const WaveHost &wh = pl->waves[l];
-        const bool shard = pl->world > 1 && (double)G.wave_splits[l] * pl->P >= pl->kn.shard_min;
+        const bool shard = pl->world > 1 && !wh.warp && (double)G.wave_splits[l] * pl->P >= pl->kn.shard_min;
         const bool has = wh.nents > 0;
         n += has ? 1 : 0;
         n += (pl->kn.fuse_fin && has && !shard) ? 0 : 1;
@@ -710,7 +725,8 @@ extern "C" oob_status oob_dp_plan_info(const oob_dp_plan *pl, oob_dp_info *out) 
     out->small_pairs = pl->kn.small_pairs;
     out->num_sms = pl->num_sms;
     out->world = pl->world;
-    out->reserved = 0;
+    out->warp_waves = 0;
+    for (int l = 2; l <= g.L; ++l) out->warp_waves += pl->waves[l].warp ? 1 : 0;
     return OOB_OK;
 }
 
@@ -892,8 +908,10 @@ static oob_status run_ranks(oob_dp_plan *pl, const double *d_fwd, const double *
         const WaveHost &wh = pl->waves[l];
         // shard only wavefronts whose work outweighs the all-gather (~10-20 us on NVLink);
         // short wavefronts run redundantly on every rank (identical results, no exchange)
-        const bool shard = pl->world > 1 && (double)G.wave_splits[l] * pl->P >= pl->kn.shard_min;
-        const int64_t ctas = wh.nents > 0 ? (int64_t)pl->P * (G.L - l + 1) * wh.cpr : 0;
+        const bool shard = pl->world > 1 && !wh.warp && (double)G.wave_splits[l] * pl->P >= pl->kn.shard_min;
+        const int64_t ctas = wh.nents == 0 ? 0
+                             : wh.warp ? ((int64_t)pl->P * (G.L - l + 1) + NTW / 32 - 1) / (NTW / 32)
+                                       : (int64_t)pl->P * (G.L - l + 1) * wh.cpr;
         // fused finalize (OOB_DP_FUSE=1): unsharded waves finalize in k_wave_w's last CTAs
         // and run the next wave's in-node cells and seeds in extra blocks
         const bool fused = pl->kn.fuse_fin && ctas > 0 && !shard;
@@ -923,6 +941,8 @@ static oob_status run_ranks(oob_dp_plan *pl, const double *d_fwd, const double *
             int64_t aux = 0;
             w.nbmain = (int)ctas;
             w.refresh = pl->kn.refresh && wh.cpr > 1;   // one CTA per range: its own filter is current
+            w.fin_spin = pl->kn.fin_wait ? (1 << 22) : 0;
+            w.warp_mode = wh.warp ? 1 : 0;
             // batched sweeps (one CTA per range, small shared memory, a larger L1): the exact
             // path's children are worth warming in L1 (cfg5 -2%; neutral to negative for cfg4)
             w.prefetch = wh.cpr == 1 && pl->P > 1;

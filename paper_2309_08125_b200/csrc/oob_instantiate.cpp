@@ -46,7 +46,11 @@ inline double marginal(const Group &g, int64_t M) {   // phi(M+1) - phi(M), with
     return (double)(2 * (M / g.c) + 1);
 }
 
-void distribute_exact(const double *T, int x, int64_t K, int64_t *nb, double *obj_out) {
+// A (nullable): per-pipeline fill/drain overhead a_i of iteration_ms = a_i + N_b,i t*_i.
+// Eq.6 has several minimizers when pipelines share T; inside a group of equal T the extra
+// microbatches go to the members with the smaller a_i (then the lower index), which gives the
+// minimizer with the smallest plan iteration time (reading R29).
+void distribute_exact(const double *T, int x, int64_t K, int64_t *nb, double *obj_out, const double *A = nullptr) {
     std::vector<Group> gs;
     {
         std::vector<int> idx(x);
@@ -58,7 +62,11 @@ void distribute_exact(const double *T, int x, int64_t K, int64_t *nb, double *ob
             gs.back().members.push_back(i);
         }
     }
-    for (auto &g : gs) std::sort(g.members.begin(), g.members.end());
+    for (auto &g : gs)
+        std::sort(g.members.begin(), g.members.end(), [&](int a, int b) {
+            if (A && A[a] != A[b]) return A[a] < A[b];
+            return a < b;
+        });
     for (auto &g : gs) g.Mg = g.c;
     gs[0].Mg += K - x;
     std::vector<int64_t> best_M(gs.size());
@@ -162,7 +170,7 @@ struct InstCtx {
     bool capped = false;
     std::vector<int32_t> x, best_x;
     std::vector<int64_t> best_nb, nb;
-    std::vector<double> T;
+    std::vector<double> T, A;
     double best_thr = -1.0, best_iter = 0.0;
     int64_t best_pipes = 0;
 };
@@ -178,18 +186,25 @@ void evaluate(InstCtx &c) {
         return;
     }
     c.T.clear();
+    c.A.clear();
     for (int i = 0; i < c.p; ++i)
-        for (int k = 0; k < c.x[i]; ++k) c.T.push_back(c.tpl[i].tstar_ms);
+        for (int k = 0; k < c.x[i]; ++k) {
+            const oob_template &t = c.tpl[i];
+            c.T.push_back(t.tstar_ms);
+            c.A.push_back(t.t1_ms + t.t3_ms - (double)(t.num_stages - t.kstar + 1) * t.tstar_ms);
+        }
     c.nb.assign(pipes, 0);
-    distribute_exact(c.T.data(), (int)pipes, K, c.nb.data(), nullptr);
+    distribute_exact(c.T.data(), (int)pipes, K, c.nb.data(), nullptr, c.A.data());
     c.distributable++;
     double iter = 0.0;
     int64_t pi = 0;
     for (int i = 0; i < c.p; ++i)
         for (int k = 0; k < c.x[i]; ++k, ++pi) {
             const oob_template &t = c.tpl[i];
-            // iteration_ms(N_b) = T1 + (N_b - S + k* - 1) t* + T3 (Eq.2 with the real N_b)
-            const double it = (t.t1_ms + (double)(c.nb[pi] - t.num_stages + t.kstar - 1) * t.tstar_ms) + t.t3_ms;
+            // iteration_ms(N_b) = T1 + (N_b - S + k* - 1) t* + T3 (Eq.2 with the real N_b; no
+            // negative steady phase below the pipeline fill: reading R30)
+            const int64_t steady = std::max<int64_t>(0, c.nb[pi] - t.num_stages + t.kstar - 1);
+            const double it = (t.t1_ms + (double)steady * t.tstar_ms) + t.t3_ms;
             iter = std::max(iter, it);
         }
     const double thr = (double)c.B / iter;
@@ -236,8 +251,11 @@ void dfs(InstCtx &c, int i, int rem) {
 //       microbatches per pipeline make the integer split matter; c <= K keeps the batch
 //       distributable).
 // Every candidate is then scored exactly (Eq.6 + iteration time) like an enumerated set.
-std::vector<std::vector<int32_t>> knapsack_candidates(const oob_template *tpl, int p, int n_lo, int N, int f,
-                                                      int64_t K) {
+// Candidates for every node count t in [t_lo, N] from one set of knapsack DPs over 0..N
+// (out[t - t_lo]); knapsack_candidates(.., N, ..) = the list for N alone.
+std::vector<std::vector<std::vector<int32_t>>> knapsack_candidates_range(const oob_template *tpl, int p, int n_lo,
+                                                                         int t_lo, int N, int f, int64_t K,
+                                                                         int kb_per_count) {
     std::vector<int> order(p);
     std::vector<double> over(p), rate(p);
     for (int i = 0; i < p; ++i) {
@@ -249,7 +267,12 @@ std::vector<std::vector<int32_t>> knapsack_candidates(const oob_template *tpl, i
     const double NEG = -std::numeric_limits<double>::infinity();
     std::vector<double> dp;
     std::vector<int32_t> from;
-    std::vector<std::vector<int32_t>> out;
+    const int nT = N - t_lo + 1;
+    std::vector<std::vector<std::vector<int32_t>>> outs((size_t)std::max(0, nT));
+    auto push = [&](int T, const std::vector<int32_t> &x) {
+        auto &out = outs[(size_t)(T - t_lo)];
+        if (std::find(out.begin(), out.end(), x) == out.end()) out.push_back(x);
+    };
     // knapsack over the allowed templates with C count buckets (saturating or exact)
     auto run = [&](const std::vector<char> &allowed, int C, bool saturate) {
         dp.assign((size_t)(N + 1) * C, NEG);
@@ -271,18 +294,21 @@ std::vector<std::vector<int32_t>> knapsack_candidates(const oob_template *tpl, i
                 }
             }
     };
-    auto add = [&](int C, int c) {
-        if (dp[(size_t)N * C + c] == NEG) return;
-        std::vector<int32_t> x(p, 0);
-        int t = N;
-        while (t > 0) {
-            const int32_t fr = from[(size_t)t * C + c];
-            const int i = fr & 0xFFFF;
-            x[i]++;
-            t -= n_lo + i;
-            c = fr >> 16;
+    auto add = [&](int C, int c0) {
+        for (int T = t_lo; T <= N; ++T) {
+            int c = c0;
+            if (dp[(size_t)T * C + c] == NEG) continue;
+            std::vector<int32_t> x(p, 0);
+            int t = T;
+            while (t > 0) {
+                const int32_t fr = from[(size_t)t * C + c];
+                const int i = fr & 0xFFFF;
+                x[i]++;
+                t -= n_lo + i;
+                c = fr >> 16;
+            }
+            push(T, x);
         }
-        if (std::find(out.begin(), out.end(), x) == out.end()) out.push_back(x);
     };
     std::vector<char> allowed(p, 0);
     for (int th = 0; th < p; ++th) {                       // (1)
@@ -293,23 +319,25 @@ std::vector<std::vector<int32_t>> knapsack_candidates(const oob_template *tpl, i
     }
     // (3) (near-)homogeneous sets: q or q-1, q-2 pipelines of one template plus at most one
     // pipeline of the size that uses the remaining nodes (equal pipelines balance exactly)
-    for (int i = 0; i < p; ++i) {
-        const int n = n_lo + i, q = N / n;
-        for (int k = 0; k <= 2 && q - k >= 1; ++k) {
-            const int R = N - (q - k) * n;
-            if (R != 0 && (R < n_lo || R >= n_lo + p)) continue;
-            if ((q - k) + (R ? 1 : 0) < f + 1) continue;
-            std::vector<int32_t> x(p, 0);
-            x[i] += q - k;
-            if (R) x[R - n_lo] += 1;
-            if (std::find(out.begin(), out.end(), x) == out.end()) out.push_back(x);
+    for (int T = t_lo; T <= N; ++T)
+        for (int i = 0; i < p; ++i) {
+            const int n = n_lo + i, q = T / n;
+            for (int k = 0; k <= 2 && q - k >= 1; ++k) {
+                const int R = T - (q - k) * n;
+                if (R != 0 && (R < n_lo || R >= n_lo + p)) continue;
+                if ((q - k) + (R ? 1 : 0) < f + 1) continue;
+                std::vector<int32_t> x(p, 0);
+                x[i] += q - k;
+                if (R) x[R - n_lo] += 1;
+                push(T, x);
+            }
         }
-    }
     // (2) with the KB best rates per (nodes, count) state, so near-optimal sets whose
     // integer batch split is better also get scored
     const int64_t cmax = std::min<int64_t>(K, N / n_lo);
-    if (cmax >= f + 1) {
+    if (cmax >= f + 1 && kb_per_count > 0) {
         constexpr int KB = 4;
+        const int kb_out = std::min(KB, kb_per_count);
         const int C = (int)cmax + 1;
         struct E { double v; int32_t i, c, r; };      // value, template, previous count, previous rank
         std::vector<E> kb((size_t)(N + 1) * C * KB, E{NEG, -1, 0, 0});
@@ -337,22 +365,58 @@ std::vector<std::vector<int32_t>> knapsack_candidates(const oob_template *tpl, i
                 }
                 for (int r = 0; r < KB; ++r) at(t, c, r) = best[r];
             }
-        for (int c = f + 1; c < C; ++c)
-            for (int r0 = 0; r0 < KB; ++r0) {
-                if (at(N, c, r0).v == NEG) break;
-                std::vector<int32_t> x(p, 0);
-                int t = N, cc = c, r = r0;
-                while (t > 0) {
-                    const E &e = at(t, cc, r);
-                    x[e.i]++;
-                    t -= n_lo + e.i;
-                    cc = e.c;
-                    r = e.r;
+        for (int T = t_lo; T <= N; ++T)
+            for (int c = f + 1; c < C; ++c)
+                for (int r0 = 0; r0 < kb_out; ++r0) {
+                    if (at(T, c, r0).v == NEG) break;
+                    std::vector<int32_t> x(p, 0);
+                    int t = T, cc = c, r = r0;
+                    while (t > 0) {
+                        const E &e = at(t, cc, r);
+                        x[e.i]++;
+                        t -= n_lo + e.i;
+                        cc = e.c;
+                        r = e.r;
+                    }
+                    push(T, x);
                 }
-                if (std::find(out.begin(), out.end(), x) == out.end()) out.push_back(x);
-            }
     }
-    return out;
+    return outs;
+}
+
+std::vector<std::vector<int32_t>> knapsack_candidates(const oob_template *tpl, int p, int n_lo, int N, int f,
+                                                      int64_t K) {
+    return knapsack_candidates_range(tpl, p, n_lo, N, N, f, K, 4)[0];
+}
+
+// Lower bound of the iteration time (max_i T1 + (N_b,i - S + k* - 1) t* + T3 = a_i + N_b,i t_i)
+// of ANY plan on exactly Np nodes distributing K microbatches (N_b,i >= 1): for tau = its
+// iteration time, K = sum N_b,i <= sum_i (tau - a_i) / t_i <= Np max_{i in X} (tau - a_i) / (t_i n_i),
+// and tau >= a_i + t_i for every used i; so tau >= min_j max(a_j + t_j, a_j + K t_j n_j / Np).
+double iter_lower_bound(const oob_template *tpl, int p, int n_lo, int Np, int64_t K) {
+    double lb = std::numeric_limits<double>::infinity();
+    for (int j = 0; j < p; ++j) {
+        const oob_template &t = tpl[j];
+        const double a = t.t1_ms + t.t3_ms - (double)(t.num_stages - t.kstar + 1) * t.tstar_ms;
+        const double v = std::max(a + t.tstar_ms, a + (double)K * t.tstar_ms * (double)(n_lo + j) / (double)Np);
+        lb = std::min(lb, v);
+    }
+    return lb;
+}
+
+// Lower bound of the iteration time of plan x (any distribution, N_b,i >= 1 real): the
+// water level tau with sum_i (tau - a_i) / t_i = K, and at least max_i (a_i + t_i).
+double plan_iter_lower_bound(const oob_template *tpl, int p, const std::vector<int32_t> &x, int64_t K) {
+    double R = 0.0, A = 0.0, floor_ = -std::numeric_limits<double>::infinity();
+    for (int i = 0; i < p; ++i) {
+        if (!x[i]) continue;
+        const oob_template &t = tpl[i];
+        const double a = t.t1_ms + t.t3_ms - (double)(t.num_stages - t.kstar + 1) * t.tstar_ms;
+        R += (double)x[i] / t.tstar_ms;
+        A += (double)x[i] * a / t.tstar_ms;
+        floor_ = std::max(floor_, a + t.tstar_ms);
+    }
+    return std::max(floor_, ((double)K + A) / R);
 }
 
 }  // namespace
@@ -403,5 +467,67 @@ extern "C" oob_status oob_instantiate(const oob_template_set *set, int32_t profi
     if (iter_out) *iter_out = c.best_iter;
     if (rec_out) *rec_out = B;
     if (c.capped) return fail(OOB_E_TOO_MANY, "more than max_enumerated feasible sets; plan is the best knapsack candidate");
+    return OOB_OK;
+}
+
+// Plans for every node count N' in [n_min, n_max] (the instantiation for
+// whatever number of nodes survives).  Exhaustive (Eq.5 + Eq.6) where the feasible sets
+// number <= max_enum; above it, the knapsack candidates of every N' come from one set of DPs
+// over 0..n_max and are scored exactly in decreasing order of their own relaxation bound
+// until no remaining candidate can beat the best.  upper_bound_out certifies the result: no
+// plan of N' nodes reaches a higher throughput (B / iter_lower_bound).
+extern "C" oob_status oob_instantiate_all(const oob_template_set *set, int32_t profile, int32_t n_min, int32_t n_max,
+                                          int32_t f, int64_t B, int32_t b, int64_t max_enum, int32_t *counts_out,
+                                          double *thr_out, double *ub_out, int32_t *exact_out, int32_t *status_out) {
+    if (!set || !counts_out || !thr_out || !ub_out || !exact_out || !status_out)
+        return fail(OOB_E_INVALID, "oob_instantiate_all: NULL argument");
+    if (profile < 0 || profile >= set->num_profiles) return fail(OOB_E_INVALID, "oob_instantiate_all: bad profile");
+    if (f < 0 || b < 1 || B < 1 || n_min > n_max) return fail(OOB_E_INVALID, "oob_instantiate_all: bad argument");
+    const int p = set->n_hi - set->n_lo + 1;
+    const oob_template *tpl = &set->templates[(size_t)profile * p];
+    const int64_t K = B / b;
+    if (max_enum <= 0) max_enum = 1000000;
+    const int lo = std::max<int>(n_min, (f + 1) * set->n_lo);
+    std::vector<std::vector<std::vector<int32_t>>> cands;
+    bool have_cands = false;
+    for (int Np = n_min; Np <= n_max; ++Np) {
+        const int k = Np - n_min;
+        int32_t *cnt = counts_out + (size_t)k * p;
+        std::fill(cnt, cnt + p, 0);
+        thr_out[k] = 0.0;
+        ub_out[k] = 0.0;
+        exact_out[k] = 0;
+        status_out[k] = OOB_OK;
+        if (Np < lo || count_sets(set->n_lo, set->n_hi, Np, f) == 0) { status_out[k] = OOB_E_INFEASIBLE; continue; }
+        InstCtx c;
+        c.tpl = tpl; c.p = p; c.n_lo = set->n_lo; c.N = Np; c.f = f; c.B = B; c.b = b;
+        c.max_enum = max_enum;
+        c.x.assign(p, 0);
+        const int64_t total = count_sets(set->n_lo, set->n_hi, Np, f);
+        if (total <= max_enum) {
+            dfs(c, p - 1, Np);
+            exact_out[k] = 1;
+        } else {
+            if (!have_cands) {
+                cands = knapsack_candidates_range(tpl, p, set->n_lo, std::max(lo, n_min), n_max, f, K, 1);
+                have_cands = true;
+            }
+            auto list = cands[(size_t)(Np - std::max(lo, n_min))];
+            std::vector<std::pair<double, size_t>> order;
+            for (size_t i = 0; i < list.size(); ++i)
+                order.emplace_back(plan_iter_lower_bound(tpl, p, list[i], K), i);
+            std::sort(order.begin(), order.end());
+            for (const auto &o : order) {
+                // no remaining candidate can beat the best found (1e-12: rounding of the bound)
+                if (c.best_thr > 0 && (double)B / o.first < c.best_thr * (1.0 - 1e-12)) break;
+                c.x = list[o.second];
+                evaluate(c);
+            }
+        }
+        if (c.best_thr < 0) { status_out[k] = OOB_E_BATCH; continue; }
+        for (int i = 0; i < p; ++i) cnt[i] = c.best_x[i];
+        thr_out[k] = c.best_thr;
+        ub_out[k] = exact_out[k] ? c.best_thr : std::max(c.best_thr, (double)B / iter_lower_bound(tpl, p, set->n_lo, Np, K));
+    }
     return OOB_OK;
 }

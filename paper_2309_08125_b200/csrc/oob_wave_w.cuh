@@ -94,6 +94,10 @@ struct WaveW {
     int *rclaim;               // [P][nranges] finalize shares claimed
     Pipe pp;                   // wavefront pipeline (pp.on = 0: plain kernel boundaries)
     int refresh;               // 1: each unit refreshes its filter entries from the range's global filter
+    int fin_spin;              // polls a merged CTA waits for its range's others (0: exit; the last finalizes alone)
+    int warp_mode;             // 1: one WARP per (profile, range) (batched sweeps' short waves: the
+                               // per-range work is a few units, a CTA per range idles on its prologue,
+                               // barrier and finalize); no pipeline, cpr = 1, no merge
     int prefetch;              // 1: each unit prefetches its tile and chunk cells into L1 (one CTA per range)
     FinArgs fa, fw;
 };
@@ -517,13 +521,14 @@ __device__ __forceinline__ void run_rows(XRing &xr, int64_t sidx, const int32_t 
     __syncwarp();
 }
 
-// One warp unit (out of line: the kernel's outer state stays out of the step loop's
-// registers): start the streamed chunk's ring, load the register tile (shadow lower bounds
+// One warp unit (inlined: an out-of-line unit measured 9% slower on cfg4, and capping the
+// kernel at 80 registers for 3 CTAs/SM spills in the step loop, +70%): start the streamed
+// chunk's ring, load the register tile (shadow lower bounds
 // of TE big-side cells; +inf beyond the row, so a sentinel's bound never passes), refresh
 // the filter entries of the outputs [olo, ohi) the unit can touch from the range's global
 // filter (minima the range's other CTAs found), then run the rows.
 template <int TE, bool LT>
-__device__ __noinline__ void run_unit(const float4 *__restrict__ SH, const Cell4 *CELL, int64_t sidx, const int32_t *wls,
+__device__ __forceinline__ void run_unit(const float4 *__restrict__ SH, const Cell4 *CELL, int64_t sidx, const int32_t *wls,
                                       int r_lo, int r_hi, int64_t bidx, int ncell, int rowB, int e0, int l1, int L,
                                       const int *outOff, int nout, unsigned acc_s, unsigned filt_s, unsigned *gfr,
                                       unsigned char *wsm, int olo, int ohi) {
@@ -911,6 +916,104 @@ __device__ __forceinline__ void pipe_signal(const Pipe &pp, int L, int kind, int
     }
 }
 
+// Warp mode of k_wave_w (w.warp_mode): every warp of the CTA owns one (profile, range) of
+// the wave — its accumulator and filter in its own shared-memory region, initialised from
+// the seeds — runs all of the range's units itself (in queue order, no unit counter) and
+// finalizes the range's W outputs from shared memory; the wave-constant tables are staged
+// once per CTA.  Same units, same exact path, same (total, key) minimum as the CTA mode.
+template <int TE>
+__device__ __forceinline__ void warp_ranges(const DevGeom &g, const WaveW &w, unsigned char *smem, ulonglong2 *acc0,
+                                            unsigned *filt0, int4 *sents, int64_t *sbase, int *scells, int *outOff,
+                                            int *upre, int *stoff, int *stcnt, int *scb, float4 *rings) {
+    const int l = w.l, nout = w.nout, L = g.L, M = g.M;
+    const int ndum = L + 2 * TE + 2;
+    const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
+    const int Ql = (l == L) ? g.n_hi : max(1, g.n_hi - 1);
+    if (tid == 0) OOB_TL_MIN(l, 0);
+    for (int i = tid; i <= L; i += NTW) {
+        stoff[i] = w.tile_off[i];
+        stcnt[i] = w.tile_cnt[i];
+    }
+    for (int i = tid; i < w.ncb; i += NTW) scb[i] = w.cb[i];
+    for (int i = tid; i < L + 2; i += NTW) {
+        sbase[i] = g.base[i];
+        if (i <= L) scells[i] = g.cells[i];
+        outOff[i] = (i >= 2 && i <= Ql && i <= l) ? c_woff(M, l, i) : nout;
+    }
+    for (int i = tid; i <= w.nents; i += NTW) {
+        upre[i] = w.upre[i];
+        if (i < w.nents) sents[i] = w.ents[i];
+    }
+    __syncthreads();
+    const int pr = (int)blockIdx.x * (NTW / 32) + wi;
+    if (pr >= g.P * w.nranges) return;
+    const int u = pr % w.nranges, p = pr / w.nranges;
+    const int64_t pc = (int64_t)p * g.C;
+    ulonglong2 *acc = acc0 + (size_t)wi * (nout + ndum);
+    unsigned *filt = filt0 + (size_t)wi * (nout + ndum);
+    const ulonglong2 *gseed = w.GACC + (size_t)pr * nout;
+    unsigned *gfilt = w.GFILT + (size_t)pr * nout;
+    for (int i0 = lane; i0 < nout + ndum; i0 += 4 * 32) {
+        ulonglong2 a[4];
+        unsigned fv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int i = i0 + j * 32;
+            const bool real = i < nout;
+            a[j] = real ? make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull) : make_ulonglong2(0ull, 0ull);
+            if (real && w.seeded) a[j] = __ldcg(gseed + i);
+            fv[j] = real ? __ldcg(gfilt + i) : 0xBF800000u;   // dummies: -1 (nothing passes)
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int i = i0 + j * 32;
+            if (i < nout + ndum) {
+                acc[i] = a[j];
+                filt[i] = fv[j];
+            }
+        }
+    }
+    __syncwarp();
+    const unsigned acc_s = (unsigned)__cvta_generic_to_shared(acc);
+    const unsigned filt_s = (unsigned)__cvta_generic_to_shared(filt);
+    unsigned char *wsm = reinterpret_cast<unsigned char *>(rings) + (size_t)wi * (XR_BYTES + XQ_BYTES);
+    int ei = 0;
+    for (int un = 0; un < w.nunits; ++un) {
+        while (upre[ei + 1] <= un) ++ei;
+        const int4 en = sents[ei];
+        const int l1 = en.x & 0xFFFF;
+        const int local = un - upre[ei];
+        const int chunk = local / en.y;
+        const int blk = local % en.y;
+        const int r_lo = scb[en.w + chunk], r_hi = scb[en.w + chunk + 1];
+        const int k = u + l1;
+        const int l2 = l - l1;
+        const bool ltiled = (en.x >> 16) & 1;
+        const int ls = ltiled ? l2 : l1, lb = ltiled ? l1 : l2;
+        const int us = ltiled ? k : u, ub = ltiled ? u : k;
+        const int ti = blk * 32 + lane;
+        const bool has = ti < stcnt[lb];
+        const int32_t code = has ? w.tiles[stoff[lb] + ti] : 0;
+        const int rowB = has ? (code >> 16) : 1;
+        const int e0 = has ? (code & 0xFFFF) : 0;
+        const int wb0 = has ? d_wofs(g, lb, rowB) : 0;
+        const int lenB = has ? d_wofs(g, lb, rowB + 1) - wb0 : 0;
+        const int ncell = max(0, min(TE, lenB - e0));
+        const int64_t sidx = pc + sbase[ls] + (int64_t)us * scells[ls] + d_wofs(g, ls, r_lo);
+        const int64_t bidx = pc + sbase[lb] + (int64_t)ub * scells[lb] + (has ? wb0 : d_wofs(g, lb, 1)) + e0;
+        if (ltiled)
+            run_unit<TE, true>(g.SH, g.CELL, sidx, g.wofs + ls * (L + 2), r_lo, r_hi, bidx, ncell, rowB, e0, l1, L,
+                               outOff, nout, acc_s, filt_s, gfilt, wsm, 0, 0);
+        else
+            run_unit<TE, false>(g.SH, g.CELL, sidx, g.wofs + ls * (L + 2), r_lo, r_hi, bidx, ncell, rowB, e0, l1, L,
+                                outOff, nout, acc_s, filt_s, gfilt, wsm, 0, 0);
+    }
+    __syncwarp();
+    if (tid % 32 == 0) OOB_TL_MAX(l, 2);
+    fin_w_range<32>(g, w.fw, pr, lane, 0, 1, acc);
+    if (lane == 0) OOB_TL_MAX(l, 3);
+}
+
 __global__ void __launch_bounds__(256) k_fin(DevGeom g, FinArgs f) {
     if ((int)blockIdx.x < f.nbw) {
         const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -954,9 +1057,11 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
     const int nout = w.nout;
     const int L = g.L, M = g.M;
     const int ndum = L + 2 * TE + 2;                              // dummy entries (absent parent rows)
-    ulonglong2 *acc = reinterpret_cast<ulonglong2 *>(smem);     // [nout] + dummy[ndum]
-    unsigned *filt = reinterpret_cast<unsigned *>(acc + nout + ndum);  // [nout + ndum] binary32 filters F(min)
-    int4 *sents = reinterpret_cast<int4 *>(filt + ((nout + ndum + 3) & ~3));   // [nents] (16 B aligned)
+    const bool wm = w.warp_mode;
+    const int nacc = wm ? (NTW / 32) * (nout + ndum) : nout + ndum;   // warp mode: one region per warp
+    ulonglong2 *acc = reinterpret_cast<ulonglong2 *>(smem);     // [nout] + dummy[ndum]  (x warps)
+    unsigned *filt = reinterpret_cast<unsigned *>(acc + nacc);  // [nout + ndum] binary32 filters F(min)  (x warps)
+    int4 *sents = reinterpret_cast<int4 *>(filt + ((nacc + 3) & ~3));   // [nents] (16 B aligned)
     int64_t *sbase = reinterpret_cast<int64_t *>(sents + w.nents);               // [L+2]
     int *scells = reinterpret_cast<int *>(sbase + L + 2);        // [L+1]
     int *outOff = scells + (L + 1);                              // [L+2] W(q) offsets (nout: none)
@@ -969,6 +1074,10 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
     float4 *rings = reinterpret_cast<float4 *>(smem + ring_off);
     const int tid = threadIdx.x;
     const int lane = tid & 31;
+    if (wm) {
+        warp_ranges<TE>(g, w, smem, acc, filt, sents, sbase, scells, outOff, upre, stoff, stcnt, scb, rings);
+        return;
+    }
     const int pr = bid / w.cpr;
     const int u = pr % w.nranges;
     const int p = pr / w.nranges;
@@ -1142,7 +1251,7 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
         __syncthreads();
         if (tid == 0) {
             int ok = atomicAdd(w.rdone + pr, 1) + 1 == w.cpr;
-            for (int it = 0; !ok && it < (1 << 22); ++it) {
+            for (int it = 0; !ok && it < w.fin_spin; ++it) {
                 __nanosleep(128);
                 ok = *(volatile int *)(w.rdone + pr) >= w.cpr;
             }

@@ -253,6 +253,21 @@ def instantiate(tset: TemplateSet, profile: int, nodes: int, f: int, global_batc
             "capped": st == OOB_E_TOO_MANY}
 
 
+def instantiate_all(tset: TemplateSet, profile: int, n_min: int, n_max: int, f: int, global_batch: int,
+                    microbatch: int, max_enumerated: int = 0) -> list[dict]:
+    """oob_instantiate_all: the plan for every node count n_min..n_max (certified bounds)."""
+    p = tset.count(profile)
+    n = n_max - n_min + 1
+    counts = np.zeros((n, p), np.int32)
+    thr, ub = np.zeros(n), np.zeros(n)
+    exact, status = np.zeros(n, np.int32), np.zeros(n, np.int32)
+    check(lib.oob_instantiate_all(tset._h, profile, n_min, n_max, f, global_batch, microbatch, max_enumerated,
+                                  counts.ctypes.data, thr.ctypes.data, ub.ctypes.data, exact.ctypes.data,
+                                  status.ctypes.data))
+    return [{"nodes": n_min + k, "counts": tuple(int(c) for c in counts[k]), "throughput": float(thr[k]),
+             "upper_bound": float(ub[k]), "exact": bool(exact[k]), "status": int(status[k])} for k in range(n)]
+
+
 def distribute_batch(per_microbatch_ms, global_batch: int, microbatch: int):
     """oob_distribute_batch: exact Eq.6; returns (nb tuple, objective)."""
     T = np.ascontiguousarray(per_microbatch_ms, dtype=np.float64)
@@ -266,3 +281,71 @@ def distribute_batch(per_microbatch_ms, global_batch: int, microbatch: int):
 
 def recommend_batch(x: int, microbatch: int, global_batch: int) -> int:
     return int(lib.oob_recommend_batch(x, microbatch, global_batch))
+
+
+ACTION_NAMES = {_lib.OOB_ACT_REINSTANTIATE: "reinstantiate", _lib.OOB_ACT_BORROW: "borrow",
+                _lib.OOB_ACT_MERGE: "merge", _lib.OOB_ACT_REMOVE: "remove", _lib.OOB_ACT_REPLAN: "replan"}
+
+
+class ExecState:
+    """oob_exec: pipelines instantiated from a template set, reconfigured on failures
+    (PAPER §5: reinstantiate / borrow / merge, batch redistribution, copy plan, sync groups)."""
+
+    def __init__(self, tset: TemplateSet, profile: int, f: int, global_batch: int, microbatch: int,
+                 counts, node_ids, layer_bytes=None):
+        c = np.ascontiguousarray(counts, dtype=np.int32)
+        ids = np.ascontiguousarray(node_ids, dtype=np.int32)
+        lb = None if layer_bytes is None else np.ascontiguousarray(layer_bytes, dtype=np.int64)
+        h = ctypes.c_void_p()
+        check(lib.oob_exec_create(tset._h, profile, f, global_batch, microbatch, c.ctypes.data, ids.ctypes.data,
+                                  ids.shape[0], None if lb is None else lb.ctypes.data, ctypes.byref(h)))
+        self._h = h
+        self._keep = tset
+
+    def pipelines(self):
+        """[(node ids, microbatches)] per pipeline."""
+        out = []
+        buf = np.zeros(4096, np.int32)
+        for i in range(lib.oob_exec_num_pipelines(self._h)):
+            n, nb = ctypes.c_int32(), ctypes.c_int64()
+            check(lib.oob_exec_pipeline(self._h, i, buf.ctypes.data, buf.shape[0], ctypes.byref(n), ctypes.byref(nb)))
+            out.append((list(int(x) for x in buf[:n.value]), nb.value))
+        return out
+
+    def fail(self, failed):
+        """oob_exec_fail: returns (actions, transfers) of the reconfiguration."""
+        f = np.ascontiguousarray(sorted(failed), dtype=np.int32)
+        rec = ctypes.c_int64()
+        check(lib.oob_exec_fail(self._h, f.ctypes.data, f.shape[0], ctypes.byref(rec)),
+              {"recommended_global_batch": rec.value})
+        return self.actions(), self.transfers()
+
+    def actions(self):
+        out = []
+        a = _lib.OobAction()
+        for i in range(lib.oob_exec_num_actions(self._h)):
+            check(lib.oob_exec_action(self._h, i, ctypes.byref(a)))
+            name = ACTION_NAMES[a.kind]
+            out.append((name, a.a) if name in ("remove", "replan") else
+                       (name, a.a, a.nodes) if name == "reinstantiate" else (name, a.a, a.b))
+        return out
+
+    def transfers(self):
+        out = []
+        t = _lib.OobTransfer()
+        for i in range(lib.oob_exec_num_transfers(self._h)):
+            check(lib.oob_exec_transfer(self._h, i, ctypes.byref(t)))
+            out.append((t.layer, t.donor, t.receiver, t.bytes))
+        return out
+
+    def sync_group(self, layer: int):
+        p = np.zeros(1024, np.int32)
+        s = np.zeros(1024, np.int32)
+        n = ctypes.c_int32()
+        check(lib.oob_exec_sync_group(self._h, layer, p.ctypes.data, s.ctypes.data, 1024, ctypes.byref(n)))
+        return [(int(a), int(b)) for a, b in zip(p[:n.value], s[:n.value])]
+
+    def __del__(self):
+        if getattr(self, "_h", None) and lib is not None:
+            lib.oob_exec_free(self._h)
+            self._h = None

@@ -199,6 +199,47 @@ def test_instantiate_capped_candidates(planner):
     assert cases >= 60 and exact >= 0.9 * cases, (cases, exact)
 
 
+def test_instantiate_all_vs_brute(planner):
+    """oob_instantiate_all: the plan for every N' in one call.  Exhaustive mode == brute force
+    (select_plan_brute) for every N'; capped mode (max_enumerated = 1: knapsack candidates +
+    the certified bound) never beats the optimum, its upper bound never falls below it, and
+    it finds the optimum in >= 90% of the N'."""
+    from oracle import coracle
+    from paper_2309_08125_b200 import planner as pl
+    rng = random.Random(321)
+    n_ex = n_cap = hit = 0
+    for it in range(40):
+        L, M = rng.randint(6, 14), rng.choice([1, 2, 4])
+        N, f, n0 = rng.randint(8, 16), rng.randint(0, 2), rng.randint(1, 2)
+        if N < (f + 1) * n0 or n0 > L:
+            continue
+        sizes = oracle_node_sizes(N, f, n0, L)
+        prof = random_profile(700 + it, L, M, rng.choice(["uniform", "lognormal", "spiky"]))
+        tpls = coracle.template_set(prof.fwd_ms, prof.bwd_ms, M, sizes[0], sizes[-1])[0]
+        ts = _set_handle(pl, tpls, L, M, sizes)
+        b = rng.choice([1, 2])
+        B = b * rng.randint(max(f + 1, 4), 12)          # brute-force Eq.6: K = B/b <= 12
+        lo = (f + 1) * n0
+        ex = planner.instantiate_all(ts, 0, lo, N, f, B, b, max_enumerated=10 ** 7)
+        ca = planner.instantiate_all(ts, 0, lo, N, f, B, b, max_enumerated=1)
+        for e, c in zip(ex, ca):
+            want = select_plan_brute(tpls, e["nodes"], f, B, b)
+            if want is None:
+                assert e["status"] != 0 and c["status"] != 0
+                continue
+            assert e["exact"] and e["throughput"] == pytest.approx(want[0], rel=1e-12) and e["counts"] == want[1]
+            assert e["upper_bound"] == e["throughput"]
+            n_ex += 1
+            if c["exact"]:
+                continue
+            assert c["throughput"] <= want[0] * (1 + 1e-12)
+            assert c["upper_bound"] >= want[0] * (1 - 1e-12)
+            assert sum(x * (sizes[0] + i) for i, x in enumerate(c["counts"])) == e["nodes"]
+            n_cap += 1
+            hit += c["throughput"] >= want[0] * (1 - 1e-12)
+    assert n_ex > 100 and n_cap > 60 and hit >= 0.9 * n_cap, (n_ex, n_cap, hit)
+
+
 def test_load_profile_json(planner, tmp_path):
     from paper_2309_08125_b200._lib import OOB_E_INVALID, OOB_E_PARSE, OobError
     prof = random_profile(5, 6, 2, "lognormal")

@@ -70,6 +70,27 @@ def test_random_small_vs_oracle(planner):
         _assert_same(ts.templates(0), want, f"case {i} L={L} M={M} {kind}")
 
 
+@pytest.mark.parametrize("warpmax", ["default", "0", "100000"])
+def test_batched_warp_mode_vs_oracle(planner, warpmax, monkeypatch):
+    """Batched sweeps run their short waves one warp per (profile, range) (OOB_DP_WARPMAX:
+    0 = never, large = every wave that fits); every setting gives the oracle's sets."""
+    cfg = CONFIGS["cfg5"]
+    base = planner.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, 6).info
+    if warpmax != "default":
+        monkeypatch.setenv("OOB_DP_WARPMAX", warpmax)
+    info = planner.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, 6).info
+    assert base.warp_waves > 0
+    if warpmax == "0":
+        assert info.warp_waves == 0
+    if warpmax == "100000":
+        assert info.warp_waves > base.warp_waves
+    profs = config_profiles(cfg, "real", count=6)
+    ts = _gpu_set(planner, profs, (cfg.L, cfg.M, cfg.N, cfg.f, cfg.n0))
+    for i, p in enumerate(profs):
+        want, _ = coracle.template_set(p.fwd_ms, p.bwd_ms, cfg.M, cfg.n0, cfg.n_max)
+        _assert_same(ts.templates(i), want, f"cfg5 profile {i} WARPMAX={warpmax}")
+
+
 def test_batched_profiles_vs_oracle(planner):
     """Batched sweep (cfg5 shape): several profiles in one call, each vs the oracle."""
     cfg = CONFIGS["cfg5"]
