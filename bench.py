@@ -184,12 +184,74 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def run_planning_grid(args):
+    """Context runs: the 36 points of tab:planning_latency —
+    ONE template of n nodes x M GPUs for L layers — on this GPU, beside the paper's seconds
+    (its Python planner on unstated hardware: context, not a target).  Device-resident GPU
+    time (CUDA events, median of --steps runs after --warmup) and the e2e latency through
+    oob_generate_templates with host buffers; points up to 5e7 splits are checked against
+    the C oracle."""
+    import torch
+    from paper_2309_08125_b200 import planner
+    from workloads import (PLANNING_GRID_GPUS, PLANNING_GRID_LAYERS, PLANNING_GRID_NODES, PLANNING_GRID_PAPER_S,
+                           gpt_profile, planning_grid_config)
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream(dev)
+    pts = []
+    for nodes in PLANNING_GRID_NODES:
+        for M in PLANNING_GRID_GPUS:
+            for li, L in enumerate(sorted(PLANNING_GRID_LAYERS)):
+                cfg = planning_grid_config(L, nodes, M)
+                prof = gpt_profile(cfg)
+                plan = planner.DPPlan(L, M, nodes, nodes, 1)
+                info = plan.info
+                fwd = torch.tensor(prof.fwd_ms[None], dtype=torch.float64, device=dev)
+                bwd = torch.tensor(prof.bwd_ms[None], dtype=torch.float64, device=dev)
+                ws = torch.empty(info.workspace_bytes, dtype=torch.uint8, device=dev)
+                packed = torch.empty(info.packed_bytes, dtype=torch.uint8, device=dev)
+
+                def run():
+                    plan.run(fwd.data_ptr(), bwd.data_ptr(), ws.data_ptr(), ws.numel(), packed.data_ptr(),
+                             stream.cuda_stream)
+                for _ in range(max(2, args.warmup)):
+                    run()
+                ms = []
+                for _ in range(max(3, args.steps)):
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    run()
+                    b.record(stream)
+                    torch.cuda.synchronize()
+                    ms.append(a.elapsed_time(b))
+                hp = planner.Profile.from_arrays(prof.fwd_ms, prof.bwd_ms)
+                t0 = time.perf_counter()
+                ts = planner.generate_templates([hp], nodes=nodes, gpus_per_node=M, f=0, n0=nodes, device=0)
+                e2e_ms = (time.perf_counter() - t0) * 1e3
+                checked = None
+                if info.splits_per_profile <= 5e7:
+                    from oracle import coracle
+                    want, _ = coracle.template_set(prof.fwd_ms, prof.bwd_ms, M, nodes, nodes)
+                    checked = ts.templates(0) == want
+                paper_s = PLANNING_GRID_PAPER_S[(nodes, M)][li]
+                gpu_ms = statistics.median(ms)
+                pts.append({"layers": L, "nodes": nodes, "gpus_per_node": M, "cells": info.cells_per_profile,
+                            "splits": info.splits_per_profile, "gpu_ms": gpu_ms, "e2e_ms": e2e_ms,
+                            "paper_s": paper_s, "paper_over_e2e": paper_s * 1e3 / e2e_ms,
+                            "oracle_match": checked, "iter_ms": ts.templates(0)[0]["total"]})
+    line = {"metric": "planning latency grid (tab:planning_latency, one template)", "unit": "ms",
+            "workload": "planning_grid", "data": "synthetic GPT-shaped profiles (hidden 1024/2560/8192/12288)",
+            "paper_context": "PAPER P:817-836, Python planner, hardware unstated (seconds)",
+            "clocks_note": "context run, not the bench contract", "points": pts}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="cfg4", choices=sorted(CONFIGS))
+    ap.add_argument("--workload", default="cfg4", choices=sorted(CONFIGS) + ["planning_grid"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--profiles-per-rank", type=int, default=0,
                     help="profiles per rank (default: 1; cfg5: 1024/N)")
@@ -201,6 +263,9 @@ def main():
     ap.add_argument("--ref-full", action="store_true",
                     help="reference arm: time the oracle on the full template set (minutes for cfg4)")
     args = ap.parse_args()
+    if args.workload == "planning_grid":
+        run_planning_grid(args)
+        return
     cfg = CONFIGS[args.workload]
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":

@@ -103,6 +103,9 @@ oob_status oob_profile_from_arrays(int32_t L, int32_t M, const double *fwd_ms,
 void oob_profile_free(oob_profile *p);
 int32_t oob_profile_layers(const oob_profile *p);
 int32_t oob_profile_gpus_per_node(const oob_profile *p);
+/* Copy the profile's costs into caller-owned host arrays fwd_ms/bwd_ms [L][M] (either may be
+ * NULL) and state_bytes [L] (may be NULL).  Errors: OOB_E_INVALID. */
+oob_status oob_profile_costs(const oob_profile *p, double *fwd_ms, double *bwd_ms, int64_t *state_bytes);
 
 /* SPEC min_nodes (P:335 gives no formula; DESIGN reading R5):
  * n0 = ceil((sum state_bytes + samples_per_gpu * sum act_bytes) / (M * gpu_mem * util)).
@@ -180,6 +183,8 @@ typedef struct {
     int32_t num_sms;                /* SMs of the device the plan was built for */
     int32_t world;                  /* ranks sharing the wavefronts (oob_dp_set_comm) */
     int32_t warp_waves;             /* batched wavefronts run one warp per (profile, range) */
+    int32_t small_range;            /* in-node cells one warp per (profile, range) */
+    int32_t reserved;
 } oob_dp_info;
 
 oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int32_t n_hi,

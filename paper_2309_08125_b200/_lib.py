@@ -53,7 +53,8 @@ class OobDpInfo(ctypes.Structure):
                 ("packed_template_bytes", c_size_t), ("packed_profile_bytes", c_size_t),
                 ("packed_bytes", c_size_t), ("kernel", c_int32), ("pipelined", c_int32),
                 ("fused", c_int32), ("seeded", c_int32), ("chunk_max", c_int32), ("refresh", c_int32),
-                ("small_pairs", c_int32), ("num_sms", c_int32), ("world", c_int32), ("warp_waves", c_int32)]
+                ("small_pairs", c_int32), ("num_sms", c_int32), ("world", c_int32), ("warp_waves", c_int32),
+                ("small_range", c_int32), ("reserved", c_int32)]
 
 
 class OobAction(ctypes.Structure):
@@ -83,6 +84,7 @@ _proto("oob_profile_from_arrays", ctypes.c_int, [c_int32, c_int32, c_void_p, c_v
 _proto("oob_profile_free", None, [c_void_p])
 _proto("oob_profile_layers", c_int32, [c_void_p])
 _proto("oob_profile_gpus_per_node", c_int32, [c_void_p])
+_proto("oob_profile_costs", ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p])
 _proto("oob_min_nodes", ctypes.c_int, [c_void_p, c_int32, c_int64, c_double, c_int32, P(c_int32)])
 _proto("oob_node_sizes", ctypes.c_int, [c_int32, c_int32, c_int32, c_int32, P(c_int32), P(c_int32)])
 _proto("oob_generate_templates", ctypes.c_int, [P(c_void_p), c_int32, P(OobPlanOpts), P(c_void_p)])
@@ -127,7 +129,7 @@ _proto("oob_exec_sync_group", ctypes.c_int, [c_void_p, c_int32, c_void_p, c_void
 
 EXPORTED = [
     "oob_last_error", "oob_status_string", "oob_load_profile", "oob_profile_from_arrays",
-    "oob_profile_free", "oob_profile_layers", "oob_profile_gpus_per_node", "oob_min_nodes",
+    "oob_profile_free", "oob_profile_layers", "oob_profile_gpus_per_node", "oob_profile_costs", "oob_min_nodes",
     "oob_node_sizes", "oob_generate_templates", "oob_template_set_profiles", "oob_template_count",
     "oob_template_get", "oob_template_set_free", "oob_dp_plan_create", "oob_dp_plan_free",
     "oob_dp_plan_info", "oob_dp_run", "oob_dp_set_timing", "oob_dp_kernel_time",

@@ -266,6 +266,7 @@ struct Knobs {
     double shard_min = SHARD_MIN_SPLITS;   // OOB_DP_SHARDMIN: waves with fewer splits run redundantly
     long long spin_max = 1ll << 24;        // OOB_DP_PIPE_SPIN: polls before a pipeline wait times out
     int fin_wait = 1;          // OOB_DP_FINWAIT=0: merged CTAs exit, the range's last one finalizes alone
+    int small_range = 1;       // OOB_DP_SMALLRANGE=0: in-node cells thread(s) per cell instead of warp per range
     int warp_units = 96;       // OOB_DP_WARPMAX: batched waves with <= this many units per range run one
                                // warp per (profile, range) (0: never)
     int debug = 0;             // OOB_DP_DEBUG: per-wave plan on stderr
@@ -288,6 +289,7 @@ Knobs read_knobs() {
     if (const char *v = env("OOB_DP_PIPE_SPIN")) k.spin_max = std::max(0ll, std::atoll(v));
     if (const char *v = env("OOB_DP_FINWAIT")) k.fin_wait = std::atoi(v) != 0;
     if (const char *v = env("OOB_DP_WARPMAX")) k.warp_units = std::max(0, std::atoi(v));
+    if (const char *v = env("OOB_DP_SMALLRANGE")) k.small_range = std::max(0, std::min(2, std::atoi(v)));
     if (env("OOB_DP_DEBUG")) k.debug = 1;
     return k;
 }
@@ -462,6 +464,22 @@ static int small_tpc(const Geometry &g, int l, int per) {
     return t;
 }
 
+// in-node cells one warp per (profile, range) (fin_small_range): batched sweeps with M <= 8,
+// unless OOB_DP_SMALLRANGE=0 (a single profile has too few ranges: one warp walking all
+// layer splits of a range sits on the pipelined critical path, cfg4 +16%; =2 forces it)
+static bool small_range_on(const oob_dp_plan *pl) {
+    return pl->g.M <= 8 && (pl->kn.small_range == 2 || (pl->kn.small_range == 1 && pl->P > 1));
+}
+
+// blocks of 256 threads computing the in-node cells of wave l (all profiles)
+static int64_t small_blocks(const oob_dp_plan *pl, int l) {
+    const Geometry &g = pl->g;
+    if (small_range_on(pl)) return ((int64_t)pl->P * (g.L - l + 1) + NTW / 32 - 1) / (NTW / 32);
+    const int tpc = small_tpc(g, l, pl->kn.small_pairs);
+    const int64_t ns = (int64_t)pl->P * (g.L - l + 1) * small_cells(g, l);
+    return (ns + (256 / tpc) - 1) / (256 / tpc);
+}
+
 // Pipelined wavefronts (k_wave_w as programmatic dependent launches synchronised by
 // counters): only the fused single-pass, unsharded W kernel, and only when every wave's main
 // grid fits the resident CTA slots (a single profile); batched sweeps have far more CTAs
@@ -599,9 +617,7 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
             if (l >= 3) {                       // produced by launch l-1's extra blocks
                 const int64_t nsd = wh.seed ? (int64_t)num_profiles * nr * wh.nout : 0;
                 ex[l] = (int32_t)((nsd + 255) / 256);
-                const int tpc = small_tpc(g, l, pl->kn.small_pairs);
-                const int64_t ns = (int64_t)num_profiles * nr * small_cells(g, l);
-                ex[(L + 2) + l] = (int32_t)((ns + (256 / tpc) - 1) / (256 / tpc));
+                ex[(L + 2) + l] = small_cells(g, l) > 0 ? (int32_t)small_blocks(pl, l) : 0;
             }
             ex[2 * (L + 2) + l] = wh.nents > 0 ? (int32_t)((int64_t)num_profiles * nr * wh.cpr) : 0;
         }
@@ -727,6 +743,8 @@ extern "C" oob_status oob_dp_plan_info(const oob_dp_plan *pl, oob_dp_info *out) 
     out->world = pl->world;
     out->warp_waves = 0;
     for (int l = 2; l <= g.L; ++l) out->warp_waves += pl->waves[l].warp ? 1 : 0;
+    out->small_range = small_range_on(pl) ? 1 : 0;
+    out->reserved = 0;
     return OOB_OK;
 }
 
@@ -812,8 +830,8 @@ static FinArgs make_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglong2 *ga
     f.ls = ls;
     f.nsmall = ls ? small_cells(G, ls) : 0;
     f.tpc = ls ? small_tpc(G, ls, pl->kn.small_pairs) : 32;
-    const int64_t ns = ls ? (int64_t)pl->P * (G.L - ls + 1) * f.nsmall : 0;
-    *nbsmall = (ns + (256 / f.tpc) - 1) / (256 / f.tpc);
+    f.small_range = small_range_on(pl) ? 1 : 0;
+    *nbsmall = (ls && f.nsmall > 0) ? small_blocks(pl, ls) : 0;
     return f;
 }
 
@@ -823,7 +841,7 @@ static cudaError_t launch_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglon
     const FinArgs f = make_fin(pl, dg, gacc, lw, ls, sharded, &nbs);
     const int64_t blocks = f.nbw + f.nbseed + nbs;
     if (blocks == 0) return cudaSuccess;
-    k_fin<<<(unsigned)blocks, 256, 0, stream>>>(dg, f);
+    k_fin<<<(unsigned)blocks, 256, f.small_range ? SR_SMEM : 0, stream>>>(dg, f);
     return cudaGetLastError();
 }
 

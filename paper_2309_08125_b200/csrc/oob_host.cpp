@@ -235,6 +235,13 @@ extern "C" oob_status oob_load_profile(const char *path, oob_profile **out) {
 extern "C" void oob_profile_free(oob_profile *p) { delete p; }
 extern "C" int32_t oob_profile_layers(const oob_profile *p) { return p ? p->L : 0; }
 extern "C" int32_t oob_profile_gpus_per_node(const oob_profile *p) { return p ? p->M : 0; }
+extern "C" oob_status oob_profile_costs(const oob_profile *p, double *fwd, double *bwd, int64_t *state_bytes) {
+    if (!p) return fail(OOB_E_INVALID, "oob_profile_costs: NULL profile");
+    if (fwd) std::copy(p->fwd.begin(), p->fwd.end(), fwd);
+    if (bwd) std::copy(p->bwd.begin(), p->bwd.end(), bwd);
+    if (state_bytes) std::copy(p->state_bytes.begin(), p->state_bytes.end(), state_bytes);
+    return OOB_OK;
+}
 
 extern "C" oob_status oob_min_nodes(const oob_profile *p, int32_t nodes, int64_t gpu_mem,
                                     double util, int32_t spg, int32_t *n0_out) {

@@ -64,6 +64,7 @@ struct FinArgs {
     unsigned *GFW, *GFS;           // global filters (binary32 bits of F(min)) of waves lw / lseed
     int ls, nsmall;                // small cells of wave ls (ls = 0: none); cells per range
     int tpc;                       // threads per small cell
+    int small_range;               // 1: one warp per (profile, range) stages the child I-parts in smem
 };
 
 struct WaveW {
@@ -871,6 +872,98 @@ __device__ __forceinline__ void fin_small_block(const DevGeom &g, const FinArgs 
                        (int)(bkey & 1023u));
 }
 
+// Small cells of wave f.ls, one WARP per (profile, range) (f.small_range; M <= 8): lane i
+// owns the range's in-node cell i (I(r) or W(1), S' >= 2; chunks of 32 when there are
+// more) and scans the layer splits l1 ascending — for each, the warp stages the I-parts of
+// the two child slabs ([u, u+l1) and [u+l1, v), <= (M-1)M/2 cells each) in shared memory,
+// the next l1's cells in flight in registers — then every device split m and stage split s
+// ascending with a strict "<": the oracle's first minimum in (k, m, s) order, read from
+// shared memory instead of one global load per child (the cells of a range share them).
+constexpr int SR_IPMAX = 28;       // (M-1)M/2 for M <= 8
+constexpr int SR_SMEM = (NTW / 32) * 2 * SR_IPMAX * 32;   // bytes per 256-thread block
+__device__ __forceinline__ void fin_small_range(const DevGeom &g, const FinArgs &f, int64_t bid,
+                                                unsigned char *smem) {
+    const int l = f.ls, M = g.M;
+    const int nr = g.L - l + 1;
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    const int64_t pr = bid * (blockDim.x >> 5) + wi;
+    if (pr >= (int64_t)g.P * nr) return;
+    const int u = (int)(pr % nr), p = (int)(pr / nr);
+    const int64_t pc = (int64_t)p * g.C;
+    const Cell4 *CP = g.CELL + pc;
+    Cell4 *buf = reinterpret_cast<Cell4 *>(smem) + (size_t)wi * 2 * SR_IPMAX;   // [left I-part][right I-part]
+    const int nsm = min(g.A, M);                                   // alloc indices 0..M-1: I(1..M-1), W(1)
+    for (int c0 = 0; c0 < f.nsmall; c0 += 32) {
+        const int ci = c0 + lane;
+        const bool active = ci < f.nsmall;
+        int a = 0, Sp = 2;
+        if (active) {
+            int rem = ci;
+            for (int aa = 0; aa < nsm; ++aa) {
+                const int c = max(0, d_hi(g, aa, l) - 1);
+                if (rem < c) { a = aa; Sp = 2 + rem; break; }
+                rem -= c;
+            }
+        }
+        const int r = d_is_whole(g, a) ? M : d_alloc_n(g, a);   // GPUs of the cell's node part
+        const double dSp3 = (double)(3 * Sp - 1);
+        double best = D_INF;
+        uint32_t bkey = 0xFFFFFFFFu;
+        // staged cells of layer split l1: lane j holds cells j and j + 32 of [left | right]
+        Cell4 nx[2 * ((2 * SR_IPMAX + 31) / 32)];
+        auto fetch = [&](int l1) {
+            const int l2 = l - l1;
+            const int nl = c_ipart(M, l1), nrt = c_ipart(M, l2);
+            const Cell4 *lrow = CP + g.base[l1] + (int64_t)u * g.cells[l1];
+            const Cell4 *rrow = CP + g.base[l2] + (int64_t)(u + l1) * g.cells[l2];
+#pragma unroll
+            for (int t = 0; t < (int)(sizeof(nx) / sizeof(nx[0])); ++t) {
+                const int i = lane + 32 * t;
+                if (i < nl) nx[t] = d_load(lrow + i);
+                else if (i >= SR_IPMAX && i - SR_IPMAX < nrt) nx[t] = d_load(rrow + (i - SR_IPMAX));
+            }
+        };
+        fetch(1);
+        for (int l1 = 1; l1 < l; ++l1) {
+            __syncwarp();
+#pragma unroll
+            for (int t = 0; t < (int)(sizeof(nx) / sizeof(nx[0])); ++t) {
+                const int i = lane + 32 * t;
+                if (i < 2 * SR_IPMAX) buf[i] = nx[t];
+            }
+            __syncwarp();
+            if (l1 + 1 < l) fetch(l1 + 1);                        // next split's cells in flight
+            if (!active) continue;
+            const int l2 = l - l1;
+            const Cell4 *lrow = buf - 1;                           // I(m) cell s at lrow[c_ipart(m, l1) + s]
+            const Cell4 *rrow = buf + SR_IPMAX - 1;
+            for (int m = 1; m <= r - 1; ++m) {
+                const int s_lo = max(1, Sp - min(l2, r - m));
+                const int s_hi = min(Sp - 1, min(l1, m));
+                const Cell4 *lb = lrow + c_ipart(m, l1);
+                const Cell4 *rb = rrow + c_ipart(r - m, l2) + Sp;
+                for (int s = s_lo; s <= s_hi; ++s) {
+                    const Cell4 Lc = lb[s];
+                    const Cell4 Rc = rb[-s];
+                    const double T1 = __dadd_rn(Lc.T1, Rc.T1);
+                    const bool left = Lc.TS >= Rc.TS;
+                    const double T3 = left ? __dadd_rn(Lc.T3, Rc.T1) : Rc.T3;
+                    const double TS = left ? Lc.TS : Rc.TS;
+                    const double KD = left ? d_kd(Lc.C1, s) : __dadd_rn((double)s, d_kd(Rc.C1, Sp - s));
+                    const double T2 = __dmul_rn(__dadd_rn(KD, dSp3), TS);
+                    const double tot = __dadd_rn(__dadd_rn(T1, T2), T3);
+                    if (tot < best) {
+                        best = tot;
+                        bkey = ((uint32_t)l1 << 20) | ((uint32_t)(m - 1) << 10) | (uint32_t)s;
+                    }
+                }
+            }
+        }
+        if (active)
+            d_write_winner(g, pc, Sp, u, l, a, (int)(bkey >> 20), (int)((bkey >> 10) & 1023u), (int)(bkey & 1023u));
+    }
+}
+
 // ---------------------------------------------------------------- wavefront pipeline
 // With OOB_DP_PIPE, wavefront l+1's kernel is launched as a programmatic dependent of wave
 // l's (it starts once every CTA of wave l has started) and synchronises through per-wave
@@ -1024,7 +1117,9 @@ __global__ void __launch_bounds__(256) k_fin(DevGeom g, FinArgs f) {
         fin_seed_one(g, f, (int64_t)(blockIdx.x - f.nbw) * blockDim.x + threadIdx.x);
         return;
     }
-    fin_small_block(g, f, (int64_t)blockIdx.x - f.nbw - f.nbseed);
+    extern __shared__ __align__(16) unsigned char fsm[];
+    if (f.small_range) fin_small_range(g, f, (int64_t)blockIdx.x - f.nbw - f.nbseed, fsm);
+    else fin_small_block(g, f, (int64_t)blockIdx.x - f.nbw - f.nbseed);
 }
 
 template <int TE>
@@ -1047,7 +1142,8 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
             // in-node cells of wave l+1 read in-node cells of waves <= l
             if (threadIdx.x == 0) pipe_wait(w.pp, L_of(g), w.fa.ls - 1, 2);
             __syncthreads();
-            fin_small_block(g, w.fa, (int64_t)ab - w.fa.nbseed);
+            if (w.fa.small_range) fin_small_range(g, w.fa, (int64_t)ab - w.fa.nbseed, smem);
+            else fin_small_block(g, w.fa, (int64_t)ab - w.fa.nbseed);
             pipe_signal(w.pp, L_of(g), 1, w.fa.ls);
         }
         if (threadIdx.x == 0) OOB_TL_MAX(w.l, 5);

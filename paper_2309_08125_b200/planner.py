@@ -54,6 +54,14 @@ class Profile:
     def M(self) -> int:
         return lib.oob_profile_gpus_per_node(self._h)
 
+    def costs(self):
+        """(fwd_ms, bwd_ms [L][M], state_bytes [L]) as held by the library (oob_profile_costs)."""
+        f = np.zeros((self.L, self.M))
+        b = np.zeros((self.L, self.M))
+        st = np.zeros(self.L, np.int64)
+        check(lib.oob_profile_costs(self._h, f.ctypes.data, b.ctypes.data, st.ctypes.data))
+        return f, b, st
+
     def min_nodes(self, nodes: int, gpu_mem_bytes: int, util: float = 0.8, samples_per_gpu: int = 1) -> int:
         out = ctypes.c_int32()
         check(lib.oob_min_nodes(self._h, nodes, gpu_mem_bytes, util, samples_per_gpu, ctypes.byref(out)))

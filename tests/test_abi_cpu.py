@@ -252,7 +252,14 @@ def test_load_profile_json(planner, tmp_path):
     path.write_text(text)
     p = planner.load_profile(str(path))
     assert (p.L, p.M) == (6, 2)
-    # the loaded profile plans identically to the array profile (host-only check: sizes)
+    # the parsed costs are the written ones, bit for bit (repr round-trips binary64), so the
+    # loaded profile plans exactly like the array profile
+    f, b, st = p.costs()
+    assert np.array_equal(f, prof.fwd_ms) and np.array_equal(b, prof.bwd_ms)
+    assert list(st) == [1000 + l for l in range(6)]
+    q = planner.Profile.from_arrays(prof.fwd_ms, prof.bwd_ms)
+    qf, qb, _ = q.costs()
+    assert np.array_equal(qf, f) and np.array_equal(qb, b)
     bad = dict(doc)
     bad["layers"] = [dict(doc["layers"][0])]
     bad["layers"][0]["fwd_ms"] = {"1": 1.0}

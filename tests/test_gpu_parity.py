@@ -79,7 +79,7 @@ def test_batched_warp_mode_vs_oracle(planner, warpmax, monkeypatch):
     if warpmax != "default":
         monkeypatch.setenv("OOB_DP_WARPMAX", warpmax)
     info = planner.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, 6).info
-    assert base.warp_waves > 0
+    assert base.warp_waves > 0 and base.small_range == 1
     if warpmax == "0":
         assert info.warp_waves == 0
     if warpmax == "100000":
@@ -222,6 +222,8 @@ VARIANTS = [
     ({"OOB_DP_PIPE": "0", "OOB_DP_SEEDINIT": "0"}, {"pipelined": 0, "seeded": 0}),
     ({"OOB_DP_CHMAX": "24"}, {"chunk_max": 24}),               # short units: many per range, long queues
     ({"OOB_DP_REFRESH": "0"}, {"refresh": 0}),                 # no per-unit filter refresh
+    ({"OOB_DP_SMALLRANGE": "2"}, {"small_range": 1}),          # in-node cells one warp per range (forced)
+    ({"OOB_DP_FINWAIT": "0"}, {}),                             # merged CTAs exit; last one finalizes alone
 ]
 
 

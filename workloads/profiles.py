@@ -103,6 +103,26 @@ CONFIGS = {
                    48, 8, 128, 2, 1, num_profiles=1024, seed=5000),
 }
 
+# tab:planning_latency: one template of n nodes x M GPUs for 24/32/64/96
+# layers.  The paper names the 24-layer (BERT-Large, GPT-2, GPT-3 Medium) and 32-layer
+# (GPT-3 2.7B/6.7B) models; the 64- and 96-layer profiles are not described, so the
+# grid uses GPT-shaped profiles of hidden size 1024 / 2560 / 8192 / 12288.
+PLANNING_GRID_LAYERS = {24: 1024, 32: 2560, 64: 8192, 96: 12288}
+PLANNING_GRID_NODES = (8, 16, 24)
+PLANNING_GRID_GPUS = (1, 4, 8)
+PLANNING_GRID_PAPER_S = {   # seconds, [nodes][gpus] -> (24, 32, 64, 96 layers)
+    (8, 1): (0.28, 0.71, 9.65, 68.50), (8, 4): (0.41, 1.15, 11.58, 74.56), (8, 8): (0.54, 1.50, 20.98, 109.76),
+    (16, 1): (3.37, 7.45, 66.35, 540.36), (16, 4): (4.56, 10.41, 108.10, 649.67),
+    (16, 8): (4.90, 11.78, 176.04, 1213.63), (24, 1): (11.35, 30.11, 262.47, 1477.54),
+    (24, 4): (14.78, 45.80, 472.53, 2153.84), (24, 8): (15.59, 49.25, 520.08, 3297.92)}
+
+
+def planning_grid_config(L: int, nodes: int, M: int) -> "Config":
+    """The grid point as a Config: one template of `nodes` nodes (n0 = nodes, f = 0, N = nodes)."""
+    return Config(f"grid-L{L}-n{nodes}-g{M}", f"tab:planning_latency {L} layers, {nodes} nodes x {M} GPUs",
+                  L, M, nodes, 0, nodes, hidden=PLANNING_GRID_LAYERS[L], seq=2048, microbatch=1, seed=200 + L)
+
+
 VOCAB = 50257
 ASSUMED_TFLOPS = 400e12   # per-GPU effective throughput used to turn FLOPs into ms
 TP_EFF = 0.85             # SPEC S:61 synth formula fwd[d] = fwd[1] / (1 + eff*(d-1))
