@@ -82,6 +82,9 @@ typedef struct {
     void *comm;                 /* optional ncclComm_t of `world` ranks (oob_nccl_comm_create),
                                    borrowed; NULL or world <= 1: this GPU only */
     int32_t world, rank;        /* ranks of `comm` and this process's rank */
+    int32_t tp_pow2;            /* stage mask: GPU counts per stage powers of two (R31) */
+    double stage_mem_bytes;     /* > 0: stage mask sum_l (state_bytes_l + samples_per_gpu *
+                                   act_bytes_l) / d <= stage_mem_bytes (R31); 0: none */
 } oob_plan_opts;
 
 /* ------------------------------------------------------------------ errors */
@@ -193,6 +196,15 @@ void oob_dp_plan_free(oob_dp_plan *plan);
 oob_status oob_dp_plan_info(const oob_dp_plan *plan, oob_dp_info *out);
 oob_status oob_dp_run(oob_dp_plan *plan, const double *d_fwd, const double *d_bwd,
                       void *d_workspace, size_t workspace_bytes, void *d_packed, void *stream);
+/* Stage masks (variants the paper is silent on, DESIGN reading R31): a
+ * stage of layers [u, v) on d GPUs of one node is allowed only if d is a power of two
+ * (pow2_tp != 0) and, when d_stage_bytes (device float64 [num_profiles][L], borrowed until
+ * the plan's runs complete) is non-NULL, sum_{l=u}^{v-1} stage_bytes[l] / d <= mem_cap_bytes.
+ * A disallowed stage is infinite like one spanning nodes; a size with no allowed
+ * mapping gives an infeasible template (num_stages = 0, costs +inf; packed status 3).
+ * pow2_tp = 0 with d_stage_bytes = NULL: no masks (the paper's method).  Errors: OOB_E_INVALID. */
+oob_status oob_dp_set_stage_masks(oob_dp_plan *plan, int32_t pow2_tp, const double *d_stage_bytes,
+                                  double mem_cap_bytes);
 /* Optional CUDA-event timing of the wavefront kernel (the dominant kernel): when enabled,
  * oob_dp_run records events around each wavefront launch on `stream`; oob_dp_kernel_time
  * returns the summed elapsed ms and number of launches since the last reset (it

@@ -48,9 +48,10 @@ def _gpu_assignments(S: int, n: int, M: int):
         yield from rec(0)
 
 
-def brute_force(fwd, bwd, M: int, n: int, S_only: int | None = None):
+def brute_force(fwd, bwd, M: int, n: int, S_only: int | None = None, allowed=None):
     """Minimum closed-form total over all mappings; returns (best_total, [argmin mappings]).
-    A mapping is a tuple of stages (u, v, d, node).  S_only restricts the stage count."""
+    A mapping is a tuple of stages (u, v, d, node).  S_only restricts the stage count;
+    allowed(u, v, d) (optional) excludes mappings with a disallowed stage (stage masks)."""
     L = len(fwd)
     best = INF
     arg = []
@@ -65,6 +66,8 @@ def brute_force(fwd, bwd, M: int, n: int, S_only: int | None = None):
                 bounds.append((u, u + c))
                 u += c
             for asg in assigns:
+                if allowed is not None and not all(allowed(b[0], b[1], g) for b, (_, g) in zip(bounds, asg)):
+                    continue
                 times = [float(stage_time(fwd, bwd, b[0], b[1], g)) for b, (_, g) in zip(bounds, asg)]
                 tot = closed_form(times)[0]
                 mapping = tuple((b[0], b[1], g, node) for b, (node, g) in zip(bounds, asg))

@@ -34,6 +34,9 @@ typedef struct {
 typedef struct {
     int L, M, Qmax, A;    /* A = number of allocation kinds: I(1..M-1), W(1..Qmax) */
     const double *fwd, *bwd;
+    int pow2;             /* stage masks (reading R31): d must be a power of two */
+    const double *stage_bytes;   /* [L] or NULL: sum/d <= mem_cap */
+    double mem_cap;
     ocell **memo;         /* [(u*(L+1)+v)*A + a] -> array indexed by S' (1..cap) */
     long long cells, splits;
 } oracle_t;
@@ -68,6 +71,18 @@ static double stage_time(const oracle_t *o, int u, int v, int d) {
     return t;
 }
 
+/* reading R31 (variants): the stage [u, v) on d GPUs is allowed iff d is a
+ * power of two (pow2) and sum_{l=u}^{v-1} stage_bytes[l] / d <= mem_cap (left to right) */
+static int stage_allowed(const oracle_t *o, int u, int v, int d) {
+    if (o->pow2 && (d & (d - 1)) != 0) return 0;
+    if (o->stage_bytes) {
+        double tot = 0.0;
+        for (int k = u; k < v; ++k) tot = tot + o->stage_bytes[k];
+        if (tot / (double)d > o->mem_cap) return 0;
+    }
+    return 1;
+}
+
 static int stage_cap(const oracle_t *o, int u, int v, int a) {
     int c = v - u, g = alloc_gpus(o, a);
     return c < g ? c : g;
@@ -89,6 +104,7 @@ static const ocell *T(oracle_t *o, int Sp, int u, int v, int a) {
     if (Sp == 1) {
         if (is_whole(o, a) && alloc_n(o, a) >= 2) { c->state = 2; return c; }   /* P:452 */
         int d = is_whole(o, a) ? o->M : alloc_n(o, a);
+        if (!stage_allowed(o, u, v, d)) { c->state = 2; return c; }           /* masked (R31) */
         double t = stage_time(o, u, v, d);                                      /* Eq.4 */
         c->T1 = t; c->T3 = t; c->tstar = t; c->kstar = 0;
         c->k = c->m = c->s = -1;
@@ -171,15 +187,16 @@ static void backtrack(oracle_t *o, int Sp, int u, int v, int a, int node, int go
  * stages[i*L*5 + j*5 + {u, v, d, node, gpu_offset}] for j < S[i].
  * Returns 0 on success, 1 when some template is infeasible, 2 on bad arguments.
  */
-int oob_oracle_template_set(int L, int M, const double *fwd, const double *bwd,
-                            int n_lo, int n_hi, int32_t *S_out, int32_t *kstar_out,
-                            double *costs_out, int32_t *stages_out,
-                            long long *cells_out, long long *splits_out) {
+int oob_oracle_template_set_masked(int L, int M, const double *fwd, const double *bwd,
+                                   int n_lo, int n_hi, int pow2, const double *stage_bytes, double mem_cap,
+                                   int32_t *S_out, int32_t *kstar_out, double *costs_out, int32_t *stages_out,
+                                   long long *cells_out, long long *splits_out) {
     if (L < 1 || M < 1 || n_lo < 1 || n_hi < n_lo || n_hi > L) return 2;
     oracle_t o;
     memset(&o, 0, sizeof o);
     o.L = L; o.M = M; o.Qmax = n_hi; o.A = (M - 1) + n_hi;
     o.fwd = fwd; o.bwd = bwd;
+    o.pow2 = pow2; o.stage_bytes = stage_bytes; o.mem_cap = mem_cap;
     size_t nkeys = (size_t)(L + 1) * (L + 1) * o.A;
     o.memo = (ocell **)calloc(nkeys, sizeof(ocell *));
     if (!o.memo) return 2;
@@ -215,4 +232,12 @@ int oob_oracle_template_set(int L, int M, const double *fwd, const double *bwd,
     for (size_t i = 0; i < nkeys; ++i) free(o.memo[i]);
     free(o.memo);
     return rc;
+}
+
+int oob_oracle_template_set(int L, int M, const double *fwd, const double *bwd,
+                            int n_lo, int n_hi, int32_t *S_out, int32_t *kstar_out,
+                            double *costs_out, int32_t *stages_out,
+                            long long *cells_out, long long *splits_out) {
+    return oob_oracle_template_set_masked(L, M, fwd, bwd, n_lo, n_hi, 0, NULL, 0.0, S_out, kstar_out, costs_out,
+                                          stages_out, cells_out, splits_out);
 }

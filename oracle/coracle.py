@@ -35,13 +35,21 @@ def _load():
                       ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                       ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_longlong),
                       ctypes.POINTER(ctypes.c_longlong)]
+        g = lib.oob_oracle_template_set_masked
+        g.restype = ctypes.c_int
+        g.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                      ctypes.c_int, ctypes.c_void_p, ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p,
+                      ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_longlong),
+                      ctypes.POINTER(ctypes.c_longlong)]
         _lib = lib
     return _lib
 
 
-def template_set(fwd, bwd, M: int, n_lo: int, n_hi: int):
-    """Templates for sizes n_lo..n_hi; same dict format as oracle.dp.TemplateDP.template.
-    Also returns (cells, splits) the oracle evaluated."""
+def template_set(fwd, bwd, M: int, n_lo: int, n_hi: int, pow2_tp: bool = False, stage_bytes=None,
+                 mem_cap=None):
+    """Templates for sizes n_lo..n_hi; same dict format as oracle.dp.TemplateDP.template
+    (None for a size without a feasible mapping: stage masks, reading R31).  Also returns
+    (cells, splits) the oracle evaluated."""
     lib = _load()
     fwd = np.ascontiguousarray(fwd, dtype=np.float64)
     bwd = np.ascontiguousarray(bwd, dtype=np.float64)
@@ -53,9 +61,12 @@ def template_set(fwd, bwd, M: int, n_lo: int, n_hi: int):
     stages = np.zeros((p, L, 5), np.int32)
     cells = ctypes.c_longlong(0)
     splits = ctypes.c_longlong(0)
-    rc = lib.oob_oracle_template_set(L, M, fwd.ctypes.data, bwd.ctypes.data, n_lo, n_hi,
-                                     S.ctypes.data, ks.ctypes.data, costs.ctypes.data,
-                                     stages.ctypes.data, ctypes.byref(cells), ctypes.byref(splits))
+    sb = None if stage_bytes is None else np.ascontiguousarray(stage_bytes, dtype=np.float64)
+    rc = lib.oob_oracle_template_set_masked(L, M, fwd.ctypes.data, bwd.ctypes.data, n_lo, n_hi,
+                                            1 if pow2_tp else 0, None if sb is None else sb.ctypes.data,
+                                            float(mem_cap) if mem_cap is not None else 0.0,
+                                            S.ctypes.data, ks.ctypes.data, costs.ctypes.data,
+                                            stages.ctypes.data, ctypes.byref(cells), ctypes.byref(splits))
     if rc == 2:
         raise ValueError("bad arguments")
     out = []

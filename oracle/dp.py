@@ -97,16 +97,42 @@ def combine(Lc: Cell, Rc: Cell, Sp: int, s: int):
     return total, T1, T3, tstar, kstar
 
 
-class TemplateDP:
-    """Memoized T(S', u, v, a) over one profile (fwd/bwd: [L][M] nested sequences)."""
+def stage_allowed(u, v, d, pow2_tp=False, stage_bytes=None, mem_cap=None):
+    """Variants the paper is silent on (DESIGN reading R31): a stage of
+    layers [u, v) on d GPUs of one node is allowed only if d is a power of two (pow2_tp:
+    tensor-parallel degrees 1, 2, 4, 8, ...) and its memory fits: the stage's per-layer
+    bytes (model states + activations) split over its d GPUs (in-stage sharding),
+    sum_{l=u}^{v-1} stage_bytes[l] / d <= mem_cap — summed left to right in binary64, the
+    division last (the paper models memory only through n0: reading R14 is the
+    default, no mask)."""
+    if pow2_tp and (d & (d - 1)) != 0:
+        return False
+    if stage_bytes is not None and mem_cap is not None:
+        tot = 0.0
+        for k in range(u, v):
+            tot = tot + float(stage_bytes[k])
+        if tot / float(d) > mem_cap:
+            return False
+    return True
 
-    def __init__(self, fwd, bwd, M: int, memo: bool = True):
+
+class TemplateDP:
+    """Memoized T(S', u, v, a) over one profile (fwd/bwd: [L][M] nested sequences).
+    Optional stage masks (reading R31): pow2_tp, stage_bytes + mem_cap — a masked-out stage
+    is infinite like one spanning nodes, and a sub-problem without any allowed
+    division is infinite (None)."""
+
+    def __init__(self, fwd, bwd, M: int, memo: bool = True, pow2_tp: bool = False, stage_bytes=None,
+                 mem_cap=None):
         self.fwd = [list(map(float, row)) for row in fwd]
         self.bwd = [list(map(float, row)) for row in bwd]
         self.L = len(self.fwd)
         self.M = M
         self.memo = {} if memo else None
         self.calls = 0
+        self.pow2_tp = pow2_tp
+        self.stage_bytes = None if stage_bytes is None else [float(x) for x in stage_bytes]
+        self.mem_cap = mem_cap
 
     def T(self, Sp: int, u: int, v: int, a):
         key = (Sp, u, v, a)
@@ -120,8 +146,11 @@ class TemplateDP:
                 res = None                            # GPUs across nodes -> infinite
             else:
                 d = M if kind == "W" else n
-                t = stage_time(self.fwd, self.bwd, u, v, d)
-                res = Cell(t, t, t, 0, None)          # Eq.4
+                if not stage_allowed(u, v, d, self.pow2_tp, self.stage_bytes, self.mem_cap):
+                    res = None                        # masked stage (reading R31)
+                else:
+                    t = stage_time(self.fwd, self.bwd, u, v, d)
+                    res = Cell(t, t, t, 0, None)      # Eq.4
         else:
             best = None
             best_total = INF
@@ -146,7 +175,8 @@ class TemplateDP:
 
     # ------------------------------------------------------------ templates
     def template(self, n: int):
-        """Pipeline template for n nodes: argmin over S in n..min(L, n*M)."""
+        """Pipeline template for n nodes: argmin over S in n..min(L, n*M) (P:454-459);
+        None when every S is infinite (only possible with stage masks)."""
         if n > self.L:
             raise ValueError("too few layers for node count")
         best = None
@@ -158,6 +188,8 @@ class TemplateDP:
             if best is None or tot < best[0]:
                 best = (tot, S, c)
         if best is None:
+            if self.pow2_tp or self.mem_cap is not None:
+                return None
             raise ValueError("no feasible template")
         tot, S, c = best
         stages = []
@@ -198,10 +230,11 @@ def node_sizes(N: int, f: int, n0: int, L: int | None = None):
     return list(range(n0, hi + 1))
 
 
-def template_set(fwd, bwd, M, sizes):
-    """All templates of a node specification from one shared memo."""
+def template_set(fwd, bwd, M, sizes, **masks):
+    """All templates of a node specification from one shared memo; `masks`:
+    TemplateDP's stage masks (reading R31), an infeasible size gives None."""
     sys.setrecursionlimit(max(10000, sys.getrecursionlimit()))
-    dp = TemplateDP(fwd, bwd, M)
+    dp = TemplateDP(fwd, bwd, M, **masks)
     # P:473: running the largest template first fills the caches for all others
     out = {}
     for n in sorted(sizes, reverse=True):

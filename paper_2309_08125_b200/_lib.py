@@ -42,7 +42,8 @@ class OobPlanOpts(ctypes.Structure):
     _fields_ = [("nodes", c_int32), ("gpus_per_node", c_int32), ("f", c_int32), ("n0", c_int32),
                 ("gpu_mem_bytes", c_int64), ("util", c_double), ("samples_per_gpu", c_int32),
                 ("device", c_int32), ("stream", c_void_p), ("workspace", c_void_p),
-                ("workspace_bytes", c_size_t), ("comm", c_void_p), ("world", c_int32), ("rank", c_int32)]
+                ("workspace_bytes", c_size_t), ("comm", c_void_p), ("world", c_int32), ("rank", c_int32),
+                ("tp_pow2", c_int32), ("stage_mem_bytes", c_double)]
 
 
 class OobDpInfo(ctypes.Structure):
@@ -97,6 +98,7 @@ _proto("oob_dp_plan_free", None, [c_void_p])
 _proto("oob_dp_plan_info", ctypes.c_int, [c_void_p, P(OobDpInfo)])
 _proto("oob_dp_run", ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p])
 _proto("oob_dp_set_timing", ctypes.c_int, [c_void_p, c_int32])
+_proto("oob_dp_set_stage_masks", ctypes.c_int, [c_void_p, c_int32, c_void_p, c_double])
 _proto("oob_dp_kernel_time", ctypes.c_int, [c_void_p, P(c_double), P(c_int64), c_int32])
 _proto("oob_template_set_from_packed", ctypes.c_int, [c_void_p, P(OobDpInfo), P(c_void_p)])
 _proto("oob_nccl_unique_id", ctypes.c_int, [c_void_p])
@@ -136,7 +138,7 @@ EXPORTED = [
     "oob_template_set_from_packed", "oob_instantiate", "oob_count_sets", "oob_distribute_batch",
     "oob_recommend_batch", "oob_nccl_unique_id", "oob_nccl_comm_create", "oob_nccl_comm_destroy",
     "oob_dp_set_comm", "oob_nccl_allgather", "oob_dp_set_virtual_shards", "oob_dp_run_virtual",
-    "oob_instantiate_all", "oob_exec_create", "oob_exec_free", "oob_exec_num_pipelines", "oob_exec_pipeline", "oob_exec_fail",
+    "oob_instantiate_all", "oob_dp_set_stage_masks", "oob_exec_create", "oob_exec_free", "oob_exec_num_pipelines", "oob_exec_pipeline", "oob_exec_fail",
     "oob_exec_num_actions", "oob_exec_action", "oob_exec_num_transfers", "oob_exec_transfer", "oob_exec_sync_group",
 ]
 NCCL_ID_BYTES = 128

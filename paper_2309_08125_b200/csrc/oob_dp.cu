@@ -47,9 +47,13 @@ __global__ void k_base(DevGeom g, const double *__restrict__ fwd, const double *
     if (g.off[l * g.A + a] < 0) return;
     const double *F = fwd + (size_t)p * g.L * g.M;
     const double *B = bwd + (size_t)p * g.L * g.M;
+    const int64_t c = (int64_t)p * g.C + d_cell(g, 1, u, l, a);
+    if (g.masked && !d_stage_allowed(g, p, u, u + l, d)) {   // masked stage (reading R31)
+        d_store_inf(g, c, 1);
+        return;
+    }
     double s = 0.0;
     for (int k = u; k < u + l; ++k) s = __dadd_rn(s, __dadd_rn(F[k * g.M + d - 1], B[k * g.M + d - 1]));
-    const int64_t c = (int64_t)p * g.C + d_cell(g, 1, u, l, a);
     d_store(g, c, s, s, s, 2.0);    // T1 = T3 = t* = t; C1 = 3*1 - 1 + k*(=0)
     g.ARG[c] = 0xFFFFFFFFu;
 }
@@ -102,6 +106,7 @@ __global__ void k_wave_v1(DevGeom g, int l) {
             }
         }
     }
+    if (bl1 == 0) { d_store_inf(g, pc + d_cell(g, Sp, u, l, a), Sp); return; }   // no finite split (masks)
     d_write_winner(g, pc, Sp, u, l, a, bl1, bj, bs);
 }
 
@@ -158,6 +163,21 @@ __global__ void k_extract(DevGeom g, unsigned char *packed, size_t tpl_bytes, Pi
         if (ob < best || (ob == best && os < bestS)) { best = ob; bestS = os; }
     }
     int status = s_err ? 2 : 0;       // 2: pipeline wait timed out (OOB_E_CUDA on the host)
+    if (!(best < __longlong_as_double(0x7ff0000000000000LL))) {
+        // every S infinite: no allowed mapping under the stage masks (reading R31) —
+        // an infeasible template (status 3, S = 0)
+        if (lane == 0) {
+            const double inf = __longlong_as_double(0x7ff0000000000000LL);
+            h->nodes = n; h->S = 0; h->kstar = 0; h->status = status ? status : 3;
+            h->T1 = h->T2 = h->T3 = h->tstar = h->iter = inf;
+            h->pad = 0.0;
+        }
+        for (int i = lane; i < L; i += 32) {
+            int32_t *r = st + 5 * i;
+            r[0] = r[1] = r[2] = r[3] = r[4] = -1;
+        }
+        return;
+    }
     if (lane == 0) {
         const Cell4 c = d_load(g.CELL + pc + d_cell(g, bestS, 0, L, aW));
         h->nodes = n; h->S = bestS; h->kstar = (int)d_kd(c.C1, bestS);
@@ -355,6 +375,9 @@ struct oob_dp_plan {
     std::vector<WaveHost> waves;         // [L+1]
     size_t max_smem = 0;
     int timing = 0;
+    int mask_pow2 = 0;                   // stage masks (oob_dp_set_stage_masks, reading R31)
+    const double *mask_sb = nullptr;     // device [P][L] stage bytes (borrowed)
+    double mask_cap = 0.0;
     std::vector<cudaEvent_t> ev;
     int ev_used = 0;
     double acc_ms = 0.0;
@@ -762,6 +785,16 @@ extern "C" oob_status oob_dp_set_comm(oob_dp_plan *pl, void *comm, int32_t world
     return OOB_OK;
 }
 
+extern "C" oob_status oob_dp_set_stage_masks(oob_dp_plan *pl, int32_t pow2_tp, const double *d_stage_bytes,
+                                             double mem_cap_bytes) {
+    if (!pl) return fail(OOB_E_INVALID, "oob_dp_set_stage_masks: NULL plan");
+    if (d_stage_bytes && !(mem_cap_bytes > 0.0)) return fail(OOB_E_INVALID, "oob_dp_set_stage_masks: cap must be > 0");
+    pl->mask_pow2 = pow2_tp ? 1 : 0;
+    pl->mask_sb = d_stage_bytes;
+    pl->mask_cap = mem_cap_bytes;
+    return OOB_OK;
+}
+
 extern "C" oob_status oob_dp_set_timing(oob_dp_plan *pl, int32_t enable) {
     if (!pl) return fail(OOB_E_INVALID, "oob_dp_set_timing: NULL plan");
     pl->timing = enable ? 1 : 0;
@@ -881,6 +914,10 @@ static oob_status run_ranks(oob_dp_plan *pl, const double *d_fwd, const double *
         dg.CELL = (Cell4 *)(R.ws + pl->off_CELL);
         dg.SH = (float4 *)(R.ws + pl->off_SH);
         dg.ARG = (uint32_t *)(R.ws + pl->off_ARG);
+        dg.pow2 = pl->mask_pow2;
+        dg.SB = pl->mask_sb;
+        dg.mem_cap = pl->mask_cap;
+        dg.masked = (pl->mask_pow2 || pl->mask_sb) ? 1 : 0;
         R.gacc = (ulonglong2 *)(R.ws + pl->off_GACC);
         R.ctr = (int *)(R.ws + pl->off_CTR);
         R.pp.cnt = R.ctr + pl->pipe_cnt_off;

@@ -31,6 +31,11 @@ struct DevGeom {
     Cell4 *CELL;              // [P*C]
     float4 *SH;               // [P*C] shadow lower bounds (filter only)
     uint32_t *ARG;            // [P*C]
+    // stage masks (DESIGN reading R31; masked = 0: none, every valid cell is finite)
+    int masked;               // 1: some cells may be infinite (written by d_store_inf)
+    int pow2;                 // a stage's GPU count must be a power of two
+    const double *SB;         // [P][L] per-layer stage bytes (NULL: no memory mask)
+    double mem_cap;           // sum_{l in stage} SB[l] / d <= mem_cap
 };
 
 __device__ __forceinline__ bool d_is_whole(const DevGeom &g, int a) { return a >= g.M - 1; }
@@ -85,6 +90,29 @@ __device__ __forceinline__ void d_store(const DevGeom &g, int64_t c, double T1, 
     reinterpret_cast<double2 *>(g.CELL + c)[0] = make_double2(T1, T3);
     reinterpret_cast<double2 *>(g.CELL + c)[1] = make_double2(TS, C1);
     g.SH[c] = d_shadow(T1, T3, TS, C1);
+}
+// Infinite cell (stage masks: no allowed stage / division): +inf values and shadow, so every
+// split using it is +inf (never passes the filter, never enters an accumulator).
+constexpr uint32_t ARG_INF = 0xFFFFFFFCu;
+__device__ __forceinline__ void d_store_inf(const DevGeom &g, int64_t c, int Sp) {
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    reinterpret_cast<double2 *>(g.CELL + c)[0] = make_double2(inf, inf);
+    reinterpret_cast<double2 *>(g.CELL + c)[1] = make_double2(inf, (double)(3 * Sp - 1));
+    const float finf = __int_as_float(0x7f800000);
+    g.SH[c] = make_float4(finf, finf, finf, finf);
+    g.ARG[c] = ARG_INF;
+}
+// Reading R31: the stage [u, v) of profile p on d GPUs of one node is allowed iff d is a
+// power of two (pow2) and sum_{l=u}^{v-1} SB[l] / d <= mem_cap (summed left to right).
+__device__ __forceinline__ bool d_stage_allowed(const DevGeom &g, int p, int u, int v, int d) {
+    if (g.pow2 && (d & (d - 1)) != 0) return false;
+    if (g.SB) {
+        const double *sb = g.SB + (size_t)p * g.L;
+        double tot = 0.0;
+        for (int k = u; k < v; ++k) tot = __dadd_rn(tot, sb[k]);
+        if (__ddiv_rn(tot, (double)d) > g.mem_cap) return false;
+    }
+    return true;
 }
 // Poison cell c (no valid split found / corrupt key): NaN value, never passes the filter.
 __device__ __forceinline__ void d_poison(const DevGeom &g, int64_t c, uint32_t code) {

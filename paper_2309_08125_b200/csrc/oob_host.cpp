@@ -290,6 +290,13 @@ extern "C" oob_status oob_template_set_from_packed(const void *h_packed, const o
             const size_t t = (size_t)pr * p + i;
             const PackedHeader *h = (const PackedHeader *)(base + t * info->packed_template_bytes);
             const int32_t *st = (const int32_t *)(h + 1);
+            if (h->status == 3 && h->S == 0) {   // no allowed mapping (stage masks, reading R31)
+                oob_template &tv = s->templates[t];
+                tv.nodes = h->nodes; tv.num_stages = 0; tv.kstar = 0; tv.reserved = 0;
+                tv.t1_ms = h->T1; tv.t2_ms = h->T2; tv.t3_ms = h->T3; tv.tstar_ms = h->tstar; tv.iter_ms = h->iter;
+                tv.stages = &s->stages[t * info->L];
+                continue;
+            }
             if (h->S < 1 || h->S > info->L || h->status != 0) {
                 const std::string where = " (profile " + std::to_string(pr) + ", template " + std::to_string(i) + ")";
                 const int code = h->status;
@@ -454,9 +461,11 @@ extern "C" oob_status oob_generate_templates(const oob_profile *const *profiles,
 
     const size_t prof_bytes = sizeof(double) * (size_t)L * M;
     const size_t gather_bytes = (world > 1 && !shard_one) ? (size_t)world * per_rank * info.packed_profile_bytes : 0;
+    const bool masked_mem = opts->stage_mem_bytes > 0.0;
+    const size_t sb_bytes = masked_mem ? align_up_host(sizeof(double) * (size_t)L * plan_P) : 0;
     size_t own_bytes = align_up_host(2 * prof_bytes * plan_P) + align_up_host(std::max<size_t>(
                                                                    info.packed_bytes, (size_t)per_rank * info.packed_profile_bytes)) +
-                       align_up_host(gather_bytes);
+                       align_up_host(gather_bytes) + sb_bytes;
     void *ws = opts->workspace;
     size_t ws_bytes = opts->workspace_bytes;
     void *own = nullptr;
@@ -478,6 +487,21 @@ extern "C" oob_status oob_generate_templates(const oob_profile *const *profiles,
     unsigned char *d_packed = (unsigned char *)d_fwd + align_up_host(2 * prof_bytes * plan_P);
     unsigned char *d_gather = d_packed + align_up_host(std::max<size_t>(info.packed_bytes,
                                                                         (size_t)per_rank * info.packed_profile_bytes));
+    double *d_sb = masked_mem ? (double *)(d_gather + align_up_host(gather_bytes)) : nullptr;
+    std::vector<double> h_sb;
+    if (masked_mem) {   // per-layer stage bytes (reading R31): state + samples_per_gpu x activations
+        const int spg = opts->samples_per_gpu > 0 ? opts->samples_per_gpu : 1;
+        h_sb.resize((size_t)L * plan_P);
+        for (int i = 0; i < plan_P; ++i) {
+            const oob_profile *pf = profiles[count > 0 ? first + i : 0];
+            for (int l = 0; l < L; ++l)
+                h_sb[(size_t)i * L + l] = (double)pf->state_bytes[l] + (double)spg * (double)pf->act_bytes[l];
+        }
+        e = cudaMemcpyAsync(d_sb, h_sb.data(), sizeof(double) * h_sb.size(), cudaMemcpyHostToDevice, stream);
+        if (e != cudaSuccess) return fail(OOB_E_CUDA, std::string("H2D stage bytes: ") + cudaGetErrorString(e));
+    }
+    st = oob_dp_set_stage_masks(plan, opts->tp_pow2, d_sb, masked_mem ? opts->stage_mem_bytes : 0.0);
+    if (st != OOB_OK) return st;
     // H2D of this rank's profile costs (one copy per array per profile; a rank without
     // profiles plans a copy of profile 0 and discards it)
     for (int i = 0; i < plan_P; ++i) {
@@ -488,6 +512,7 @@ extern "C" oob_status oob_generate_templates(const oob_profile *const *profiles,
         if (e != cudaSuccess) return fail(OOB_E_CUDA, std::string("H2D profile: ") + cudaGetErrorString(e));
     }
     st = oob_dp_run(plan, d_fwd, d_bwd, ws, info.workspace_bytes, d_packed, stream);
+    oob_dp_set_stage_masks(plan, 0, nullptr, 0.0);   // the cached plan carries no masks to other calls
     if (st != OOB_OK) return st;
     if (world == 1 || shard_one) {
         std::vector<unsigned char> host(info.packed_bytes);

@@ -145,17 +145,20 @@ extern "C" oob_status oob_distribute_batch(const double *T, int32_t x, int64_t B
 namespace {
 
 // Count of X (sizes n_lo..n_hi, sum x_i n_i = N, sum x_i >= f+1), saturating at INT64_MAX.
-int64_t count_sets(int n_lo, int n_hi, int N, int f) {
+// ok (nullable): ok[i] = 0 excludes the template of size n_lo + i (infeasible under stage masks).
+int64_t count_sets(int n_lo, int n_hi, int N, int f, const char *ok = nullptr) {
     const int C = f + 2;   // pipeline count buckets 0..f+1 (f+1 = "at least f+1")
     std::vector<double> cnt((size_t)(N + 1) * C, 0.0);   // double: counts can exceed 2^64
     cnt[0] = 1.0;
-    for (int n = n_lo; n <= n_hi; ++n)
+    for (int n = n_lo; n <= n_hi; ++n) {
+        if (ok && !ok[n - n_lo]) continue;
         for (int t = n; t <= N; ++t)
             for (int c = 0; c < C; ++c) {
                 const double v = cnt[(size_t)(t - n) * C + c];
                 if (v == 0.0) continue;
                 cnt[(size_t)t * C + std::min(c + 1, C - 1)] += v;
             }
+    }
     const double r = cnt[(size_t)N * C + (C - 1)];
     return r >= 9.2e18 ? INT64_MAX : (int64_t)r;
 }
@@ -232,7 +235,8 @@ void dfs(InstCtx &c, int i, int rem) {
         return;
     }
     const int n = c.n_lo + i;
-    for (int k = 0; k * n <= rem; ++k) {
+    const int kmax = c.tpl[i].num_stages > 0 ? rem / n : 0;   // infeasible template (masks): never used
+    for (int k = 0; k <= kmax; ++k) {
         c.x[i] = k;
         dfs(c, i - 1, rem - k * n);
         if (c.capped) break;
@@ -258,8 +262,10 @@ std::vector<std::vector<std::vector<int32_t>>> knapsack_candidates_range(const o
                                                                          int kb_per_count) {
     std::vector<int> order(p);
     std::vector<double> over(p), rate(p);
+    std::vector<char> feas(p, 1);
     for (int i = 0; i < p; ++i) {
         order[i] = i;
+        feas[i] = tpl[i].num_stages > 0;
         rate[i] = 1.0 / tpl[i].tstar_ms;
         over[i] = tpl[i].t1_ms + tpl[i].t3_ms - (double)(tpl[i].num_stages - tpl[i].kstar + 1) * tpl[i].tstar_ms;
     }
@@ -280,7 +286,7 @@ std::vector<std::vector<std::vector<int32_t>>> knapsack_candidates_range(const o
         dp[0] = 0.0;
         for (int t = 1; t <= N; ++t)
             for (int i = 0; i < p; ++i) {
-                if (!allowed[i]) continue;
+                if (!allowed[i] || !feas[i]) continue;
                 const int n = n_lo + i;
                 if (n > t) break;
                 for (int c = 0; c < C; ++c) {
@@ -322,9 +328,10 @@ std::vector<std::vector<std::vector<int32_t>>> knapsack_candidates_range(const o
     for (int T = t_lo; T <= N; ++T)
         for (int i = 0; i < p; ++i) {
             const int n = n_lo + i, q = T / n;
+            if (!feas[i]) continue;
             for (int k = 0; k <= 2 && q - k >= 1; ++k) {
                 const int R = T - (q - k) * n;
-                if (R != 0 && (R < n_lo || R >= n_lo + p)) continue;
+                if (R != 0 && (R < n_lo || R >= n_lo + p || !feas[R - n_lo])) continue;
                 if ((q - k) + (R ? 1 : 0) < f + 1) continue;
                 std::vector<int32_t> x(p, 0);
                 x[i] += q - k;
@@ -350,6 +357,7 @@ std::vector<std::vector<std::vector<int32_t>>> knapsack_candidates_range(const o
                 for (int i = 0; i < p; ++i) {
                     const int n = n_lo + i;
                     if (n > t) break;
+                    if (!feas[i]) continue;
                     for (int r = 0; r < KB; ++r) {
                         const E &prev = at(t - n, c - 1, r);
                         if (prev.v == NEG) break;
@@ -397,6 +405,7 @@ double iter_lower_bound(const oob_template *tpl, int p, int n_lo, int Np, int64_
     double lb = std::numeric_limits<double>::infinity();
     for (int j = 0; j < p; ++j) {
         const oob_template &t = tpl[j];
+        if (t.num_stages < 1) continue;          // infeasible template (stage masks)
         const double a = t.t1_ms + t.t3_ms - (double)(t.num_stages - t.kstar + 1) * t.tstar_ms;
         const double v = std::max(a + t.tstar_ms, a + (double)K * t.tstar_ms * (double)(n_lo + j) / (double)Np);
         lb = std::min(lb, v);
@@ -443,7 +452,9 @@ extern "C" oob_status oob_instantiate(const oob_template_set *set, int32_t profi
     c.p = p; c.n_lo = set->n_lo; c.N = N; c.f = f; c.B = B; c.b = b;
     c.max_enum = max_enum > 0 ? max_enum : 1000000;
     c.x.assign(p, 0);
-    const int64_t total = count_sets(set->n_lo, set->n_hi, N, f);
+    std::vector<char> ok(p);
+    for (int i = 0; i < p; ++i) ok[i] = c.tpl[i].num_stages > 0;
+    const int64_t total = count_sets(set->n_lo, set->n_hi, N, f, ok.data());
     if (num_feasible_out) *num_feasible_out = total;
     if (total == 0) return fail(OOB_E_INFEASIBLE, "no feasible pipeline set for this node count");
     if (total <= c.max_enum) {
@@ -488,6 +499,8 @@ extern "C" oob_status oob_instantiate_all(const oob_template_set *set, int32_t p
     const int64_t K = B / b;
     if (max_enum <= 0) max_enum = 1000000;
     const int lo = std::max<int>(n_min, (f + 1) * set->n_lo);
+    std::vector<char> ok(p);
+    for (int i = 0; i < p; ++i) ok[i] = tpl[i].num_stages > 0;
     std::vector<std::vector<std::vector<int32_t>>> cands;
     bool have_cands = false;
     for (int Np = n_min; Np <= n_max; ++Np) {
@@ -498,12 +511,15 @@ extern "C" oob_status oob_instantiate_all(const oob_template_set *set, int32_t p
         ub_out[k] = 0.0;
         exact_out[k] = 0;
         status_out[k] = OOB_OK;
-        if (Np < lo || count_sets(set->n_lo, set->n_hi, Np, f) == 0) { status_out[k] = OOB_E_INFEASIBLE; continue; }
+        if (Np < lo || count_sets(set->n_lo, set->n_hi, Np, f, ok.data()) == 0) {
+            status_out[k] = OOB_E_INFEASIBLE;
+            continue;
+        }
         InstCtx c;
         c.tpl = tpl; c.p = p; c.n_lo = set->n_lo; c.N = Np; c.f = f; c.B = B; c.b = b;
         c.max_enum = max_enum;
         c.x.assign(p, 0);
-        const int64_t total = count_sets(set->n_lo, set->n_hi, Np, f);
+        const int64_t total = count_sets(set->n_lo, set->n_hi, Np, f, ok.data());
         if (total <= max_enum) {
             dfs(c, p - 1, Np);
             exact_out[k] = 1;

@@ -77,6 +77,8 @@ extern "C" oob_status oob_exec_create(const oob_template_set *set, int32_t profi
         oob_template t;
         oob_status st = oob_template_get(set, profile, i, &t);
         if (st != OOB_OK) return st;
+        if (t.num_stages < 1)   // reinstantiation assumes every size n_lo..n_hi has a template
+            return fail(OOB_E_INVALID, "oob_exec_create: the template set has an infeasible size (stage masks)");
         if (i == 0) x->n_lo = t.nodes;
         x->n_hi = t.nodes;
         x->stages.emplace_back(t.stages, t.stages + t.num_stages);

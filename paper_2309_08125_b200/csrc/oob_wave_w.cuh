@@ -593,8 +593,9 @@ __device__ __forceinline__ void fin_w_one(const DevGeom &g, const FinArgs &f, in
     }
     const int64_t pc = (int64_t)p * g.C;
     const int aW = (g.M - 1) + q - 1;
-    if (a.x >= ACC_EMPTY) {   // no split found: impossible for a valid cell; poison it
-        d_poison(g, pc + d_cell(g, Sp, u, l, aW), 0xFFFFFFFEu);
+    if (a.x >= ACC_EMPTY) {   // no finite split: infinite under stage masks, else impossible (poison)
+        if (g.masked) d_store_inf(g, pc + d_cell(g, Sp, u, l, aW), Sp);
+        else d_poison(g, pc + d_cell(g, Sp, u, l, aW), 0xFFFFFFFEu);
         return;
     }
     const uint32_t key = (uint32_t)a.y;
@@ -656,8 +657,9 @@ __device__ __forceinline__ void fin_w_range(const DevGeom &g, const FinArgs &f, 
             sv[j] = 0;
             if (q[j] < 2) continue;
             const int aW = (M - 1) + q[j] - 1;
-            if (a[j].x >= ACC_EMPTY) {       // no split found: impossible for a valid cell; poison it
-                d_poison(g, pc + d_cell(g, Sp[j], u, l, aW), 0xFFFFFFFEu);
+            if (a[j].x >= ACC_EMPTY) {       // no finite split: infinite under masks, else poison
+                if (g.masked) d_store_inf(g, pc + d_cell(g, Sp[j], u, l, aW), Sp[j]);
+                else d_poison(g, pc + d_cell(g, Sp[j], u, l, aW), 0xFFFFFFFEu);
                 continue;
             }
             const uint32_t key = (uint32_t)a[j].y;
@@ -766,7 +768,7 @@ __device__ __forceinline__ void fin_seed_one(const DevGeom &g, const FinArgs &f,
 #pragma unroll
             for (int side = 0; side < 2; ++side) {
                 const uint32_t arg = args[side];
-                if (arg >= 0xFFFFFFFEu) continue;
+                if (arg >= ARG_INF) continue;
                 const int l1p = (int)(arg & 1023u) + 1 + 2 * side, j = (int)((arg >> 10) & 1023u) + 1;
                 const int s = (int)(arg >> 20);
                 const int jr = q - j, sr = Sp - s;
@@ -867,9 +869,11 @@ __device__ __forceinline__ void fin_small_block(const DevGeom &g, const FinArgs 
         const uint32_t ok = __shfl_down_sync(0xFFFFFFFFu, bkey, d, wd);
         if (ob < best || (ob == best && ok < bkey)) { best = ob; bkey = ok; }
     }
-    if (tl == 0 && active)
-        d_write_winner(g, (int64_t)p * g.C, Sp, u, l, a, (int)(bkey >> 20), (int)((bkey >> 10) & 1023u),
-                       (int)(bkey & 1023u));
+    if (tl == 0 && active) {
+        if (bkey == 0xFFFFFFFFu) d_store_inf(g, (int64_t)p * g.C + d_cell(g, Sp, u, l, a), Sp);   // masks
+        else d_write_winner(g, (int64_t)p * g.C, Sp, u, l, a, (int)(bkey >> 20), (int)((bkey >> 10) & 1023u),
+                            (int)(bkey & 1023u));
+    }
 }
 
 // Small cells of wave f.ls, one WARP per (profile, range) (f.small_range; M <= 8): lane i
@@ -959,7 +963,8 @@ __device__ __forceinline__ void fin_small_range(const DevGeom &g, const FinArgs 
                 }
             }
         }
-        if (active)
+        if (active && bkey == 0xFFFFFFFFu) d_store_inf(g, pc + d_cell(g, Sp, u, l, a), Sp);   // masks
+        else if (active)
             d_write_winner(g, pc, Sp, u, l, a, (int)(bkey >> 20), (int)((bkey >> 10) & 1023u), (int)(bkey & 1023u));
     }
 }

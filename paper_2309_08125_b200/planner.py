@@ -103,10 +103,12 @@ class TemplateSet:
     def count(self, profile: int = 0) -> int:
         return lib.oob_template_count(self._h, profile)
 
-    def get(self, profile: int, i: int) -> dict:
+    def get(self, profile: int, i: int):
+        """Template i (size n_lo + i) as a dict; None when the size has no allowed mapping
+        (stage masks)."""
         t = OobTemplate()
         check(lib.oob_template_get(self._h, profile, i, ctypes.byref(t)))
-        return _template_dict(t)
+        return _template_dict(t) if t.num_stages > 0 else None
 
     def templates(self, profile: int = 0) -> list[dict]:
         return [self.get(profile, i) for i in range(self.count(profile))]
@@ -120,18 +122,21 @@ class TemplateSet:
 def generate_templates(profiles, nodes: int, gpus_per_node: int, f: int, n0: int = 0,
                        gpu_mem_bytes: int = 0, util: float = 0.8, samples_per_gpu: int = 1,
                        device: int = -1, stream: int = 0, workspace: int = 0,
-                       workspace_bytes: int = 0, comm: "NcclComm | None" = None) -> TemplateSet:
+                       workspace_bytes: int = 0, comm: "NcclComm | None" = None, tp_pow2: bool = False,
+                       stage_mem_bytes: float = 0.0) -> TemplateSet:
     """oob_generate_templates: host profiles in, template set out (H2D + GPU DP + D2H).
     With `comm` (an NcclComm of world > 1, every rank passing the same profiles): one
     profile is sharded per wavefront across the ranks, a batch of profiles in contiguous
-    blocks with one all-gather; every rank gets the whole set."""
+    blocks with one all-gather; every rank gets the whole set.  tp_pow2 / stage_mem_bytes:
+    the stage masks of reading R31 (infeasible sizes come back as None)."""
     profs = [p if isinstance(p, Profile) else Profile.from_arrays(*p) for p in profiles]
     arr = (ctypes.c_void_p * len(profs))(*[p._h for p in profs])
     opts = OobPlanOpts(nodes=nodes, gpus_per_node=gpus_per_node, f=f, n0=n0,
                        gpu_mem_bytes=gpu_mem_bytes, util=util, samples_per_gpu=samples_per_gpu,
                        device=device, stream=stream or None, workspace=workspace or None,
                        workspace_bytes=workspace_bytes, comm=comm.handle if comm is not None else None,
-                       world=comm.world if comm is not None else 1, rank=comm.rank if comm is not None else 0)
+                       world=comm.world if comm is not None else 1, rank=comm.rank if comm is not None else 0,
+                       tp_pow2=1 if tp_pow2 else 0, stage_mem_bytes=stage_mem_bytes)
     h = ctypes.c_void_p()
     check(lib.oob_generate_templates(arr, len(profs), ctypes.byref(opts), ctypes.byref(h)))
     ts = TemplateSet(h)

@@ -369,3 +369,52 @@ def test_single_profile_sharding_two_gpus(planner):
         p.join(timeout=300)
     res = sorted(q.get() for _ in range(2))
     assert res == [(0, True), (1, True)]
+
+
+def test_stage_masks_vs_oracle(planner):
+    """Stage masks (reading R31: power-of-two GPU counts per stage, per-stage memory
+    sum_l state_bytes / d <= cap): GPU == C oracle on random shapes, including sizes with no
+    allowed mapping (None), through oob_generate_templates' tp_pow2 / stage_mem_bytes."""
+    rng = random.Random(909)
+    feasible_seen = infeasible_seen = 0
+    for i in range(60):
+        L = rng.choice([3, 5, 8, 12, 16, 24])
+        M = rng.choice([2, 3, 4, 6, 8])
+        prof = random_profile(9100 + i, L, M, rng.choice(["lognormal", "integer", "uniform"]))
+        state = np.array([rng.randint(1, 50) for _ in range(L)], dtype=np.int64)
+        pow2 = rng.random() < 0.6
+        cap = float(state.max()) * rng.uniform(1.0, max(1.5, L / 2)) if rng.random() < 0.7 else 0.0
+        n0 = rng.randint(1, max(1, min(L, 3)))
+        f = rng.randint(0, 2)
+        N = (f + 1) * n0 + rng.randint(0, L)
+        n_hi = min(N - f * n0, L)
+        hp = planner.Profile.from_arrays(prof.fwd_ms, prof.bwd_ms, state)
+        ts = planner.generate_templates([hp], nodes=N, gpus_per_node=M, f=f, n0=n0, device=0, tp_pow2=pow2,
+                                        stage_mem_bytes=cap)
+        want, _ = coracle.template_set(prof.fwd_ms, prof.bwd_ms, M, n0, n_hi, pow2_tp=pow2,
+                                       stage_bytes=state.astype(np.float64) if cap > 0 else None,
+                                       mem_cap=cap if cap > 0 else None)
+        got = ts.templates(0)
+        assert len(got) == len(want)
+        for g, w in zip(got, want):
+            if w is None:
+                assert g is None, (i, L, M)
+                infeasible_seen += 1
+                continue
+            _assert_same([g], [w], f"masks case {i}")
+            feasible_seen += 1
+    assert feasible_seen > 50 and infeasible_seen > 0
+
+
+def test_stage_masks_cfg4_pow2(planner):
+    """The north-star shape with power-of-two TP: the smallest templates vs the oracle (they
+    touch few cells) and every template's stages use 1, 2, 4 or 8 GPUs."""
+    cfg = CONFIGS["cfg4"]
+    prof = config_profiles(cfg, "real")[0]
+    ts = planner.generate_templates([(prof.fwd_ms, prof.bwd_ms)], nodes=cfg.N, gpus_per_node=cfg.M, f=cfg.f,
+                                    n0=cfg.n0, device=0, tp_pow2=True)
+    got = ts.templates(0)
+    for t in got:
+        assert all(d in (1, 2, 4, 8) for (_, _, d, _, _) in t["stages"])
+    want, _ = coracle.template_set(prof.fwd_ms, prof.bwd_ms, cfg.M, cfg.n0, cfg.n0 + 2, pow2_tp=True)
+    _assert_same(got[:3], want, "cfg4 pow2 small templates")

@@ -302,3 +302,68 @@ def test_node_split_order_smaller_j_wins():
     t = _both_oracles(fwd, bwd, 2, 3)
     assert t["total"] == 51.0
     assert t["stages"] == first
+
+
+# ------------------------------------------------------------------ stage masks (reading R31)
+from oracle.dp import stage_allowed  # noqa: E402
+
+
+def test_pow2_mask_hand_example():
+    """pow2_tp: with M = 3 a single stage on the whole node would use 3 GPUs (not a power of
+    two), so the 1-node template must split into stages of (1, 2) or (2, 1) GPUs.  L = 2,
+    F+B per layer: 1 GPU -> 4, 2 GPUs -> 2, 3 GPUs -> 1.
+      unmasked: S=1 on 3 GPUs, t = 2: total 4*2 = 8 (vs S=2 splits >= 10);
+      masked:   (I(1), I(2)): times (4, 2): T1 = 6, k* = 0, T2 = 5*4 = 20, T3 = 6 -> 32;
+                (I(2), I(1)): times (2, 4): T1 = 6, k* = 1, T2 = 6*4 = 24, T3 = 4 -> 34."""
+    fwd, bwd = _cd_profile([[4, 2, 1], [4, 2, 1]])
+    free = TemplateDP(fwd, bwd, 3).template(1)
+    assert (free["S"], free["total"]) == (1, 8.0)
+    t = TemplateDP(fwd, bwd, 3, pow2_tp=True).template(1)
+    assert (t["S"], t["total"]) == (2, 32.0)
+    assert t["stages"] == [(0, 1, 1, 0, 0), (1, 2, 2, 0, 1)]
+    c, _ = coracle.template_set(fwd, bwd, 3, 1, 1, pow2_tp=True)
+    assert c[0] == t
+
+
+def test_memory_mask_hand_example():
+    """Stage memory (sum of the stage's layer bytes / d <= cap): L = 4 layers of 10 bytes,
+    M = 1, n = 2, cap = 25: a 3-layer stage (30) does not fit, so only the 2+2 split is
+    allowed although 1+3 / 3+1 exist; cap = 15 leaves no feasible 2-node template (None)."""
+    fwd, bwd = _cd_profile([[1], [1], [1], [1]])
+    sb = [10.0] * 4
+    t = TemplateDP(fwd, bwd, 1, stage_bytes=sb, mem_cap=25.0).template(2)
+    assert [s[:2] for s in t["stages"]] == [(0, 2), (2, 4)]
+    assert TemplateDP(fwd, bwd, 1, stage_bytes=sb, mem_cap=15.0).template(2) is None
+    assert stage_allowed(0, 3, 1, stage_bytes=sb, mem_cap=25.0) is False
+    assert stage_allowed(0, 3, 2, stage_bytes=sb, mem_cap=25.0) is True
+
+
+def test_masks_vs_brute_force_and_c_oracle():
+    """With stage masks the recursion stays a heuristic over the allowed mappings: DP total
+    >= brute force over allowed mappings, equal for S <= 2 templates, never a disallowed
+    stage; the C oracle equals the Python oracle."""
+    rng = random.Random(31)
+    checked = 0
+    for i in range(80):
+        L, M = rng.randint(2, 6), rng.choice([2, 3, 4])
+        n = rng.randint(1, min(3, L))
+        p = random_profile(4400 + i, L, M, rng.choice(["integer", "uniform"]))
+        sb = [float(rng.randint(1, 9)) for _ in range(L)]
+        masks = rng.choice([{"pow2_tp": True}, {"stage_bytes": sb, "mem_cap": float(rng.randint(6, 30))},
+                            {"pow2_tp": True, "stage_bytes": sb, "mem_cap": float(rng.randint(6, 30))}])
+        ok = lambda u, v, d: stage_allowed(u, v, d, masks.get("pow2_tp", False), masks.get("stage_bytes"),
+                                           masks.get("mem_cap"))
+        t = TemplateDP(p.fwd_ms, p.bwd_ms, M, **masks).template(n)
+        best, _ = brute_force(p.fwd_ms, p.bwd_ms, M, n, allowed=ok)
+        c, _ = coracle.template_set(p.fwd_ms, p.bwd_ms, M, n, n, **masks)
+        assert c[0] == t
+        if t is None:
+            assert best == float("inf")
+            continue
+        assert all(ok(u, v, d) for (u, v, d, _, _) in t["stages"])
+        assert t["total"] >= best - 1e-9 * best
+        if t["S"] <= 2:
+            b2, _ = brute_force(p.fwd_ms, p.bwd_ms, M, n, S_only=t["S"], allowed=ok)
+            assert t["total"] <= b2 * (1 + 1e-12)
+        checked += 1
+    assert checked > 40
