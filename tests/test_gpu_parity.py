@@ -418,3 +418,24 @@ def test_stage_masks_cfg4_pow2(planner):
         assert all(d in (1, 2, 4, 8) for (_, _, d, _, _) in t["stages"])
     want, _ = coracle.template_set(prof.fwd_ms, prof.bwd_ms, cfg.M, cfg.n0, cfg.n0 + 2, pow2_tp=True)
     _assert_same(got[:3], want, "cfg4 pow2 small templates")
+
+
+def test_profiler_to_templates(planner, tmp_path):
+    """Real profile ingestion: the B200 layer profiler writes the SPEC
+    profile JSON, oob_load_profile reads it back exactly, per-layer costs fall with
+    the tensor-parallel degree for a large block, and the measured profile plans on the GPU
+    bit-identically to the oracle."""
+    from paper_2309_08125_b200 import profiler
+    doc = profiler.profile_gpt(hidden=2048, heads=16, layers=6, seq=1024, microbatch=2, gpus_per_node=4,
+                               reps=5, busbw_gbps=600.0)
+    path = str(tmp_path / "prof.json")
+    profiler.write_profile(doc, path)
+    prof = planner.load_profile(path)
+    f, b, st = prof.costs()
+    for l, ly in enumerate(doc["layers"]):
+        assert [f[l, d - 1] for d in range(1, 5)] == [ly["fwd_ms"][str(d)] for d in range(1, 5)]
+        assert st[l] == ly["state_bytes"]
+    assert f[1, 0] > f[1, 1] > f[1, 3] > 0 and b[1, 0] > b[1, 3] > 0
+    ts = planner.generate_templates([prof], nodes=5, gpus_per_node=4, f=1, n0=1, device=0)
+    want, _ = coracle.template_set(f, b, 4, 1, 4)
+    _assert_same(ts.templates(0), want, "measured profile")
