@@ -287,7 +287,7 @@ oob_status oob_instantiate(const oob_template_set *set, int32_t profile, int32_t
  * set) or OOB_E_BATCH (B not distributable).  Above max_enumerated the knapsack candidates
  * of every N' (one set of DPs over 0..n_max) are scored exactly in decreasing order of their
  * own relaxation bound until none can beat the best; the bound of N' is
- * B / min_j max(a_j + t*_j, a_j + K t*_j n_j / N') with a_j = T1 + T3 - (S - k* + 1) t*
+ * B / min_j max(T1_j + T3_j, a_j + K t*_j n_j / N') with a_j = T1 + T3 - (S - k* + 1) t*
  * (DESIGN.md §8).  Caller-owned outputs of (n_max - n_min + 1) entries.  Errors:
  * OOB_E_INVALID. */
 oob_status oob_instantiate_all(const oob_template_set *set, int32_t profile, int32_t n_min,

@@ -82,7 +82,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
         nlib = os.path.join(NCCL, "lib")
         _run([NVCC, "-shared", "-o", LIB] + objs + ["-cudart", "static", "-gencode", "arch=compute_100a,code=sm_100a",
-                                                     "-L", nlib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + nlib], log)
+                                                     "-L", nlib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + nlib, "-lpthread"], log)
     if verbose:
         print("\n".join(x for x in log if x.strip()))
     return LIB

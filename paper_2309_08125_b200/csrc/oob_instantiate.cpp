@@ -1,9 +1,13 @@
 // Pipeline instantiation (Eq.5, PAPER §4.2.1) and batch distribution (Eq.6,
 // §4.2.2) on the host, over a template set produced by the CUDA DP.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <thread>
 #include <cstdint>
 #include <limits>
+#include <string>
+#include <unordered_set>
 #include <vector>
 
 #include "oob_internal.h"
@@ -178,6 +182,8 @@ struct InstCtx {
     int64_t best_pipes = 0;
 };
 
+double plan_iter_lower_bound(const oob_template *tpl, int p, const std::vector<int32_t> &x, int64_t K);
+
 void evaluate(InstCtx &c) {
     int64_t pipes = 0;
     for (int i = 0; i < c.p; ++i) pipes += c.x[i];
@@ -186,6 +192,12 @@ void evaluate(InstCtx &c) {
     const int64_t K = c.B / c.b;
     if (c.B % c.b != 0 || K < pipes) {
         c.min_pipes_fail = std::min<int64_t>(c.min_pipes_fail, pipes);
+        return;
+    }
+    // bound first: no distribution of K microbatches over X beats B / (water level); skip
+    // X when even that cannot reach the best throughput found (exact: ties are kept)
+    if (c.best_thr > 0 && (double)c.B / plan_iter_lower_bound(c.tpl, c.p, c.x, K) < c.best_thr * (1.0 - 1e-12)) {
+        c.distributable++;
         return;
     }
     c.T.clear();
@@ -275,9 +287,10 @@ std::vector<std::vector<std::vector<int32_t>>> knapsack_candidates_range(const o
     std::vector<int32_t> from;
     const int nT = N - t_lo + 1;
     std::vector<std::vector<std::vector<int32_t>>> outs((size_t)std::max(0, nT));
+    std::vector<std::unordered_set<std::string>> seen((size_t)std::max(0, nT));   // dedupe per target
     auto push = [&](int T, const std::vector<int32_t> &x) {
-        auto &out = outs[(size_t)(T - t_lo)];
-        if (std::find(out.begin(), out.end(), x) == out.end()) out.push_back(x);
+        std::string key(reinterpret_cast<const char *>(x.data()), x.size() * sizeof(int32_t));
+        if (seen[(size_t)(T - t_lo)].insert(std::move(key)).second) outs[(size_t)(T - t_lo)].push_back(x);
     };
     // knapsack over the allowed templates with C count buckets (saturating or exact)
     auto run = [&](const std::vector<char> &allowed, int C, bool saturate) {
@@ -400,21 +413,23 @@ std::vector<std::vector<int32_t>> knapsack_candidates(const oob_template *tpl, i
 // Lower bound of the iteration time (max_i T1 + (N_b,i - S + k* - 1) t* + T3 = a_i + N_b,i t_i)
 // of ANY plan on exactly Np nodes distributing K microbatches (N_b,i >= 1): for tau = its
 // iteration time, K = sum N_b,i <= sum_i (tau - a_i) / t_i <= Np max_{i in X} (tau - a_i) / (t_i n_i),
-// and tau >= a_i + t_i for every used i; so tau >= min_j max(a_j + t_j, a_j + K t_j n_j / Np).
+// and tau >= T1_i + T3_i for every used i (the steady phase is never negative, R30); so
+// tau >= min_j max(T1_j + T3_j, a_j + K t_j n_j / Np).
 double iter_lower_bound(const oob_template *tpl, int p, int n_lo, int Np, int64_t K) {
     double lb = std::numeric_limits<double>::infinity();
     for (int j = 0; j < p; ++j) {
         const oob_template &t = tpl[j];
         if (t.num_stages < 1) continue;          // infeasible template (stage masks)
         const double a = t.t1_ms + t.t3_ms - (double)(t.num_stages - t.kstar + 1) * t.tstar_ms;
-        const double v = std::max(a + t.tstar_ms, a + (double)K * t.tstar_ms * (double)(n_lo + j) / (double)Np);
+        const double v = std::max(t.t1_ms + t.t3_ms, a + (double)K * t.tstar_ms * (double)(n_lo + j) / (double)Np);
         lb = std::min(lb, v);
     }
     return lb;
 }
 
 // Lower bound of the iteration time of plan x (any distribution, N_b,i >= 1 real): the
-// water level tau with sum_i (tau - a_i) / t_i = K, and at least max_i (a_i + t_i).
+// water level tau with sum_i (tau - a_i) / t_i = K, and at least max_i (T1_i + T3_i) (the
+// clamped steady phase, R30, keeps every pipeline at or above its fill + drain).
 double plan_iter_lower_bound(const oob_template *tpl, int p, const std::vector<int32_t> &x, int64_t K) {
     double R = 0.0, A = 0.0, floor_ = -std::numeric_limits<double>::infinity();
     for (int i = 0; i < p; ++i) {
@@ -423,7 +438,7 @@ double plan_iter_lower_bound(const oob_template *tpl, int p, const std::vector<i
         const double a = t.t1_ms + t.t3_ms - (double)(t.num_stages - t.kstar + 1) * t.tstar_ms;
         R += (double)x[i] / t.tstar_ms;
         A += (double)x[i] * a / t.tstar_ms;
-        floor_ = std::max(floor_, a + t.tstar_ms);
+        floor_ = std::max(floor_, t.t1_ms + t.t3_ms);
     }
     return std::max(floor_, ((double)K + A) / R);
 }
@@ -501,9 +516,16 @@ extern "C" oob_status oob_instantiate_all(const oob_template_set *set, int32_t p
     const int lo = std::max<int>(n_min, (f + 1) * set->n_lo);
     std::vector<char> ok(p);
     for (int i = 0; i < p; ++i) ok[i] = tpl[i].num_stages > 0;
+    // candidates of every capped N' from one set of knapsack DPs (only when some N' needs them)
     std::vector<std::vector<std::vector<int32_t>>> cands;
-    bool have_cands = false;
-    for (int Np = n_min; Np <= n_max; ++Np) {
+    const int c_lo = std::max(lo, n_min);
+    for (int Np = c_lo; Np <= n_max; ++Np)
+        if (count_sets(set->n_lo, set->n_hi, Np, f, ok.data()) > max_enum) {
+            cands = knapsack_candidates_range(tpl, p, set->n_lo, c_lo, n_max, f, K, 4);
+            break;
+        }
+    // the node counts are independent: host threads over N' (each its own context)
+    auto solve = [&](int Np) {
         const int k = Np - n_min;
         int32_t *cnt = counts_out + (size_t)k * p;
         std::fill(cnt, cnt + p, 0);
@@ -511,24 +533,20 @@ extern "C" oob_status oob_instantiate_all(const oob_template_set *set, int32_t p
         ub_out[k] = 0.0;
         exact_out[k] = 0;
         status_out[k] = OOB_OK;
-        if (Np < lo || count_sets(set->n_lo, set->n_hi, Np, f, ok.data()) == 0) {
+        const int64_t total = Np < lo ? 0 : count_sets(set->n_lo, set->n_hi, Np, f, ok.data());
+        if (total == 0) {
             status_out[k] = OOB_E_INFEASIBLE;
-            continue;
+            return;
         }
         InstCtx c;
         c.tpl = tpl; c.p = p; c.n_lo = set->n_lo; c.N = Np; c.f = f; c.B = B; c.b = b;
         c.max_enum = max_enum;
         c.x.assign(p, 0);
-        const int64_t total = count_sets(set->n_lo, set->n_hi, Np, f, ok.data());
         if (total <= max_enum) {
             dfs(c, p - 1, Np);
             exact_out[k] = 1;
         } else {
-            if (!have_cands) {
-                cands = knapsack_candidates_range(tpl, p, set->n_lo, std::max(lo, n_min), n_max, f, K, 1);
-                have_cands = true;
-            }
-            auto list = cands[(size_t)(Np - std::max(lo, n_min))];
+            const auto &list = cands[(size_t)(Np - c_lo)];
             std::vector<std::pair<double, size_t>> order;
             for (size_t i = 0; i < list.size(); ++i)
                 order.emplace_back(plan_iter_lower_bound(tpl, p, list[i], K), i);
@@ -540,10 +558,18 @@ extern "C" oob_status oob_instantiate_all(const oob_template_set *set, int32_t p
                 evaluate(c);
             }
         }
-        if (c.best_thr < 0) { status_out[k] = OOB_E_BATCH; continue; }
+        if (c.best_thr < 0) { status_out[k] = OOB_E_BATCH; return; }
         for (int i = 0; i < p; ++i) cnt[i] = c.best_x[i];
         thr_out[k] = c.best_thr;
         ub_out[k] = exact_out[k] ? c.best_thr : std::max(c.best_thr, (double)B / iter_lower_bound(tpl, p, set->n_lo, Np, K));
-    }
+    };
+    const int nthr = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), n_max - n_min + 1));
+    std::atomic<int> next(n_min);
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nthr; ++t)
+        pool.emplace_back([&]() {
+            for (int Np; (Np = next.fetch_add(1)) <= n_max;) solve(Np);
+        });
+    for (auto &th : pool) th.join();
     return OOB_OK;
 }

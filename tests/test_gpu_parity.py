@@ -439,3 +439,59 @@ def test_profiler_to_templates(planner, tmp_path):
     ts = planner.generate_templates([prof], nodes=5, gpus_per_node=4, f=1, n0=1, device=0)
     want, _ = coracle.template_set(f, b, 4, 1, 4)
     _assert_same(ts.templates(0), want, "measured profile")
+
+
+def _comm_worker(rank, world, port, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        from paper_2309_08125_b200 import planner as pl
+        comm = pl.NcclComm(world, rank, rank)
+        ok = True
+        # one profile, wavefronts sharded (every wave: OOB_DP_SHARDMIN=0)
+        os.environ["OOB_DP_SHARDMIN"] = "0"
+        cfg = CONFIGS["cfg3"]
+        prof = config_profiles(cfg, "real")[0]
+        ts = pl.generate_templates([(prof.fwd_ms, prof.bwd_ms)], nodes=cfg.N, gpus_per_node=cfg.M, f=cfg.f,
+                                   n0=cfg.n0, device=rank, comm=comm)
+        want, _ = coracle.template_set(prof.fwd_ms, prof.bwd_ms, cfg.M, cfg.n0, cfg.n_max)
+        ok = ok and ts.templates(0) == want
+        del os.environ["OOB_DP_SHARDMIN"]
+        # a batch of 5 profiles in contiguous blocks + one all-gather (every rank: all 5)
+        cfg = CONFIGS["cfg5"]
+        profs = config_profiles(cfg, "real", count=5)
+        ts = pl.generate_templates([(p.fwd_ms, p.bwd_ms) for p in profs], nodes=cfg.N, gpus_per_node=cfg.M,
+                                   f=cfg.f, n0=cfg.n0, device=rank, comm=comm)
+        for i, p in enumerate(profs):
+            want, _ = coracle.template_set(p.fwd_ms, p.bwd_ms, cfg.M, cfg.n0, cfg.n_max)
+            ok = ok and ts.templates(i) == want
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_generate_templates_with_communicator_two_gpus(planner):
+    """oob_generate_templates with opts.comm (the headline API's multi-GPU path): one
+    profile sharded per wavefront, and a batch split in blocks + NCCL all-gather; every
+    rank receives the oracle's whole template set (needs >= 2 GPUs)."""
+    import socket
+    import torch
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = [ctx.Process(target=_comm_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=600)
+    res = sorted(q.get() for _ in range(2))
+    assert res == [(0, True), (1, True)]
