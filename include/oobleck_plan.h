@@ -186,7 +186,7 @@ typedef struct {
     int32_t num_sms;                /* SMs of the device the plan was built for */
     int32_t world;                  /* ranks sharing the wavefronts (oob_dp_set_comm) */
     int32_t warp_waves;             /* batched wavefronts run one warp per (profile, range) */
-    int32_t small_range;            /* in-node cells one warp per (profile, range) */
+    int32_t small_range;            /* wavefronts whose in-node cells run one warp per (profile, range) */
     int32_t reserved;
 } oob_dp_info;
 

@@ -287,6 +287,8 @@ struct Knobs {
     long long spin_max = 1ll << 24;        // OOB_DP_PIPE_SPIN: polls before a pipeline wait times out
     int fin_wait = 1;          // OOB_DP_FINWAIT=0: merged CTAs exit, the range's last one finalizes alone
     int small_range = 1;       // OOB_DP_SMALLRANGE=0: in-node cells thread(s) per cell instead of warp per range
+    double slot_frac = 1.0;    // OOB_DP_SLOTFRAC: share of the resident CTA slots one wave's grid fills
+    int slot_frac_lmax = 1 << 30;   // OOB_DP_SLOTFRAC_LMAX: ... for waves l <= this only
     int warp_units = 96;       // OOB_DP_WARPMAX: batched waves with <= this many units per range run one
                                // warp per (profile, range) (0: never)
     int debug = 0;             // OOB_DP_DEBUG: per-wave plan on stderr
@@ -310,6 +312,8 @@ Knobs read_knobs() {
     if (const char *v = env("OOB_DP_FINWAIT")) k.fin_wait = std::atoi(v) != 0;
     if (const char *v = env("OOB_DP_WARPMAX")) k.warp_units = std::max(0, std::atoi(v));
     if (const char *v = env("OOB_DP_SMALLRANGE")) k.small_range = std::max(0, std::min(2, std::atoi(v)));
+    if (const char *v = env("OOB_DP_SLOTFRAC")) k.slot_frac = std::max(0.05, std::min(1.0, std::atof(v)));
+    if (const char *v = env("OOB_DP_SLOTFRAC_LMAX")) k.slot_frac_lmax = std::atoi(v);
     if (env("OOB_DP_DEBUG")) k.debug = 1;
     return k;
 }
@@ -490,14 +494,17 @@ static int small_tpc(const Geometry &g, int l, int per) {
 // in-node cells one warp per (profile, range) (fin_small_range): batched sweeps with M <= 8,
 // unless OOB_DP_SMALLRANGE=0 (a single profile has too few ranges: one warp walking all
 // layer splits of a range sits on the pipelined critical path, cfg4 +16%; =2 forces it)
-static bool small_range_on(const oob_dp_plan *pl) {
-    return pl->g.M <= 8 && (pl->kn.small_range == 2 || (pl->kn.small_range == 1 && pl->P > 1));
+static bool small_range_on(const oob_dp_plan *pl, int l) {
+    // enough (profile, range) pairs for every resident warp slot to get >= 2 of them
+    const int64_t pairs = (int64_t)pl->P * (pl->g.L - l + 1);
+    const int64_t warp_slots = (int64_t)CTAS_PER_SM * pl->num_sms * (NTW / 32);
+    return pl->g.M <= 8 && (pl->kn.small_range == 2 || (pl->kn.small_range == 1 && pairs >= 2 * warp_slots));
 }
 
 // blocks of 256 threads computing the in-node cells of wave l (all profiles)
 static int64_t small_blocks(const oob_dp_plan *pl, int l) {
     const Geometry &g = pl->g;
-    if (small_range_on(pl)) return ((int64_t)pl->P * (g.L - l + 1) + NTW / 32 - 1) / (NTW / 32);
+    if (small_range_on(pl, l)) return ((int64_t)pl->P * (g.L - l + 1) + NTW / 32 - 1) / (NTW / 32);
     const int tpc = small_tpc(g, l, pl->kn.small_pairs);
     const int64_t ns = (int64_t)pl->P * (g.L - l + 1) * small_cells(g, l);
     return (ns + (256 / tpc) - 1) / (256 / tpc);
@@ -546,7 +553,8 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
         int per_sm = CTAS_PER_SM;
         for (int pass = 0; pass < 2; ++pass) {
             for (int CH = pl->kn.chunk_max;; CH /= 2) {
-                build_wave(pl, l, per_sm * SMS, wh, CH);
+                const double frac = l <= pl->kn.slot_frac_lmax ? pl->kn.slot_frac : 1.0;
+                build_wave(pl, l, std::max(1, (int)(per_sm * SMS * frac)), wh, CH);
                 if (CH <= 12 || ((int64_t)wh.nunits * num_profiles * (L - l + 1) >= 4LL * per_sm * SMS * (NTW / 32) &&
                                  wh.nunits >= pl->kn.units_per_cta * wh.cpr))
                     break;
@@ -557,7 +565,9 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
             per_sm = ps;
         }
         // batched sweeps: short waves (few units per range) one warp per (profile, range)
-        if (num_profiles > 1 && pl->kn.fuse_fin && wh.nunits <= pl->kn.warp_units) {
+        // ... when there are enough (profile, range) pairs for >= 2 per resident warp slot
+        if (num_profiles > 1 && pl->kn.fuse_fin && wh.nunits <= pl->kn.warp_units &&
+            (int64_t)num_profiles * (L - l + 1) >= 2LL * CTAS_PER_SM * SMS * (NTW / 32)) {
             WaveHost ww = wh;
             ww.warp = true;
             build_wave(pl, l, per_sm * SMS, ww, pl->kn.chunk_max);
@@ -766,7 +776,8 @@ extern "C" oob_status oob_dp_plan_info(const oob_dp_plan *pl, oob_dp_info *out) 
     out->world = pl->world;
     out->warp_waves = 0;
     for (int l = 2; l <= g.L; ++l) out->warp_waves += pl->waves[l].warp ? 1 : 0;
-    out->small_range = small_range_on(pl) ? 1 : 0;
+    out->small_range = 0;
+    for (int l = 2; l <= g.L; ++l) out->small_range += small_range_on(pl, l) ? 1 : 0;   // waves
     out->reserved = 0;
     return OOB_OK;
 }
@@ -863,7 +874,7 @@ static FinArgs make_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglong2 *ga
     f.ls = ls;
     f.nsmall = ls ? small_cells(G, ls) : 0;
     f.tpc = ls ? small_tpc(G, ls, pl->kn.small_pairs) : 32;
-    f.small_range = small_range_on(pl) ? 1 : 0;
+    f.small_range = (ls && small_range_on(pl, ls)) ? 1 : 0;
     *nbsmall = (ls && f.nsmall > 0) ? small_blocks(pl, ls) : 0;
     return f;
 }

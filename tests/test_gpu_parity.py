@@ -72,21 +72,25 @@ def test_random_small_vs_oracle(planner):
 
 @pytest.mark.parametrize("warpmax", ["default", "0", "100000"])
 def test_batched_warp_mode_vs_oracle(planner, warpmax, monkeypatch):
-    """Batched sweeps run their short waves one warp per (profile, range) (OOB_DP_WARPMAX:
-    0 = never, large = every wave that fits); every setting gives the oracle's sets."""
+    """Batched sweeps run their short waves one warp per (profile, range) and their in-node
+    cells one warp per (profile, range) (OOB_DP_WARPMAX: 0 = never, large = every wave
+    that fits); every setting gives the oracle's sets.  160 profiles: enough ranges for the
+    warp modes; 6 of them are checked."""
     cfg = CONFIGS["cfg5"]
-    base = planner.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, 6).info
+    P = 160
+    base = planner.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, P).info
     if warpmax != "default":
         monkeypatch.setenv("OOB_DP_WARPMAX", warpmax)
-    info = planner.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, 6).info
-    assert base.warp_waves > 0 and base.small_range == 1
+    info = planner.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, P).info
+    assert base.warp_waves > 0 and base.small_range > 0
     if warpmax == "0":
         assert info.warp_waves == 0
     if warpmax == "100000":
-        assert info.warp_waves > base.warp_waves
-    profs = config_profiles(cfg, "real", count=6)
+        assert info.warp_waves >= base.warp_waves
+    profs = config_profiles(cfg, "real", count=P)
     ts = _gpu_set(planner, profs, (cfg.L, cfg.M, cfg.N, cfg.f, cfg.n0))
-    for i, p in enumerate(profs):
+    for i in (0, 1, 57, 101, 158, 159):
+        p = profs[i]
         want, _ = coracle.template_set(p.fwd_ms, p.bwd_ms, cfg.M, cfg.n0, cfg.n_max)
         _assert_same(ts.templates(i), want, f"cfg5 profile {i} WARPMAX={warpmax}")
 
@@ -222,7 +226,7 @@ VARIANTS = [
     ({"OOB_DP_PIPE": "0", "OOB_DP_SEEDINIT": "0"}, {"pipelined": 0, "seeded": 0}),
     ({"OOB_DP_CHMAX": "24"}, {"chunk_max": 24}),               # short units: many per range, long queues
     ({"OOB_DP_REFRESH": "0"}, {"refresh": 0}),                 # no per-unit filter refresh
-    ({"OOB_DP_SMALLRANGE": "2"}, {"small_range": 1}),          # in-node cells one warp per range (forced)
+    ({"OOB_DP_SMALLRANGE": "0"}, {"small_range": 0}),          # in-node cells thread(s) per cell
     ({"OOB_DP_FINWAIT": "0"}, {}),                             # merged CTAs exit; last one finalizes alone
 ]
 
