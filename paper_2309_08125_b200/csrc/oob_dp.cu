@@ -286,6 +286,7 @@ struct Knobs {
     double shard_min = SHARD_MIN_SPLITS;   // OOB_DP_SHARDMIN: waves with fewer splits run redundantly
     long long spin_max = 1ll << 24;        // OOB_DP_PIPE_SPIN: polls before a pipeline wait times out
     int fin_wait = 1;          // OOB_DP_FINWAIT=0: merged CTAs exit, the range's last one finalizes alone
+    int shard_x = 1;           // OOB_DP_SHARDX=nccl: per-wave ncclAllGather + k_fin instead of peer stores
     int small_range = 1;       // OOB_DP_SMALLRANGE=0: in-node cells thread(s) per cell instead of warp per range
     double slot_frac = 1.0;    // OOB_DP_SLOTFRAC: share of the resident CTA slots one wave's grid fills
     int slot_frac_lmax = 1 << 30;   // OOB_DP_SLOTFRAC_LMAX: ... for waves l <= this only
@@ -310,6 +311,7 @@ Knobs read_knobs() {
     if (const char *v = env("OOB_DP_SHARDMIN")) k.shard_min = std::atof(v);
     if (const char *v = env("OOB_DP_PIPE_SPIN")) k.spin_max = std::max(0ll, std::atoll(v));
     if (const char *v = env("OOB_DP_FINWAIT")) k.fin_wait = std::atoi(v) != 0;
+    if (const char *v = env("OOB_DP_SHARDX")) k.shard_x = std::string(v) == "nccl" ? 0 : 1;
     if (const char *v = env("OOB_DP_WARPMAX")) k.warp_units = std::max(0, std::atoi(v));
     if (const char *v = env("OOB_DP_SMALLRANGE")) k.small_range = std::max(0, std::min(2, std::atoi(v)));
     if (const char *v = env("OOB_DP_SLOTFRAC")) k.slot_frac = std::max(0.05, std::min(1.0, std::atof(v)));
@@ -370,6 +372,15 @@ struct oob_dp_plan {
     int64_t gacc_n = 0;
     void *comm = nullptr;                // ncclComm_t (single-profile sharding), world > 1
     int rank = 0, world = 1;
+    // fused exchange over peer memory (sharded waves; default with a communicator):
+    // plan-owned exchange buffer XB = [3 parities][world][gacc_n] partial argmins + [ctr_n]
+    // epoch-based "ranks published" counters, IPC-mapped into every rank
+    bool xpeer = false;
+    void *xb = nullptr;                  // this rank's exchange buffer (cudaMalloc)
+    int xb_dev = -1;
+    std::vector<void *> xb_peer;         // [world] every rank's buffer in this process (own = xb)
+    size_t xb_off_done = 0, xb_bytes = 0;
+    unsigned epoch = 0;                  // runs so far (peer counters are never reset)
     size_t off_GPART = 0;                // [world][wave partial] gathered partial accumulators
     size_t ws_bytes_base = 0;
     size_t ctr_n = 0;
@@ -516,7 +527,7 @@ static int64_t small_blocks(const oob_dp_plan *pl, int l) {
 // than slots and gain nothing from the overlap.
 static bool plan_pipe_on(const oob_dp_plan *pl) {
     const Geometry &G = pl->g;
-    bool on = pl->kn.pipe && pl->kernel == 2 && pl->world == 1 && pl->kn.fuse_fin;
+    bool on = pl->kn.pipe && pl->kernel == 2 && (pl->world == 1 || pl->xpeer) && pl->kn.fuse_fin;
     for (int l = 2; l <= G.L && on; ++l)
         on = pl->waves[l].nents > 0 && !pl->waves[l].warp &&
              (int64_t)pl->P * (G.L - l + 1) * pl->waves[l].cpr <= (int64_t)CTAS_PER_SM * pl->num_sms;
@@ -684,6 +695,21 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
     return OOB_OK;
 }
 
+// Peer exchange buffers of a sharded plan (see oob_dp_set_comm).
+static void release_exchange(oob_dp_plan *pl) {
+    if (!pl->xb) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(pl->xb_dev);
+    for (int r = 0; r < (int)pl->xb_peer.size(); ++r)
+        if (r != pl->rank && pl->xb_peer[r]) cudaIpcCloseMemHandle(pl->xb_peer[r]);
+    cudaFree(pl->xb);
+    cudaSetDevice(cur);
+    pl->xb = nullptr;
+    pl->xb_peer.clear();
+    pl->xpeer = false;
+}
+
 extern "C" void oob_dp_plan_free(oob_dp_plan *pl) {
     if (!pl) return;
     for (auto e : pl->ev) cudaEventDestroy(e);
@@ -694,6 +720,7 @@ extern "C" void oob_dp_plan_free(oob_dp_plan *pl) {
             cudaSetDevice(cur);
         }
     }
+    release_exchange(pl);
     delete pl;
 }
 
@@ -746,7 +773,7 @@ static int64_t count_launches(const oob_dp_plan *pl) {
         const bool shard = pl->world > 1 && !wh.warp && (double)G.wave_splits[l] * pl->P >= pl->kn.shard_min;
         const bool has = wh.nents > 0;
         n += has ? 1 : 0;
-        n += (pl->kn.fuse_fin && has && !shard) ? 0 : 1;
+        n += (pl->kn.fuse_fin && has && (!shard || pl->xpeer)) ? 0 : 1;
     }
     return n;
 }
@@ -787,11 +814,46 @@ extern "C" oob_status oob_dp_set_comm(oob_dp_plan *pl, void *comm, int32_t world
         return fail(OOB_E_INVALID, "oob_dp_set_comm: bad argument");
     if (world > 1 && pl->kernel != 2)
         return fail(OOB_E_INVALID, "oob_dp_set_comm: sharding needs the W-kernel path");
+    if (world > OOB_MAX_WORLD) return fail(OOB_E_INVALID, "oob_dp_set_comm: world above OOB_MAX_WORLD");
+    release_exchange(pl);
     pl->comm = world > 1 ? comm : nullptr;
     pl->world = world;
     pl->rank = world > 1 ? rank : 0;
     pl->off_GPART = pl->ws_bytes_base;
     pl->ws_bytes = pl->ws_bytes_base + (world > 1 ? align_up(16 * (size_t)world * pl->gacc_n, 256) : 0);
+    if (world > 1 && pl->kn.shard_x && pl->kn.fuse_fin) {
+        // peer exchange buffer, IPC handles all-gathered over the communicator (collective:
+        // every rank calls oob_dp_set_comm)
+        cudaError_t e;
+        const size_t part = 3 * 16 * (size_t)world * pl->gacc_n;
+        pl->xb_off_done = align_up(part, 256);
+        pl->xb_bytes = pl->xb_off_done + align_up(4 * pl->ctr_n + 4, 256);
+        if ((e = cudaGetDevice(&pl->xb_dev)) != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+        if ((e = cudaMalloc(&pl->xb, pl->xb_bytes)) != cudaSuccess) return cuda_fail(e, "cudaMalloc exchange buffer");
+        if ((e = cudaMemset(pl->xb, 0, pl->xb_bytes)) != cudaSuccess) return cuda_fail(e, "cudaMemset exchange buffer");
+        cudaIpcMemHandle_t h;
+        if ((e = cudaIpcGetMemHandle(&h, pl->xb)) != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+        void *dh = nullptr;
+        if ((e = cudaMalloc(&dh, sizeof(h) * (world + 1))) != cudaSuccess) return cuda_fail(e, "cudaMalloc handles");
+        std::vector<cudaIpcMemHandle_t> all((size_t)world);
+        e = cudaMemcpy(dh, &h, sizeof(h), cudaMemcpyHostToDevice);
+        oob_status st = e == cudaSuccess ? nccl_allgather_bytes(comm, dh, (char *)dh + sizeof(h), sizeof(h),
+                                                                 sizeof(h) * world, world, nullptr)
+                                         : cuda_fail(e, "H2D handle");
+        if (st == OOB_OK) {
+            e = cudaMemcpy(all.data(), (char *)dh + sizeof(h), sizeof(h) * world, cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) st = cuda_fail(e, "D2H handles");
+        }
+        cudaFree(dh);
+        if (st != OOB_OK) { release_exchange(pl); return st; }
+        pl->xb_peer.assign((size_t)world, nullptr);
+        for (int r = 0; r < world; ++r) {
+            if (r == rank) { pl->xb_peer[r] = pl->xb; continue; }
+            e = cudaIpcOpenMemHandle(&pl->xb_peer[r], all[r], cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) { release_exchange(pl); return cuda_fail(e, "cudaIpcOpenMemHandle (peer exchange)"); }
+        }
+        pl->xpeer = true;
+    }
     pl->pipe_on = plan_pipe_on(pl);
     return OOB_OK;
 }
@@ -850,7 +912,7 @@ static unsigned *gfilt_of(const oob_dp_plan *pl, ulonglong2 *gacc, int l) {
 // Finalize arguments for wave lw (0: none) and in-node cells + seeds of wave ls (0: none);
 // *nbsmall receives the blocks of the small-cell part.
 static FinArgs make_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglong2 *gacc, int lw, int ls, bool sharded,
-                        int64_t *nbsmall) {
+                        int64_t *nbsmall, const ulonglong2 *gpart = nullptr) {
     const int lsd = ls;                 // seeds of the same wave as the in-node cells
     const Geometry &G = pl->g;
     FinArgs f;
@@ -863,7 +925,7 @@ static FinArgs make_fin(const oob_dp_plan *pl, const DevGeom &dg, ulonglong2 *ga
     f.GFW = gfilt_of(pl, gacc, lw);
     f.world = sharded ? pl->world : 1;
     f.part_stride = (int64_t)pl->P * f.nranges_w * f.nout_w;   // all-gather: rank r at r x (wave partial)
-    f.GPART = (const ulonglong2 *)((const unsigned char *)dg.CELL - pl->off_CELL + pl->off_GPART);
+    f.GPART = gpart ? gpart : (const ulonglong2 *)((const unsigned char *)dg.CELL - pl->off_CELL + pl->off_GPART);
     // seeds for wave ls (children of length <= ls-2: final before this launch)
     f.lseed = (lsd >= 2 && lsd <= G.L && pl->waves[lsd].seed) ? lsd : 0;
     f.nout_s = f.lseed ? pl->waves[lsd].nout : 0;
@@ -913,6 +975,7 @@ static oob_status run_ranks(oob_dp_plan *pl, const double *d_fwd, const double *
     if (gs != OOB_OK) return gs;
     cudaError_t e;
     const bool pipe_on = pl->pipe_on;
+    if (pl->xpeer) ++pl->epoch;           // peer counters: targets epoch x world (never reset)
     for (int i = 0; i < nr; ++i) {
         RankRun &R = rr[i];
         DevGeom &dg = R.dg;
@@ -975,12 +1038,13 @@ static oob_status run_ranks(oob_dp_plan *pl, const double *d_fwd, const double *
         // shard only wavefronts whose work outweighs the all-gather (~10-20 us on NVLink);
         // short wavefronts run redundantly on every rank (identical results, no exchange)
         const bool shard = pl->world > 1 && !wh.warp && (double)G.wave_splits[l] * pl->P >= pl->kn.shard_min;
+        const bool peer = shard && pl->xpeer;   // fused exchange through peer memory
         const int64_t ctas = wh.nents == 0 ? 0
                              : wh.warp ? ((int64_t)pl->P * (G.L - l + 1) + NTW / 32 - 1) / (NTW / 32)
                                        : (int64_t)pl->P * (G.L - l + 1) * wh.cpr;
         // fused finalize (OOB_DP_FUSE=1): unsharded waves finalize in k_wave_w's last CTAs
         // and run the next wave's in-node cells and seeds in extra blocks
-        const bool fused = pl->kn.fuse_fin && ctas > 0 && !shard;
+        const bool fused = pl->kn.fuse_fin && ctas > 0 && (!shard || peer);
         if (pl->timing && (!pipe_on || l == 2)) cudaEventRecord(pl->ev[pl->ev_used], stream);
         for (int i = 0; i < nr && ctas > 0; ++i) {
             RankRun &R = rr[i];
@@ -1015,10 +1079,20 @@ static oob_status run_ranks(oob_dp_plan *pl, const double *d_fwd, const double *
             w.fin_inline = fused ? 1 : 0;
             w.rdone = R.ctr + wh.done_off;
             w.rclaim = w.rdone + (size_t)pl->P * w.nranges;
+            w.peer = peer ? 1 : 0;
+            w.epoch = pl->epoch;
+            const size_t xpar = (size_t)(l % 3) * 16 * (size_t)pl->world * pl->gacc_n;   // this wave's gather buffer
+            for (int r = 0; r < OOB_MAX_WORLD; ++r) {
+                w.xpart[r] = (peer && r < pl->world) ? (ulonglong2 *)((unsigned char *)pl->xb_peer[r] + xpar) : nullptr;
+                w.xdone[r] = (peer && r < pl->world)
+                                 ? (int *)((unsigned char *)pl->xb_peer[r] + pl->xb_off_done) + wh.done_off
+                                 : nullptr;
+            }
             if (fused) {
                 int64_t nbs = 0, nbw = 0;
                 w.fa = make_fin(pl, R.dg, R.gacc, 0, l < G.L ? l + 1 : 0, false, &nbs);
-                w.fw = make_fin(pl, R.dg, R.gacc, l, 0, false, &nbw);
+                w.fw = make_fin(pl, R.dg, R.gacc, l, 0, peer, &nbw,
+                                peer ? (const ulonglong2 *)((unsigned char *)pl->xb + xpar) : nullptr);
                 aux = w.fa.nbseed + nbs;
             }
             w.pp = R.pp;
@@ -1045,7 +1119,7 @@ static oob_status run_ranks(oob_dp_plan *pl, const double *d_fwd, const double *
             cudaEventRecord(pl->ev[pl->ev_used + 1], stream);
             pl->ev_used += 2;
         }
-        if (shard) {   // all-gather of the wave's partial argmins (every rank finalizes all)
+        if (shard && !peer) {   // all-gather of the wave's partial argmins (every rank finalizes all)
             const size_t bytes = 16 * (size_t)pl->P * (G.L - l + 1) * wh.nout;
             if (pl->comm) {
                 oob_status st = nccl_allgather_bytes(pl->comm, gacc_of(pl, rr[0].gacc, l), rr[0].ws + pl->off_GPART,
@@ -1060,7 +1134,7 @@ static oob_status run_ranks(oob_dp_plan *pl, const double *d_fwd, const double *
                     }
             }
         }
-        for (int i = 0; i < nr && !fused; ++i)
+        for (int i = 0; i < nr && !fused; ++i)   // (peer-exchanged waves finalize inside k_wave_w)
             if ((e = launch_fin(pl, rr[i].dg, rr[i].gacc, l, l < G.L ? l + 1 : 0, stream, shard)) != cudaSuccess)
                 return cuda_fail(e, "k_fin launch");
     }
@@ -1089,6 +1163,7 @@ extern "C" oob_status oob_dp_set_virtual_shards(oob_dp_plan *pl, int32_t world) 
     if (!pl || world < 1 || world > 64) return fail(OOB_E_INVALID, "oob_dp_set_virtual_shards: bad argument");
     if (world > 1 && pl->kernel != 2)
         return fail(OOB_E_INVALID, "oob_dp_set_virtual_shards: sharding needs the W-kernel path");
+    release_exchange(pl);
     pl->comm = nullptr;
     pl->world = world;
     pl->rank = 0;

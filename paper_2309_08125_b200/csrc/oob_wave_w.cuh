@@ -51,6 +51,10 @@ struct Pipe {
     long long spin_max;    // polls before a wait gives up (~200 ns each)
 };
 
+#ifndef OOB_MAX_WORLD
+#define OOB_MAX_WORLD 8
+#endif
+
 // Finalize / in-node work of one wavefront (k_fin, or k_wave_w's extra blocks and last CTAs).
 struct FinArgs {
     int lw, nranges_w, nout_w;     // W finalize of wave lw (lw = 0: none)
@@ -100,6 +104,15 @@ struct WaveW {
                                // per-range work is a few units, a CTA per range idles on its prologue,
                                // barrier and finalize); no pipeline, cpr = 1, no merge
     int prefetch;              // 1: each unit prefetches its tile and chunk cells into L1 (one CTA per range)
+    // fused exchange over NVLink peer memory (single-profile sharding, oob_dp_set_comm):
+    // the range's last local CTA stores the range's partial argmins into every rank's
+    // gather slot of this rank (plain remote stores), fences, and counts itself in every
+    // rank's per-range counter; the finalize waits for all ranks' partials (epoch-based
+    // counters, never reset) and takes the lexicographic minimum over them
+    int peer;                  // 1: this wave exchanges through peer memory
+    unsigned epoch;            // run number (counter targets epoch x world)
+    ulonglong2 *xpart[OOB_MAX_WORLD];   // rank r's gather buffer of this wave (slot of this rank: + rank * part_stride)
+    int *xdone[OOB_MAX_WORLD];          // rank r's per-range "ranks published" counters of this wave
     FinArgs fa, fw;
 };
 
@@ -645,6 +658,10 @@ __device__ __forceinline__ void fin_w_range(const DevGeom &g, const FinArgs &f, 
             if (lo < 2) continue;
             ulonglong2 *ga = f.GACC + (int64_t)pr * nout + i;
             a[j] = sacc ? sacc[i] : __ldcg(ga);
+            for (int r = 0; r < f.world && f.world > 1; ++r) {   // lexicographic min over the ranks' partials
+                const ulonglong2 b = __ldcg(f.GPART + (int64_t)r * f.part_stride + (int64_t)pr * nout + i);
+                if (lex_less(b.x, (uint32_t)b.y, a[j].x, (uint32_t)a[j].y)) a[j] = b;
+            }
             __stcg(ga, make_ulonglong2(ACC_EMPTY, 0xFFFFFFFFull));
             __stcg(f.GFW + (int64_t)pr * nout + i, FILT_EMPTY);
         }
@@ -1341,7 +1358,51 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
             }
         }
     }
-    if (w.fin_inline) {
+    if (w.fin_inline && w.peer) {
+        // Peer exchange: the range's last local CTA publishes the local minima to every rank;
+        // every local CTA of the range then waits for all ranks' partials and claims
+        // finalize shares (fin_w_range takes the minimum over the gathered partials).
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) s_last = atomicAdd(w.rdone + pr, 1) + 1 == w.cpr;
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            for (int r = 0; r < w.world; ++r) {
+                ulonglong2 *dst = w.xpart[r] + (int64_t)w.rank * w.fw.part_stride + ((int64_t)p * w.nranges + u) * nout;
+                for (int i = tid; i < nout; i += NTW) dst[i] = __ldcg(ga + i);   // NVLink store into rank r
+            }
+            __threadfence_system();
+            __syncthreads();
+            if (tid < w.world) atomicAdd(w.xdone[tid] + pr, 1);
+        }
+        if (tid == 0) {
+            const int target = (int)w.epoch * w.world;
+            int ok = 0;
+            for (long long it = 0; it < w.pp.spin_max; ++it) {
+                int v;
+                asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(w.xdone[w.rank] + pr) : "memory");
+                if (v >= target) { ok = 1; break; }
+                if (*(volatile int *)w.pp.err) break;
+                __nanosleep(200);
+            }
+            if (!ok) atomicExch(w.pp.err, 1);   // surfaces as OOB_E_CUDA (k_extract)
+            s_last = ok;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            for (;;) {
+                __syncthreads();
+                if (tid == 0) s_last = atomicAdd(w.rclaim + pr, 1);
+                __syncthreads();
+                const int c = s_last;
+                if (c >= w.cpr) break;
+                fin_w_range<NTW>(g, w.fw, pr, tid, c, w.cpr);
+                pipe_signal(w.pp, L, 2, l);
+            }
+        }
+    } else if (w.fin_inline) {
         // The range's W outputs are final once all its cpr CTAs have merged.  The host sizes
         // the main grid to the resident CTA slots whenever cpr > 1 (the extra blocks come
         // after it), so the range's CTAs are co-resident: each waits for the others, then

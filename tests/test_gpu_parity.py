@@ -324,11 +324,14 @@ def test_virtual_shards_cfg4_golden(planner):
         _assert_same(ts.templates(0), rec["profiles"][0]["templates"], f"cfg4 virtual rank {r}/4")
 
 
-def _shard_worker(rank, world, port, q):
+def _shard_worker(rank, world, port, q, xmode="peer"):
     import os
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if xmode == "nccl":
+        os.environ["OOB_DP_SHARDX"] = "nccl"
+    os.environ["OOB_DP_SHARDMIN"] = "0"          # every wavefront sharded
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
     try:
@@ -339,23 +342,30 @@ def _shard_worker(rank, world, port, q):
         plan = pl.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, 1)
         plan.set_comm(comm)
         info = plan.info
+        assert info.world == world and info.pipelined == (1 if xmode == "peer" else 0)
         fwd = torch.tensor(prof.fwd_ms[None], dtype=torch.float64, device="cuda")
         bwd = torch.tensor(prof.bwd_ms[None], dtype=torch.float64, device="cuda")
         ws = torch.empty(info.workspace_bytes, dtype=torch.uint8, device="cuda")
         packed = torch.zeros(info.packed_bytes, dtype=torch.uint8, device="cuda")
-        plan.run(fwd.data_ptr(), bwd.data_ptr(), ws.data_ptr(), ws.numel(), packed.data_ptr(),
-                 torch.cuda.current_stream().cuda_stream)
-        torch.cuda.synchronize()
-        got = plan.template_set(packed.cpu().numpy()).templates(0)
+        ok = True
         want, _ = coracle.template_set(prof.fwd_ms, prof.bwd_ms, cfg.M, cfg.n0, cfg.n_max)
-        q.put((rank, got == want))
+        for _ in range(3):                    # repeated runs: epoch-based peer counters
+            packed.zero_()
+            plan.run(fwd.data_ptr(), bwd.data_ptr(), ws.data_ptr(), ws.numel(), packed.data_ptr(),
+                     torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            ok = ok and plan.template_set(packed.cpu().numpy()).templates(0) == want
+        q.put((rank, ok))
     finally:
         dist.destroy_process_group()
 
 
-def test_single_profile_sharding_two_gpus(planner):
-    """oob_dp_set_comm: one profile split across 2 GPUs (NCCL all-gather of partial argmins
-    per wavefront) gives the oracle's template set on both ranks (needs >= 2 GPUs)."""
+@pytest.mark.parametrize("xmode", ["peer", "nccl"])
+def test_single_profile_sharding_two_gpus(planner, xmode):
+    """oob_dp_set_comm: one profile split across 2 GPUs, every wavefront sharded — partial
+    argmins exchanged inside k_wave_w through NVLink peer memory (peer, pipelined) or by a
+    per-wavefront ncclAllGather + k_fin (nccl) — gives the oracle's template set on both
+    ranks, run after run (needs >= 2 GPUs)."""
     import socket
     import torch
     import torch.multiprocessing as mp
@@ -366,7 +376,7 @@ def test_single_profile_sharding_two_gpus(planner):
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
-    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q, xmode)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:
