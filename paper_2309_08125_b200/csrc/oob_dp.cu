@@ -265,7 +265,8 @@ using namespace oob;
 namespace {
 
 constexpr int TE_W = 4;                    // k_wave_w register tile: TE cells per lane
-constexpr double SHARD_MIN_SPLITS = 2e7;   // wavefronts sharded across ranks (oob_dp_set_comm)
+constexpr double SHARD_MIN_SPLITS = 2e7;   // wavefronts sharded across ranks (per-wave ncclAllGather)
+constexpr double SHARD_MIN_SPLITS_PEER = 5e6;   // ... with the fused peer exchange (cfg4 4 GPUs: 9.57 -> 9.15 ms)
 constexpr int SEED_MIN_L = 6;              // waves seeded with proportional splits (k_fin)
 constexpr int CTAS_PER_SM = WAVE_CTAS_PER_SM;   // k_wave_w: resident CTAs per SM (register bound; smem may allow fewer)
 
@@ -283,7 +284,8 @@ struct Knobs {
     int chunk_max = 192;       // OOB_DP_CHMAX: streamed cells per unit (upper bound)
     int units_per_cta = 0;     // OOB_DP_UPC: minimum queue units per CTA (chunk size)
     int refresh = 1;           // OOB_DP_REFRESH=0: no per-unit filter refresh
-    double shard_min = SHARD_MIN_SPLITS;   // OOB_DP_SHARDMIN: waves with fewer splits run redundantly
+    double shard_min = -1.0;   // OOB_DP_SHARDMIN: waves with fewer splits run redundantly (default:
+                               // 5e6 with the peer exchange, 2e7 with per-wave ncclAllGather)
     long long spin_max = 1ll << 24;        // OOB_DP_PIPE_SPIN: polls before a pipeline wait times out
     int fin_wait = 1;          // OOB_DP_FINWAIT=0: merged CTAs exit, the range's last one finalizes alone
     int shard_x = 1;           // OOB_DP_SHARDX=nccl: per-wave ncclAllGather + k_fin instead of peer stores
@@ -317,6 +319,7 @@ Knobs read_knobs() {
     if (const char *v = env("OOB_DP_SLOTFRAC")) k.slot_frac = std::max(0.05, std::min(1.0, std::atof(v)));
     if (const char *v = env("OOB_DP_SLOTFRAC_LMAX")) k.slot_frac_lmax = std::atoi(v);
     if (env("OOB_DP_DEBUG")) k.debug = 1;
+    if (k.shard_min < 0) k.shard_min = k.shard_x ? SHARD_MIN_SPLITS_PEER : SHARD_MIN_SPLITS;
     return k;
 }
 
