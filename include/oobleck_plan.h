@@ -215,16 +215,25 @@ oob_status oob_dp_kernel_time(oob_dp_plan *plan, double *ms_out, int64_t *launch
 /* ------------------------------------------------------------------ multi-GPU (one profile)
  * Single-profile sharding across `world` GPUs of one box: every rank calls
  * oob_dp_run on the same profile with the same plan geometry; the W-cell splits of every
- * wavefront are divided across ranks (rank r takes units r, r+world, ... of each range's
- * unit queue) and one ncclAllGather of the per-rank partial argmins per wavefront (16 bytes
- * per output) lets every rank finalize the whole wavefront, so every rank ends with the same
- * table and packed templates (bit-identical to world = 1).
+ * large wavefront are divided across ranks (rank r takes units r, r+world, ... of each
+ * range's unit queue) and the per-rank partial argmins (16 bytes per output) are exchanged
+ * so every rank finalizes the whole wavefront with the same lexicographic minimum: every
+ * rank ends with the same table and packed templates (bit-identical to world = 1).
  *   oob_nccl_unique_id : rank 0 creates the id (OOB_NCCL_ID_BYTES bytes), the caller
  *                        broadcasts it (e.g. torch.distributed);
  *   oob_nccl_comm_create: every rank, on its CUDA device (`device` < 0: current);
  *   oob_dp_set_comm    : attach the communicator to a plan (comm = NULL, world = 1: detach);
  *                        the plan's workspace grows by world x (largest wavefront partial):
  *                        re-read oob_dp_plan_info afterwards.  The communicator is borrowed.
+ *                        Collective (every rank, same order).  By default the partial
+ *                        argmins are exchanged INSIDE the wavefront kernel through NVLink
+ *                        peer memory: the call allocates a plan-owned exchange buffer and
+ *                        maps every rank's (cudaIpc handles all-gathered over `comm`), the
+ *                        wavefronts stay pipelined, and every rank must then run the plan the
+ *                        same number of times (the peer counters are per run; a rank that
+ *                        skips a run makes the others' waits time out -> OOB_E_CUDA).
+ *                        OOB_DP_SHARDX=nccl selects one ncclAllGather + finalize launch per
+ *                        sharded wavefront instead.
  * Errors: OOB_E_INVALID, OOB_E_NCCL, OOB_E_CUDA. */
 #define OOB_NCCL_ID_BYTES 128
 oob_status oob_nccl_unique_id(void *id_out);

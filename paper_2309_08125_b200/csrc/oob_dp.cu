@@ -283,6 +283,7 @@ struct Knobs {
     int small_pairs = 1;       // OOB_DP_SMALLPAIRS: layer splits per thread of an in-node cell
     int chunk_max = 192;       // OOB_DP_CHMAX: streamed cells per unit (upper bound)
     int units_per_cta = 0;     // OOB_DP_UPC: minimum queue units per CTA (chunk size)
+    int units_per_warp = 4;    // OOB_DP_UPW: chunks shrink until every warp slot has this many units
     int refresh = 1;           // OOB_DP_REFRESH=0: no per-unit filter refresh
     double shard_min = -1.0;   // OOB_DP_SHARDMIN: waves with fewer splits run redundantly (default:
                                // 5e6 with the peer exchange, 2e7 with per-wave ncclAllGather)
@@ -309,6 +310,7 @@ Knobs read_knobs() {
     if (const char *v = env("OOB_DP_SMALLPAIRS")) k.small_pairs = std::max(1, std::atoi(v));
     if (const char *v = env("OOB_DP_CHMAX")) k.chunk_max = std::max(12, std::atoi(v));
     if (const char *v = env("OOB_DP_UPC")) k.units_per_cta = std::max(0, std::atoi(v));
+    if (const char *v = env("OOB_DP_UPW")) k.units_per_warp = std::max(1, std::atoi(v));
     if (const char *v = env("OOB_DP_REFRESH")) k.refresh = std::atoi(v) != 0;
     if (const char *v = env("OOB_DP_SHARDMIN")) k.shard_min = std::atof(v);
     if (const char *v = env("OOB_DP_PIPE_SPIN")) k.spin_max = std::max(0ll, std::atoll(v));
@@ -569,7 +571,8 @@ extern "C" oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int
             for (int CH = pl->kn.chunk_max;; CH /= 2) {
                 const double frac = l <= pl->kn.slot_frac_lmax ? pl->kn.slot_frac : 1.0;
                 build_wave(pl, l, std::max(1, (int)(per_sm * SMS * frac)), wh, CH);
-                if (CH <= 12 || ((int64_t)wh.nunits * num_profiles * (L - l + 1) >= 4LL * per_sm * SMS * (NTW / 32) &&
+                if (CH <= 12 || ((int64_t)wh.nunits * num_profiles * (L - l + 1) >=
+                                     (int64_t)pl->kn.units_per_warp * per_sm * SMS * (NTW / 32) &&
                                  wh.nunits >= pl->kn.units_per_cta * wh.cpr))
                     break;
             }
