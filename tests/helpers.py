@@ -33,6 +33,10 @@ def pack_templates(templates_per_profile, L: int, M: int, n_lo: int, n_hi: int):
     for pi, tpls in enumerate(templates_per_profile):
         for i, t in enumerate(tpls):
             o = (pi * p + i) * tpl_bytes
+            if t is None:       # infeasible size (stage masks): S = 0, status 3, costs +inf
+                inf = float("inf")
+                struct.pack_into("<iiiidddddd", buf, o, n_lo + i, 0, 0, 3, inf, inf, inf, inf, inf, 0.0)
+                continue
             struct.pack_into("<iiiidddddd", buf, o, t["nodes"], t["S"], t["kstar"], 0, t["T1"], t["T2"],
                              t["T3"], t["tstar"], t["total"], 0.0)
             for j, s in enumerate(t["stages"]):

@@ -201,3 +201,38 @@ def test_engine_matches_oracle_random_failures():
             _same_state(ex, st)
             compared += 1
     assert compared > 200
+
+
+def test_masked_sets_instantiate_and_exec_rules():
+    """A template set with an infeasible size (stage masks, reading R31): oob_instantiate
+    never uses it (brute force over the feasible sizes agrees), and the reconfiguration
+    state refuses the set (reinstantiation needs every size n_lo..n_hi)."""
+    from paper_2309_08125_b200 import planner
+    from paper_2309_08125_b200._lib import OOB_E_INVALID, OobError
+    from oracle.instantiate import select_plan_brute
+    tpls = _templates(8, 1, 2, 5)
+    holed = [tpls[0], None, tpls[2], tpls[3]]            # size 3 infeasible
+    ts = _cpp_set(holed, 8, 1)
+    assert ts.templates(0)[1] is None
+    from oracle.instantiate import distribute_for_plan, enumerate_sets_brute
+    feas = [t for t in holed if t is not None]
+    for Np in range(4, 12):
+        best = None
+        for X in enumerate_sets_brute([t["nodes"] for t in feas], Np, 1):
+            pipes = [t for t, c in zip(feas, X) for _ in range(c)]
+            try:
+                _, it = distribute_for_plan(pipes, 12, 1)
+            except ValueError:
+                continue
+            key = (-12 / it, sum(X), X)
+            best = key if best is None or key < best else best
+        if best is None:                                  # only size-3 pipelines would fit
+            with pytest.raises(OobError):
+                planner.instantiate(ts, 0, Np, 1, 12, 1)
+            continue
+        got = planner.instantiate(ts, 0, Np, 1, 12, 1)
+        assert got["counts"][1] == 0
+        assert got["throughput"] == pytest.approx(-best[0], rel=1e-12)
+    with pytest.raises(OobError) as e:
+        planner.ExecState(ts, 0, 1, 12, 1, [1, 0, 0, 1], list(range(7)))
+    assert e.value.status == OOB_E_INVALID
