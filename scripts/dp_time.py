@@ -1,4 +1,5 @@
-"""Time the device-resident DP (oob_dp_run) for a config: python scripts/dp_time.py cfg4 [reps] (diagnostic)."""
+"""Time the device-resident DP (oob_dp_run) for a config (diagnostic):
+    python scripts/dp_time.py cfg4 [reps] [profiles]   (3 untimed sets first; cfg5 default 64 profiles)"""
 import os
 import sys
 
@@ -13,7 +14,8 @@ from workloads import CONFIGS, config_profiles  # noqa: E402
 key = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 cfg = CONFIGS[key]
-profs = config_profiles(cfg, "real", count=64 if key == "cfg5" else 1)
+nprof = int(sys.argv[3]) if len(sys.argv) > 3 else (64 if key == "cfg5" else 1)
+profs = config_profiles(cfg, "real", count=nprof)
 plan = planner.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, len(profs))
 info = plan.info
 fwd = torch.tensor(np.stack([p.fwd_ms for p in profs]), dtype=torch.float64, device="cuda")
