@@ -85,6 +85,9 @@ typedef struct {
     int32_t tp_pow2;            /* stage mask: GPU counts per stage powers of two (R31) */
     double stage_mem_bytes;     /* > 0: stage mask sum_l (state_bytes_l + samples_per_gpu *
                                    act_bytes_l) / d <= stage_mem_bytes (R31); 0: none */
+    int32_t exact;              /* 1: return the EXACT optimum of the 1F1B objective per template
+                                   (oob_exact_run, bounded by the recursion's own templates);
+                                   0: the paper's recursion (default).  Not with stage masks. */
 } oob_plan_opts;
 
 /* ------------------------------------------------------------------ errors */
@@ -257,6 +260,34 @@ oob_status oob_dp_set_virtual_shards(oob_dp_plan *plan, int32_t world);
 oob_status oob_dp_run_virtual(oob_dp_plan *plan, const double *d_fwd, const double *d_bwd,
                               void *const *d_workspace, size_t workspace_bytes,
                               void *const *d_packed, void *stream);
+
+/* ------------------------------------------------------------------ exact optimum
+ * The paper's recursion (Eqs.1-4) keeps one argmin per memo cell of the
+ * sub-problem's own objective, which is a heuristic for the parent: it can
+ * miss the minimum of the closed form T1 + (3S - 1 + k*) t* + T3 (P:381-386, P:424-429,
+ * N_b = 4S) over all mappings.  oob_exact_run returns that minimum for every template size
+ * n_lo..n_hi: for each distinct stage time tau (the bottleneck t*), the stages before the
+ * first bottleneck cost t + 4 tau each and those after it 2t + 3 tau, two shortest paths over
+ * (layer boundary, GPUs) solved on the device; the best over tau and bottleneck placements
+ * is the optimum (derivation in csrc/oob_exact.cu).  Ties: smallest total,
+ * then smallest tau, then the first (layer, GPU) placement; stage costs summed left to
+ * right (reading R12).  No stage masks.
+ *   d_fwd, d_bwd   : device float64 [num_profiles][L][M] (as oob_dp_run)
+ *   d_packed_ub    : device packed templates of the same shape (oob_dp_run's output) whose
+ *                    totals bound the search (only tau <= iter / (3n + 1) can win), or NULL
+ *                    for an unbounded search (every stage time; slower)
+ *   d_workspace    : >= oob_exact_workspace_bytes (same shape, current device); its first 8
+ *                    bytes receive the number of (profile, tau) tasks solved (uint64)
+ *   d_packed_out   : packed templates in oob_dp_run's layout (status 0; 3 = no mapping); may
+ *                    be d_packed_ub (each bound is read before any output is written)
+ * Enqueued on `stream`, no synchronisation.  Errors: OOB_E_INVALID (shape: 1 <= n_lo <=
+ * n_hi <= L <= 1023, M <= 64), OOB_E_NOMEM (workspace), OOB_E_CUDA. */
+oob_status oob_exact_workspace_bytes(int32_t L, int32_t M, int32_t n_lo, int32_t n_hi,
+                                     int32_t num_profiles, size_t *bytes);
+oob_status oob_exact_run(int32_t L, int32_t M, int32_t n_lo, int32_t n_hi, int32_t num_profiles,
+                         const double *d_fwd, const double *d_bwd, const void *d_packed_ub,
+                         void *d_workspace, size_t workspace_bytes, void *d_packed_out,
+                         void *stream);
 
 /* Build a template set from a HOST copy of the packed output (d_packed copied back). */
 oob_status oob_template_set_from_packed(const void *h_packed, const oob_dp_info *info,

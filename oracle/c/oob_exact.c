@@ -67,8 +67,11 @@ static void dps(const ctx_t *c, double tau, double *pre, double *suf, int *ppar,
             /* a stage [l0, l) on GPUs [m-d, m) ending here */
             for (int d = 1; d <= M && d <= m && ((m - d) % M) + d <= M; ++d)
                 for (int l0 = l - 1; l0 >= 0; --l0) {
+                    /* sums from different start layers: stop only clearly past tau (an
+                       out-of-order rounding is ~1e-13 relative), skip the rest exactly */
                     const double t = T(c, l0, l, d);
-                    if (!(t <= tau)) break;
+                    if (t > tau * (1.0 + 0x1p-30)) break;
+                    if (!(t <= tau)) continue;
                     const double v = s + (2.0 * t + 3.0 * tau);
                     if (v < suf[l0 * W + m - d]) {
                         suf[l0 * W + m - d] = v;

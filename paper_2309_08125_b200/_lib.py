@@ -43,7 +43,7 @@ class OobPlanOpts(ctypes.Structure):
                 ("gpu_mem_bytes", c_int64), ("util", c_double), ("samples_per_gpu", c_int32),
                 ("device", c_int32), ("stream", c_void_p), ("workspace", c_void_p),
                 ("workspace_bytes", c_size_t), ("comm", c_void_p), ("world", c_int32), ("rank", c_int32),
-                ("tp_pow2", c_int32), ("stage_mem_bytes", c_double)]
+                ("tp_pow2", c_int32), ("stage_mem_bytes", c_double), ("exact", c_int32)]
 
 
 class OobDpInfo(ctypes.Structure):
@@ -128,6 +128,9 @@ _proto("oob_exec_action", ctypes.c_int, [c_void_p, c_int32, P(OobAction)])
 _proto("oob_exec_num_transfers", c_int32, [c_void_p])
 _proto("oob_exec_transfer", ctypes.c_int, [c_void_p, c_int32, P(OobTransfer)])
 _proto("oob_exec_sync_group", ctypes.c_int, [c_void_p, c_int32, c_void_p, c_void_p, c_int32, P(c_int32)])
+_proto("oob_exact_workspace_bytes", ctypes.c_int, [c_int32, c_int32, c_int32, c_int32, c_int32, P(c_size_t)])
+_proto("oob_exact_run", ctypes.c_int, [c_int32, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
+                                       c_void_p, c_size_t, c_void_p, c_void_p])
 
 EXPORTED = [
     "oob_last_error", "oob_status_string", "oob_load_profile", "oob_profile_from_arrays",
@@ -140,6 +143,7 @@ EXPORTED = [
     "oob_dp_set_comm", "oob_nccl_allgather", "oob_dp_set_virtual_shards", "oob_dp_run_virtual",
     "oob_instantiate_all", "oob_dp_set_stage_masks", "oob_exec_create", "oob_exec_free", "oob_exec_num_pipelines", "oob_exec_pipeline", "oob_exec_fail",
     "oob_exec_num_actions", "oob_exec_action", "oob_exec_num_transfers", "oob_exec_transfer", "oob_exec_sync_group",
+    "oob_exact_workspace_bytes", "oob_exact_run",
 ]
 NCCL_ID_BYTES = 128
 

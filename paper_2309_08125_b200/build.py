@@ -32,7 +32,7 @@ def _nccl_dir() -> str:
 
 NCCL = _nccl_dir()
 
-CU_SOURCES = ["oob_dp.cu"]
+CU_SOURCES = ["oob_dp.cu", "oob_exact.cu"]
 CPP_SOURCES = ["oob_host.cpp", "oob_geometry.cpp", "oob_instantiate.cpp", "oob_dist.cpp", "oob_reconfig.cpp"]
 HEADERS = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".h", ".cuh"))] + \
     [os.path.join(INC, "oobleck_plan.h")]

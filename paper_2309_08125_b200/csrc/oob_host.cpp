@@ -304,6 +304,8 @@ extern "C" oob_status oob_template_set_from_packed(const void *h_packed, const o
                 if (code == 2)
                     return fail(OOB_E_CUDA, "wavefront pipeline wait timed out (GPU shared with other work?): "
                                             "the DP table is incomplete" + where);
+                if (code == 4)
+                    return fail(OOB_E_CUDA, "exact solver: bottleneck stage list overflow" + where);
                 return fail(OOB_E_CUDA, "corrupt packed template" + where);
             }
             oob_template &tv = s->templates[t];
@@ -400,6 +402,8 @@ extern "C" oob_status oob_generate_templates(const oob_profile *const *profiles,
     }
     if (opts->gpus_per_node != M)
         return fail(OOB_E_INVALID, "opts.gpus_per_node does not match the profile");
+    if (opts->exact && (opts->tp_pow2 || opts->stage_mem_bytes > 0.0))
+        return fail(OOB_E_INVALID, "opts.exact does not support stage masks");
     int n0 = opts->n0;
     if (n0 <= 0) {
         for (int i = 0; i < num_profiles; ++i) {
@@ -514,6 +518,19 @@ extern "C" oob_status oob_generate_templates(const oob_profile *const *profiles,
     st = oob_dp_run(plan, d_fwd, d_bwd, ws, info.workspace_bytes, d_packed, stream);
     oob_dp_set_stage_masks(plan, 0, nullptr, 0.0);   // the cached plan carries no masks to other calls
     if (st != OOB_OK) return st;
+    // exact optimum (oob_exact_run): the recursion's templates bound the search, the exact
+    // ones overwrite them in place
+    void *ex_ws = nullptr;
+    std::unique_ptr<void, void (*)(void *)> ex_guard(nullptr, [](void *q) { if (q) cudaFree(q); });
+    if (opts->exact) {
+        size_t ex_bytes = 0;
+        if ((st = oob_exact_workspace_bytes(L, M, n_lo, n_hi, plan_P, &ex_bytes)) != OOB_OK) return st;
+        if ((e = cudaMalloc(&ex_ws, ex_bytes)) != cudaSuccess)
+            return fail(OOB_E_NOMEM, std::string("cudaMalloc exact workspace: ") + cudaGetErrorString(e));
+        ex_guard.reset(ex_ws);
+        st = oob_exact_run(L, M, n_lo, n_hi, plan_P, d_fwd, d_bwd, d_packed, ex_ws, ex_bytes, d_packed, stream);
+        if (st != OOB_OK) return st;
+    }
     if (world == 1 || shard_one) {
         std::vector<unsigned char> host(info.packed_bytes);
         e = cudaMemcpyAsync(host.data(), d_packed, info.packed_bytes, cudaMemcpyDeviceToHost, stream);

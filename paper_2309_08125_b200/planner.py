@@ -123,8 +123,10 @@ def generate_templates(profiles, nodes: int, gpus_per_node: int, f: int, n0: int
                        gpu_mem_bytes: int = 0, util: float = 0.8, samples_per_gpu: int = 1,
                        device: int = -1, stream: int = 0, workspace: int = 0,
                        workspace_bytes: int = 0, comm: "NcclComm | None" = None, tp_pow2: bool = False,
-                       stage_mem_bytes: float = 0.0) -> TemplateSet:
+                       stage_mem_bytes: float = 0.0, exact: bool = False) -> TemplateSet:
     """oob_generate_templates: host profiles in, template set out (H2D + GPU DP + D2H).
+    exact=True: the exact optimum of the 1F1B objective per size (oob_exact_run) instead of
+    the paper's recursion.
     With `comm` (an NcclComm of world > 1, every rank passing the same profiles): one
     profile is sharded per wavefront across the ranks, a batch of profiles in contiguous
     blocks with one all-gather; every rank gets the whole set.  tp_pow2 / stage_mem_bytes:
@@ -136,12 +138,27 @@ def generate_templates(profiles, nodes: int, gpus_per_node: int, f: int, n0: int
                        device=device, stream=stream or None, workspace=workspace or None,
                        workspace_bytes=workspace_bytes, comm=comm.handle if comm is not None else None,
                        world=comm.world if comm is not None else 1, rank=comm.rank if comm is not None else 0,
-                       tp_pow2=1 if tp_pow2 else 0, stage_mem_bytes=stage_mem_bytes)
+                       tp_pow2=1 if tp_pow2 else 0, stage_mem_bytes=stage_mem_bytes, exact=1 if exact else 0)
     h = ctypes.c_void_p()
     check(lib.oob_generate_templates(arr, len(profs), ctypes.byref(opts), ctypes.byref(h)))
     ts = TemplateSet(h)
     ts._keep = profs
     return ts
+
+
+def exact_workspace_bytes(L: int, M: int, n_lo: int, n_hi: int, num_profiles: int = 1) -> int:
+    """oob_exact_workspace_bytes for the current device."""
+    b = ctypes.c_size_t(0)
+    check(lib.oob_exact_workspace_bytes(L, M, n_lo, n_hi, num_profiles, ctypes.byref(b)))
+    return b.value
+
+
+def exact_run(L: int, M: int, n_lo: int, n_hi: int, num_profiles: int, d_fwd: int, d_bwd: int, d_packed_ub: int,
+              d_workspace: int, workspace_bytes: int, d_packed_out: int, stream: int = 0) -> None:
+    """oob_exact_run: exact-optimum templates into d_packed_out (oob_dp_run's layout);
+    d_packed_ub = the recursion's packed output (bounds the search) or 0."""
+    check(lib.oob_exact_run(L, M, n_lo, n_hi, num_profiles, d_fwd, d_bwd, d_packed_ub or None, d_workspace,
+                            workspace_bytes, d_packed_out, stream or None))
 
 
 class DPPlan:
