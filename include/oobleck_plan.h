@@ -281,7 +281,7 @@ oob_status oob_dp_run_virtual(oob_dp_plan *plan, const double *d_fwd, const doub
  *   d_packed_out   : packed templates in oob_dp_run's layout (status 0; 3 = no mapping); may
  *                    be d_packed_ub (each bound is read before any output is written)
  * Enqueued on `stream`, no synchronisation.  Errors: OOB_E_INVALID (shape: 1 <= n_lo <=
- * n_hi <= L <= 1023, M <= 64), OOB_E_NOMEM (workspace), OOB_E_CUDA. */
+ * n_hi <= L <= 1023, M <= 64, n_hi * M <= ~21,000), OOB_E_NOMEM (workspace), OOB_E_CUDA. */
 oob_status oob_exact_workspace_bytes(int32_t L, int32_t M, int32_t n_lo, int32_t n_hi,
                                      int32_t num_profiles, size_t *bytes);
 oob_status oob_exact_run(int32_t L, int32_t M, int32_t n_lo, int32_t n_hi, int32_t num_profiles,

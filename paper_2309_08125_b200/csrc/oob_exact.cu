@@ -47,7 +47,9 @@
 namespace {
 
 constexpr int EXT = 256;                            // threads per CTA
-constexpr int EX_CTAS_PER_SM = 2;
+constexpr int EXS = 256;                            // k_ex_solve threads per CTA
+constexpr int EX_CTAS_PER_SM = 6;                  // k_ex_solve (latency bound: many resident tasks)
+constexpr int EX_RECON_PER_SM = 2;
 constexpr double EX_INF = __builtin_huge_val();
 // a stage-time loop whose sums are not built from one start point may see an out-of-order
 // rounding: stop only clearly past tau (rounding of <= 1023 positive terms is ~1e-13 relative)
@@ -58,7 +60,8 @@ struct ExGeom {
     int Gmax, W;        // W = Gmax + 1: row stride of the DP tables
     int E;              // T entries per profile: M (L+1)^2
     int H;              // hash slots per profile
-    int slots;          // persistent CTAs (scratch owners)
+    int slots;          // k_ex_solve persistent CTAs (value scratch owners)
+    int rslots;         // k_ex_recon persistent CTAs (value + parent scratch owners)
     int list_cap;       // bottleneck stage list (shared memory)
     size_t tpl_bytes, prof_bytes;
 };
@@ -158,11 +161,23 @@ __global__ void k_ex_hash(ExGeom g, const double *__restrict__ T, unsigned long 
     }
 }
 
-__global__ void k_ex_window(ExGeom g, const unsigned char *__restrict__ packed_ub, double *tw, double *twmax,
-                            ulonglong2 *acc) {
+__global__ void k_ex_window(ExGeom g, const double *__restrict__ fwd, const double *__restrict__ bwd,
+                            const unsigned char *__restrict__ packed_ub, double *tw, double *twmax, ulonglong2 *acc) {
     const int p = blockIdx.x;
-    __shared__ double s_max;
-    if (threadIdx.x == 0) s_max = 0.0;
+    __shared__ double s_max, s_clb;
+    if (threadIdx.x == 0) {
+        // C_lb <= sum of all stage times of any mapping (every layer runs on some d <= M
+        // GPUs), shrunk by 2^-30 for rounding: total >= (C_lb - tau) + (3n + 1) tau
+        const double *F = fwd + (size_t)p * g.L * g.M, *B = bwd + (size_t)p * g.L * g.M;
+        double c = 0.0;
+        for (int l = 0; l < g.L; ++l) {
+            double m = EX_INF;
+            for (int d = 0; d < g.M; ++d) m = fmin(m, __dadd_rn(F[(size_t)l * g.M + d], B[(size_t)l * g.M + d]));
+            c = __dadd_rn(c, m);
+        }
+        s_clb = __dmul_rn(c, 1.0 - 0x1p-30);
+        s_max = 0.0;
+    }
     __syncthreads();
     for (int i = threadIdx.x; i < g.nsz; i += blockDim.x) {
         const int n = g.n_lo + i;
@@ -170,8 +185,13 @@ __global__ void k_ex_window(ExGeom g, const unsigned char *__restrict__ packed_u
         if (packed_ub) {
             const oob::PackedHeader *h =
                 (const oob::PackedHeader *)(packed_ub + (size_t)p * g.prof_bytes + (size_t)i * g.tpl_bytes);
-            if (h->status == 0 && h->S > 0) w = __dmul_rn(__ddiv_rn(h->iter, __dadd_rn(__dmul_rn(3.0, (double)n), 1.0)),
-                                                          __dadd_rn(1.0, 1e-12));
+            if (h->status == 0 && h->S > 0) {
+                // every stage adds >= 3 tau, the bottleneck 4 tau, S >= n: total >= (3n + 1) tau;
+                // and total >= C_lb + 3n tau (above) — only tau under both bounds can win
+                const double w1 = __ddiv_rn(h->iter, __dadd_rn(__dmul_rn(3.0, (double)n), 1.0));
+                const double w2 = __ddiv_rn(__dadd_rn(h->iter, -s_clb), __dmul_rn(3.0, (double)n));
+                w = __dmul_rn(fmin(w1, w2), __dadd_rn(1.0, 1e-12));
+            }
         }
         tw[(size_t)p * g.nsz + i] = w;
         acc[(size_t)p * g.nsz + i] = make_ulonglong2(~0ull, ~0ull);
@@ -202,9 +222,9 @@ __global__ void k_ex_tasks(ExGeom g, const double *__restrict__ T, const unsigne
 }
 
 // ------------------------------------------------------------------ the two shortest paths
-// Pre over rows l = 0..L and m = 0..G; Suf over rows l = L..0 and r = 0..G (GPUs remaining).
-// PAR: also record the parent (previous boundary << 8 | GPUs) with the oracle's priorities.
-template <bool PAR>
+// Pre over rows l = 0..L and m = 0..G; Suf over rows l = L..0 and r = 0..G (GPUs remaining),
+// one thread per target, recording the parent (previous boundary << 8 | GPUs) with the
+// oracle's priorities on equal values (k_ex_recon).
 __device__ void ex_paths(const ExGeom &g, const double *__restrict__ Tp, int G, double tau, double *pre, double *suf,
                          int *ppar, int *spar) {
     const int L = g.L, M = g.M, W = g.W;
@@ -229,7 +249,7 @@ __device__ void ex_paths(const ExGeom &g, const double *__restrict__ Tp, int G, 
                         const double pv = pre[(size_t)l * W + m - d];
                         if (pv == EX_INF) continue;
                         const double v = __dadd_rn(pv, __dadd_rn(t, t4));
-                        if (v < best || (PAR && v == best && (l < bl || (l == bl && d > bd)))) {
+                        if (v < best || (v == best && (l < bl || (l == bl && d > bd)))) {
                             best = v;
                             bl = l;
                             bd = d;
@@ -238,7 +258,7 @@ __device__ void ex_paths(const ExGeom &g, const double *__restrict__ Tp, int G, 
                 }
             }
             pre[(size_t)l2 * W + m] = best;
-            if (PAR) ppar[(size_t)l2 * W + m] = (bl << 8) | bd;
+            ppar[(size_t)l2 * W + m] = (bl << 8) | bd;
         }
         __syncthreads();
     }
@@ -256,7 +276,7 @@ __device__ void ex_paths(const ExGeom &g, const double *__restrict__ Tp, int G, 
                         const double sv = suf[(size_t)l * W + r - d];
                         if (sv == EX_INF) continue;
                         const double v = __dadd_rn(sv, __dadd_rn(__dmul_rn(2.0, t), t3));
-                        if (v < best || (PAR && v == best && (l > bl || (l == bl && d > bd)))) {
+                        if (v < best || (v == best && (l > bl || (l == bl && d > bd)))) {
                             best = v;
                             bl = l;
                             bd = d;
@@ -265,7 +285,69 @@ __device__ void ex_paths(const ExGeom &g, const double *__restrict__ Tp, int G, 
                 }
             }
             suf[(size_t)l0 * W + r] = best;
-            if (PAR) spar[(size_t)l0 * W + r] = (bl << 8) | bd;
+            spar[(size_t)l0 * W + r] = (bl << 8) | bd;
+        }
+        __syncthreads();
+    }
+}
+
+// Value-only paths (k_ex_solve): the same recurrences as ex_paths, with the (GPU count,
+// stage GPUs) pairs of a row spread over the threads (few GPUs but long stage ranges for
+// large tau) and a shared-memory min per target; equal values need no tie rule here.
+__device__ void ex_paths_fast(const ExGeom &g, const double *__restrict__ Tp, int G, double tau, double *pre,
+                              double *suf, unsigned long long *s_row) {
+    const int L = g.L, M = g.M, W = g.W;
+    const double t4 = __dmul_rn(4.0, tau), t3 = __dmul_rn(3.0, tau), brk = __dmul_rn(tau, EX_BRK);
+    const unsigned long long INFB = 0x7FF0000000000000ull;
+    for (int m = threadIdx.x; m <= G; m += blockDim.x) {
+        pre[m] = m == 0 ? 0.0 : EX_INF;
+        suf[(size_t)L * W + m] = m == 0 ? 0.0 : EX_INF;
+        s_row[m] = INFB;
+    }
+    __syncthreads();
+    const int pairs = G * M;
+    for (int l2 = 1; l2 <= L; ++l2) {
+        for (int i = threadIdx.x; i < pairs; i += blockDim.x) {
+            const int m = i / M + 1, d = i % M + 1;
+            if (d > (m - 1) % M + 1) continue;
+            double best = EX_INF;
+            const double *tc = Tp + t_index(L, d, l2, 0);
+            for (int l = l2 - 1; l >= 0; --l) {
+                const double t = tc[l];
+                if (t >= brk) break;
+                if (!(t < tau)) continue;
+                const double pv = pre[(size_t)l * W + m - d];
+                if (pv == EX_INF) continue;
+                best = fmin(best, __dadd_rn(pv, __dadd_rn(t, t4)));
+            }
+            if (best < EX_INF) atomicMin(s_row + m, (unsigned long long)__double_as_longlong(best));
+        }
+        __syncthreads();
+        for (int m = threadIdx.x; m <= G; m += blockDim.x) {
+            pre[(size_t)l2 * W + m] = __longlong_as_double((long long)s_row[m]);
+            s_row[m] = INFB;
+        }
+        __syncthreads();
+    }
+    for (int l0 = L - 1; l0 >= 0; --l0) {
+        for (int i = threadIdx.x; i < pairs; i += blockDim.x) {
+            const int r = i / M + 1, d = i % M + 1;
+            if (d > (r - 1) % M + 1) continue;
+            double best = EX_INF;
+            for (int l = l0 + 1; l <= L; ++l) {
+                const double t = Tp[t_index(L, d, l, l0)];
+                if (t > brk) break;
+                if (!(t <= tau)) continue;
+                const double sv = suf[(size_t)l * W + r - d];
+                if (sv == EX_INF) continue;
+                best = fmin(best, __dadd_rn(sv, __dadd_rn(__dmul_rn(2.0, t), t3)));
+            }
+            if (best < EX_INF) atomicMin(s_row + r, (unsigned long long)__double_as_longlong(best));
+        }
+        __syncthreads();
+        for (int r = threadIdx.x; r <= G; r += blockDim.x) {
+            suf[(size_t)l0 * W + r] = __longlong_as_double((long long)s_row[r]);
+            s_row[r] = INFB;
         }
         __syncthreads();
     }
@@ -310,9 +392,11 @@ __device__ unsigned long long block_min_u64(unsigned long long v, unsigned long 
     return v;    // valid in warp 0
 }
 
-__global__ void __launch_bounds__(EXT) k_ex_solve(ExGeom g, ExWs w) {
-    extern __shared__ int s_list[];
-    __shared__ unsigned long long s_red[EXT / 32];
+__global__ void __launch_bounds__(EXS, EX_CTAS_PER_SM) k_ex_solve(ExGeom g, ExWs w) {
+    extern __shared__ unsigned long long s_dyn[];
+    unsigned long long *s_row = s_dyn;                       // [Gmax + 1]
+    int *s_list = (int *)(s_dyn + g.W);                      // [list_cap]
+    __shared__ unsigned long long s_red[EXS / 32];
     __shared__ int s_task, s_n;
     double *pre = w.dp + (size_t)blockIdx.x * 2 * (g.L + 1) * g.W;
     double *suf = pre + (size_t)(g.L + 1) * g.W;
@@ -334,7 +418,7 @@ __global__ void __launch_bounds__(EXT) k_ex_solve(ExGeom g, ExWs w) {
         for (int i = g.nsz - 1; i >= 0; --i)
             if (tau <= tw[i]) { nmax = g.n_lo + i; break; }
         const int Gt = nmax * g.M;
-        ex_paths<false>(g, Tp, Gt, tau, pre, suf, nullptr, nullptr);
+        ex_paths_fast(g, Tp, Gt, tau, pre, suf, s_row);
         const int nent = ex_bottlenecks(g, Tp, tau, s_list, &s_n, w.ctr);
         const double t4 = __dmul_rn(4.0, tau);
         const unsigned long long tbits = (unsigned long long)__double_as_longlong(tau);
@@ -390,7 +474,7 @@ __global__ void __launch_bounds__(EXT) k_ex_recon(ExGeom g, ExWs w, unsigned cha
         }
         const double tau = __longlong_as_double((long long)a.y);
         const double t4 = __dmul_rn(4.0, tau);
-        ex_paths<true>(g, Tp, G, tau, pre, suf, ppar, spar);
+        ex_paths(g, Tp, G, tau, pre, suf, ppar, spar);
         // the first placement (a, m, d, b) in the oracle's scan order reaching the optimum
         for (int j = threadIdx.x; j < g.L * g.M; j += blockDim.x) {
             const int A = j / g.M, d = j % g.M + 1;
@@ -474,7 +558,10 @@ bool ex_geom(int L, int M, int n_lo, int n_hi, int P, int sms, ExGeom &g) {
     g.H = 1;
     while (g.H < 2 * valid) g.H <<= 1;
     g.slots = sms * EX_CTAS_PER_SM;
-    g.list_cap = 2 * L * M;
+    g.rslots = sms * EX_RECON_PER_SM;
+    g.list_cap = std::min(2 * L * M, 8192);
+    // k_ex_solve's shared memory: one row of targets + the bottleneck list
+    if (sizeof(unsigned long long) * (size_t)g.W + sizeof(int) * (size_t)g.list_cap > 200 * 1024) return false;
     g.tpl_bytes = oob::packed_template_bytes(L);
     g.prof_bytes = g.tpl_bytes * (size_t)g.nsz;
     return true;
@@ -493,7 +580,7 @@ size_t ex_layout(const ExGeom &g, unsigned char *base, ExWs *w) {
                          align_up_host(sizeof(int2) * (size_t)g.P * valid),
                          align_up_host(sizeof(ulonglong2) * (size_t)g.P * g.nsz),
                          align_up_host(sizeof(double) * (size_t)g.slots * 2 * rows),
-                         align_up_host(sizeof(int) * (size_t)g.slots * 2 * rows)};
+                         align_up_host(sizeof(int) * (size_t)g.rslots * 2 * rows)};
     size_t off[10], tot = 0;
     for (int i = 0; i < 10; ++i) { off[i] = tot; tot += sz[i]; }
     if (w) {
@@ -553,15 +640,15 @@ extern "C" oob_status oob_exact_run(int32_t L, int32_t M, int32_t n_lo, int32_t 
     const int grid = (int)std::min<int64_t>((flat + EXT - 1) / EXT, (int64_t)sms * 16);
     k_ex_times<<<g.P * g.M, 128, 0, s>>>(g, d_fwd, d_bwd, w.T);
     k_ex_hash<<<grid, EXT, 0, s>>>(g, w.T, w.hkey, w.hidx);
-    k_ex_window<<<g.P, 128, 0, s>>>(g, (const unsigned char *)d_packed_ub, w.tw, w.twmax, w.acc);
+    k_ex_window<<<g.P, 128, 0, s>>>(g, d_fwd, d_bwd, (const unsigned char *)d_packed_ub, w.tw, w.twmax, w.acc);
     k_ex_tasks<<<grid, EXT, 0, s>>>(g, w.T, w.hkey, w.hidx, w.twmax, w.tasks, w.ctr);
-    const size_t smem = sizeof(int) * (size_t)g.list_cap;
+    const size_t smem = sizeof(unsigned long long) * (size_t)g.W + sizeof(int) * (size_t)g.list_cap;
     if (smem > 48 * 1024) {
         e = cudaFuncSetAttribute(k_ex_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return oob::fail(OOB_E_CUDA, std::string("oob_exact_run smem: ") + cudaGetErrorString(e));
     }
-    k_ex_solve<<<g.slots, EXT, smem, s>>>(g, w);
-    k_ex_recon<<<g.slots, EXT, 0, s>>>(g, w, (unsigned char *)d_packed_out);
+    k_ex_solve<<<g.slots, EXS, smem, s>>>(g, w);
+    k_ex_recon<<<g.rslots, EXT, 0, s>>>(g, w, (unsigned char *)d_packed_out);
     e = cudaGetLastError();
     if (e != cudaSuccess) return oob::fail(OOB_E_CUDA, std::string("oob_exact_run launch: ") + cudaGetErrorString(e));
     return OOB_OK;
