@@ -261,6 +261,7 @@ def main():
     ap.add_argument("--profiles-per-rank", type=int, default=0,
                     help="profiles per rank (default: 1; cfg5: 1024/N)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-exact", action="store_true", help="skip the exact-optimum context run (1 GPU only)")
     ap.add_argument("--shard-profile", action="store_true",
                     help="N > 1: all ranks plan ONE profile, wavefronts split across GPUs (strong scaling)")
     ap.add_argument("--ref-sample-sizes", type=int, default=5,
@@ -461,6 +462,14 @@ def main():
     except Exception as exc:  # report, never hide
         all_ok = {"error": str(exc)}
     inst_all_ms = (time.perf_counter() - t0) * 1e3
+    # context (outside the timed region): the exact optimum of the same objective on the same
+    # device-resident inputs, bounded by the recursion's templates of the last timed step
+    exact = None
+    if world == 1 and not args.no_exact:
+        try:
+            exact = exact_context(planner, cfg, P, fwd, bwd, packed, info, sptr)
+        except Exception as exc:  # report, never hide
+            exact = {"error": str(exc)}
 
     if rank == 0:
         cpu = None
@@ -493,12 +502,46 @@ def main():
                                          "instantiate_every_surviving_N": inst_all_ms,
                                          "instantiate_every_surviving_N_detail": all_ok,
                                          "total": e2e_s * 1e3 + inst_ms + inst_all_ms},
+                "exact_optimum": exact,
                 "gpu_launches": int(info.kernel_launches) * args.steps,
                 "clocks": clocks, "step_ms": {"min": min(step_ms), "max": max(step_ms)}}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def exact_context(planner, cfg, P, fwd, bwd, packed, info, sptr):
+    """oob_exact_run on the timed step's inputs, bounded by its packed templates: ms per set
+    (CUDA events, after one warm-up run), tasks, and how far the recursion is from the optimum."""
+    import torch
+    xb = planner.exact_workspace_bytes(cfg.L, cfg.M, cfg.n0, cfg.n_max, P)
+    xws = torch.empty(xb, dtype=torch.uint8, device=fwd.device)
+    out = torch.empty_like(packed)
+
+    def run():
+        planner.exact_run(cfg.L, cfg.M, cfg.n0, cfg.n_max, P, fwd.data_ptr(), bwd.data_ptr(), packed.data_ptr(),
+                          xws.data_ptr(), xb, out.data_ptr(), sptr)
+    run()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    run()
+    b.record()
+    torch.cuda.synchronize()
+    tb = int(info.packed_template_bytes)
+    n = P * (cfg.n_max - cfg.n0 + 1)
+    hh = packed.cpu().numpy()[: n * tb].reshape(n, tb)
+    xx = out.cpu().numpy()[: n * tb].reshape(n, tb)
+    h_iter = hh[:, 48:56].copy().view(np.float64)[:, 0]
+    x_iter = xx[:, 48:56].copy().view(np.float64)[:, 0]
+    x_stat = xx[:, 12:16].copy().view(np.int32)[:, 0]
+    gap = h_iter / x_iter - 1.0
+    better = gap > 1e-12
+    return {"ms_per_set": a.elapsed_time(b), "tasks": int(xws[:8].cpu().numpy().view(np.uint64)[0]),
+            "templates": n, "status_ok": int((x_stat == 0).sum()), "recursion_above_optimum": int(better.sum()),
+            "max_gap": float(gap.max()), "mean_gap_where_above": float(gap[better].mean()) if better.any() else 0.0,
+            "workspace_bytes": xb, "kernel": "oob_exact_run (k_ex_*), see DESIGN.md section 12"}
 
 
 def _cpu_model():
