@@ -305,22 +305,28 @@ __device__ void ex_paths_fast(const ExGeom &g, const double *__restrict__ Tp, in
         s_row[m] = INFB;
     }
     __syncthreads();
-    const int pairs = G * M;
+    const int nt = blockDim.x, sq = nt / M, sr = nt % M;    // pair index i = (m - 1) M + (d - 1)
     for (int l2 = 1; l2 <= L; ++l2) {
-        for (int i = threadIdx.x; i < pairs; i += blockDim.x) {
-            const int m = i / M + 1, d = i % M + 1;
-            if (d > (m - 1) % M + 1) continue;
+        // targets m <= M l2 only (every stage has >= 1 layer and <= M GPUs)
+        const int pairs = min(G, M * l2) * M;
+        int m = threadIdx.x / M + 1, d = threadIdx.x % M + 1;
+        for (int i = threadIdx.x; i < pairs; i += nt) {
+            const int mc = m, dc = d;
+            m += sq;
+            d += sr;
+            if (d > M) { d -= M; ++m; }
+            if (dc > (mc - 1) % M + 1) continue;
             double best = EX_INF;
-            const double *tc = Tp + t_index(L, d, l2, 0);
+            const double *tc = Tp + t_index(L, dc, l2, 0);
             for (int l = l2 - 1; l >= 0; --l) {
                 const double t = tc[l];
                 if (t >= brk) break;
                 if (!(t < tau)) continue;
-                const double pv = pre[(size_t)l * W + m - d];
+                const double pv = pre[(size_t)l * W + mc - dc];
                 if (pv == EX_INF) continue;
                 best = fmin(best, __dadd_rn(pv, __dadd_rn(t, t4)));
             }
-            if (best < EX_INF) atomicMin(s_row + m, (unsigned long long)__double_as_longlong(best));
+            if (best < EX_INF) atomicMin(s_row + mc, (unsigned long long)__double_as_longlong(best));
         }
         __syncthreads();
         for (int m = threadIdx.x; m <= G; m += blockDim.x) {
@@ -330,19 +336,25 @@ __device__ void ex_paths_fast(const ExGeom &g, const double *__restrict__ Tp, in
         __syncthreads();
     }
     for (int l0 = L - 1; l0 >= 0; --l0) {
-        for (int i = threadIdx.x; i < pairs; i += blockDim.x) {
-            const int r = i / M + 1, d = i % M + 1;
-            if (d > (r - 1) % M + 1) continue;
+        const int pairs = min(G, M * (L - l0)) * M;             // r <= M (L - l0)
+        int r = threadIdx.x / M + 1, d = threadIdx.x % M + 1;
+        for (int i = threadIdx.x; i < pairs; i += nt) {
+            const int rc = r, dc = d;
+            r += sq;
+            d += sr;
+            if (d > M) { d -= M; ++r; }
+            if (dc > (rc - 1) % M + 1) continue;
             double best = EX_INF;
+            const double *tc = Tp + t_index(L, dc, 0, l0);
             for (int l = l0 + 1; l <= L; ++l) {
-                const double t = Tp[t_index(L, d, l, l0)];
+                const double t = tc[(size_t)l * (L + 1)];
                 if (t > brk) break;
                 if (!(t <= tau)) continue;
-                const double sv = suf[(size_t)l * W + r - d];
+                const double sv = suf[(size_t)l * W + rc - dc];
                 if (sv == EX_INF) continue;
                 best = fmin(best, __dadd_rn(sv, __dadd_rn(__dmul_rn(2.0, t), t3)));
             }
-            if (best < EX_INF) atomicMin(s_row + r, (unsigned long long)__double_as_longlong(best));
+            if (best < EX_INF) atomicMin(s_row + rc, (unsigned long long)__double_as_longlong(best));
         }
         __syncthreads();
         for (int r = threadIdx.x; r <= G; r += blockDim.x) {
