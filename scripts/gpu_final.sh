@@ -1,6 +1,7 @@
 #!/bin/bash
 # Round measurements on one GPU (run under gpurun): GPU tests, bench lines (cfg4, cfg5,
-# reference arm), ncu launch list + DRAM traffic of one cfg4 set, full captures of two waves.
+# reference arm), ncu launch list + DRAM traffic of one cfg4 set, full captures of two waves,
+# exact-solver timings.
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()"
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/final_pytest_gpu.log 2>&1; tail -3 gpurun_out/final_pytest_gpu.log
@@ -17,3 +18,4 @@ for W in 36 80; do
       --launch-count 1 -o gpurun_out/final_ncu_wave$W -f python scripts/dp_time.py cfg4 1 > gpurun_out/final_ncu_wave$W.log 2>&1
 done
 tail -c 300 gpurun_out/final_bench_cfg4.json
+for c in "cfg2 5" "cfg3 3" "cfg4 3" "cfg5 1 64"; do timeout 300 python scripts/exact_time.py $c; done > gpurun_out/final_exact_time.txt 2>&1
