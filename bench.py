@@ -490,7 +490,7 @@ def main():
                            "cells_per_step": cells_step, "splits_per_step": splits_step,
                            "l2": "flushed (256 MiB write) before every timed step",
                            "parallelism": (f"one profile, wavefronts sharded over {world} GPUs (partial argmins "
-                                           + ("exchanged inside k_wave_w over NVLink peer memory" if plan.info.pipelined
+                                           + ("exchanged inside k_wave_w over NVLink peer memory" if plan.info.exchange == 1
                                               else "all-gathered by NCCL per wavefront") + ")") if shard else
                                           f"independent template DPs, {P} profile(s) per rank x {world} rank(s)"
                                           + (", NCCL all-gather of packed template sets" if world > 1 and not shard

@@ -190,7 +190,9 @@ typedef struct {
     int32_t world;                  /* ranks sharing the wavefronts (oob_dp_set_comm) */
     int32_t warp_waves;             /* batched wavefronts run one warp per (profile, range) */
     int32_t small_range;            /* wavefronts whose in-node cells run one warp per (profile, range) */
-    int32_t reserved;
+    int32_t exchange;               /* sharded plans: 1 = partials exchanged inside k_wave_w over
+                                       NVLink peer memory, 2 = ncclAllGather + k_fin per wave,
+                                       3 = virtual shards (device copies); 0 = not sharded */
 } oob_dp_info;
 
 oob_status oob_dp_plan_create(int32_t L, int32_t M, int32_t n_lo, int32_t n_hi,

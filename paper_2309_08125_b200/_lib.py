@@ -55,7 +55,7 @@ class OobDpInfo(ctypes.Structure):
                 ("packed_bytes", c_size_t), ("kernel", c_int32), ("pipelined", c_int32),
                 ("fused", c_int32), ("seeded", c_int32), ("chunk_max", c_int32), ("refresh", c_int32),
                 ("small_pairs", c_int32), ("num_sms", c_int32), ("world", c_int32), ("warp_waves", c_int32),
-                ("small_range", c_int32), ("reserved", c_int32)]
+                ("small_range", c_int32), ("exchange", c_int32)]
 
 
 class OobAction(ctypes.Structure):

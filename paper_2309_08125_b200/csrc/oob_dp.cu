@@ -811,7 +811,7 @@ extern "C" oob_status oob_dp_plan_info(const oob_dp_plan *pl, oob_dp_info *out) 
     for (int l = 2; l <= g.L; ++l) out->warp_waves += pl->waves[l].warp ? 1 : 0;
     out->small_range = 0;
     for (int l = 2; l <= g.L; ++l) out->small_range += small_range_on(pl, l) ? 1 : 0;   // waves
-    out->reserved = 0;
+    out->exchange = pl->world > 1 ? (pl->xpeer ? 1 : (pl->comm ? 2 : 3)) : 0;
     return OOB_OK;
 }
 

@@ -53,6 +53,7 @@ ok = rec is not None and got == rec["profiles"][0]["templates"]
 oks = [None] * world
 dist.all_gather_object(oks, ok)
 if rank == 0:
-    print(json.dumps({"workload": key, "world": world, "ms_per_template_set": float(ms), "identical_to_oracle": oks}))
+    print(json.dumps({"workload": key, "world": world, "ms_per_template_set": float(ms), "identical_to_oracle": oks,
+                      "pipelined": info.pipelined, "exchange": info.exchange, "fused": info.fused}))
 dist.barrier()
 dist.destroy_process_group()

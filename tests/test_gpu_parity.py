@@ -287,7 +287,7 @@ def _virtual_run(planner, cfg, profs, world):
     plan = planner.DPPlan(cfg.L, cfg.M, cfg.n0, cfg.n_max, len(profs))
     plan.set_virtual_shards(world)
     info = plan.info
-    assert info.world == world and info.pipelined == 0
+    assert info.world == world and info.pipelined == 0 and (world == 1 or info.exchange == 3)
     fwd = torch.tensor(np.stack([p.fwd_ms for p in profs]), dtype=torch.float64, device="cuda")
     bwd = torch.tensor(np.stack([p.bwd_ms for p in profs]), dtype=torch.float64, device="cuda")
     ws = [torch.empty(info.workspace_bytes, dtype=torch.uint8, device="cuda") for _ in range(world)]
@@ -343,6 +343,7 @@ def _shard_worker(rank, world, port, q, xmode="peer"):
         plan.set_comm(comm)
         info = plan.info
         assert info.world == world and info.pipelined == (1 if xmode == "peer" else 0)
+        assert info.exchange == (1 if xmode == "peer" else 2)
         fwd = torch.tensor(prof.fwd_ms[None], dtype=torch.float64, device="cuda")
         bwd = torch.tensor(prof.bwd_ms[None], dtype=torch.float64, device="cuda")
         ws = torch.empty(info.workspace_bytes, dtype=torch.uint8, device="cuda")
