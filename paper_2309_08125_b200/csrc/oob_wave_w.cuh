@@ -1375,6 +1375,11 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
             __threadfence_system();
             __syncthreads();
             if (tid < w.world) atomicAdd(w.xdone[tid] + pr, 1);
+        } else if (w.fin_spin == 0) {
+            // OOB_DP_FINWAIT=0: merged CTAs leave (their slots go to the next wave); the
+            // range's publishing CTA waits for the other ranks and finalizes every share
+            if (tid == 0) OOB_TL_MAX(l, 3);
+            return;
         }
         if (tid == 0) {
             const int target = (int)w.epoch * w.world;
