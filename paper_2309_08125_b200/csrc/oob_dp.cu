@@ -289,7 +289,9 @@ struct Knobs {
                                // 5e6 with the peer exchange, 2e7 with per-wave ncclAllGather)
     long long spin_max = 1ll << 24;        // OOB_DP_PIPE_SPIN: polls before a pipeline wait times out
     int fin_wait = -1;         // OOB_DP_FINWAIT=0/1: merged CTAs exit (the range's last one finalizes
-                               // alone) / wait and share; default: wait on 1 GPU, exit with a peer exchange
+                               // alone) / wait and share; default: wait on 1 GPU, a few helpers with a
+                               // peer exchange
+    int fin_help = 512;        // OOB_DP_FINHELP: peer exchange, outputs of a range per finalize helper CTA
     int shard_x = 1;           // OOB_DP_SHARDX=nccl: per-wave ncclAllGather + k_fin instead of peer stores
     int small_range = 1;       // OOB_DP_SMALLRANGE=0: in-node cells thread(s) per cell instead of warp per range
     double slot_frac = 1.0;    // OOB_DP_SLOTFRAC: share of the resident CTA slots one wave's grid fills
@@ -316,6 +318,7 @@ Knobs read_knobs() {
     if (const char *v = env("OOB_DP_SHARDMIN")) k.shard_min = std::atof(v);
     if (const char *v = env("OOB_DP_PIPE_SPIN")) k.spin_max = std::max(0ll, std::atoll(v));
     if (const char *v = env("OOB_DP_FINWAIT")) k.fin_wait = std::atoi(v) != 0 ? 1 : 0;
+    if (const char *v = env("OOB_DP_FINHELP")) k.fin_help = std::max(1, std::atoi(v));
     if (const char *v = env("OOB_DP_SHARDX")) k.shard_x = std::string(v) == "nccl" ? 0 : 1;
     if (const char *v = env("OOB_DP_WARPMAX")) k.warp_units = std::max(0, std::atoi(v));
     if (const char *v = env("OOB_DP_SMALLRANGE")) k.small_range = std::max(0, std::min(2, std::atoi(v)));
@@ -1078,9 +1081,14 @@ static oob_status run_ranks(oob_dp_plan *pl, const double *d_fwd, const double *
             int64_t aux = 0;
             w.nbmain = (int)ctas;
             w.refresh = pl->kn.refresh && wh.cpr > 1;   // one CTA per range: its own filter is current
-            // merged CTAs wait to share the finalize (1 GPU), or leave and let the range's
-            // publishing CTA finalize alone (peer exchange: cfg4 on 4 GPUs 9.04 -> 8.57 ms)
-            w.fin_spin = (pl->kn.fin_wait > 0 || (pl->kn.fin_wait < 0 && !peer)) ? (1 << 22) : 0;
+            w.fin_spin = pl->kn.fin_wait != 0 ? (1 << 22) : 0;
+            // peer exchange: only the range's last merged CTAs wait for the other ranks' partials
+            // and share the finalize (~512 outputs each); the others leave at once and their
+            // slots go to the next wave (OOB_DP_FINWAIT=1: every CTA helps, 0: the last alone)
+            w.fin_helpers = pl->kn.fin_wait > 0 ? wh.cpr
+                            : pl->kn.fin_wait == 0 ? 1
+                                                   : std::max(1, std::min(wh.cpr, (wh.nout + pl->kn.fin_help - 1) /
+                                                                                      pl->kn.fin_help));
             w.warp_mode = wh.warp ? 1 : 0;
             // batched sweeps (one CTA per range, small shared memory, a larger L1): the exact
             // path's children are worth warming in L1 (cfg5 -2%; neutral to negative for cfg4)

@@ -100,6 +100,7 @@ struct WaveW {
     Pipe pp;                   // wavefront pipeline (pp.on = 0: plain kernel boundaries)
     int refresh;               // 1: each unit refreshes its filter entries from the range's global filter
     int fin_spin;              // polls a merged CTA waits for its range's others (0: exit; the last finalizes alone)
+    int fin_helpers;           // peer exchange: the range's last fin_helpers merged CTAs wait and share the finalize
     int warp_mode;             // 1: one WARP per (profile, range) (batched sweeps' short waves: the
                                // per-range work is a few units, a CTA per range idles on its prologue,
                                // barrier and finalize); no pipeline, cpr = 1, no merge
@@ -1364,7 +1365,12 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
         // finalize shares (fin_w_range takes the minimum over the gathered partials).
         __threadfence();
         __syncthreads();
-        if (tid == 0) s_last = atomicAdd(w.rdone + pr, 1) + 1 == w.cpr;
+        __shared__ int s_help;
+        if (tid == 0) {
+            const int ticket = atomicAdd(w.rdone + pr, 1) + 1;   // merge order, 1..cpr
+            s_last = ticket == w.cpr;
+            s_help = ticket > w.cpr - w.fin_helpers;            // the last fin_helpers CTAs finalize
+        }
         __syncthreads();
         if (s_last) {
             __threadfence();
@@ -1375,9 +1381,9 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
             __threadfence_system();
             __syncthreads();
             if (tid < w.world) atomicAdd(w.xdone[tid] + pr, 1);
-        } else if (w.fin_spin == 0) {
-            // OOB_DP_FINWAIT=0: merged CTAs leave (their slots go to the next wave); the
-            // range's publishing CTA waits for the other ranks and finalizes every share
+        } else if (!s_help) {
+            // merged CTAs other than the range's last fin_helpers leave (their slots go to
+            // the next wave); the helpers wait for the other ranks and share the finalize
             if (tid == 0) OOB_TL_MAX(l, 3);
             return;
         }
