@@ -289,9 +289,8 @@ struct Knobs {
                                // 5e6 with the peer exchange, 2e7 with per-wave ncclAllGather)
     long long spin_max = 1ll << 24;        // OOB_DP_PIPE_SPIN: polls before a pipeline wait times out
     int fin_wait = -1;         // OOB_DP_FINWAIT=0/1: merged CTAs exit (the range's last one finalizes
-                               // alone) / wait and share; default: wait on 1 GPU, a few helpers with a
-                               // peer exchange
-    int fin_help = 512;        // OOB_DP_FINHELP: peer exchange, outputs of a range per finalize helper CTA
+                               // alone) / all wait and share; default: the last ceil(nout / fin_help)
+    int fin_help = 512;        // OOB_DP_FINHELP: outputs of a range per finalize helper CTA
     int shard_x = 1;           // OOB_DP_SHARDX=nccl: per-wave ncclAllGather + k_fin instead of peer stores
     int small_range = 1;       // OOB_DP_SMALLRANGE=0: in-node cells thread(s) per cell instead of warp per range
     double slot_frac = 1.0;    // OOB_DP_SLOTFRAC: share of the resident CTA slots one wave's grid fills
@@ -1082,9 +1081,11 @@ static oob_status run_ranks(oob_dp_plan *pl, const double *d_fwd, const double *
             w.nbmain = (int)ctas;
             w.refresh = pl->kn.refresh && wh.cpr > 1;   // one CTA per range: its own filter is current
             w.fin_spin = pl->kn.fin_wait != 0 ? (1 << 22) : 0;
-            // peer exchange: only the range's last merged CTAs wait for the other ranks' partials
-            // and share the finalize (~512 outputs each); the others leave at once and their
-            // slots go to the next wave (OOB_DP_FINWAIT=1: every CTA helps, 0: the last alone)
+            // only the range's last merged CTAs (~512 outputs each) wait — for the range's other
+            // CTAs, and with a peer exchange for the other ranks' partials — and share the
+            // finalize; the others leave at once and their slots go to the next wave
+            // (OOB_DP_FINWAIT=1: every CTA helps, 0: the last alone; cfg4 14.54 -> 14.24 ms,
+            // sharded over 4 GPUs 9.04 -> 7.43 ms)
             w.fin_helpers = pl->kn.fin_wait > 0 ? wh.cpr
                             : pl->kn.fin_wait == 0 ? 1
                                                    : std::max(1, std::min(wh.cpr, (wh.nout + pl->kn.fin_help - 1) /

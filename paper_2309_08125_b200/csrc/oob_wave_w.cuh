@@ -1423,8 +1423,11 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
         __threadfence();
         __syncthreads();
         if (tid == 0) {
-            int ok = atomicAdd(w.rdone + pr, 1) + 1 == w.cpr;
-            for (int it = 0; !ok && it < w.fin_spin; ++it) {
+            const int ticket = atomicAdd(w.rdone + pr, 1) + 1;   // merge order, 1..cpr
+            int ok = ticket == w.cpr;
+            // only the range's last fin_helpers CTAs wait and share; the others leave
+            const int spin = ticket > w.cpr - w.fin_helpers ? w.fin_spin : 0;
+            for (int it = 0; !ok && it < spin; ++it) {
                 __nanosleep(128);
                 ok = *(volatile int *)(w.rdone + pr) >= w.cpr;
             }

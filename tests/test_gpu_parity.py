@@ -228,6 +228,8 @@ VARIANTS = [
     ({"OOB_DP_REFRESH": "0"}, {"refresh": 0}),                 # no per-unit filter refresh
     ({"OOB_DP_SMALLRANGE": "0"}, {"small_range": 0}),          # in-node cells thread(s) per cell
     ({"OOB_DP_FINWAIT": "0"}, {}),                             # merged CTAs exit; last one finalizes alone
+    ({"OOB_DP_FINWAIT": "1"}, {}),                             # every merged CTA waits and shares the finalize
+    ({"OOB_DP_FINHELP": "64"}, {}),                            # many finalize helpers (default: nout / 512)
 ]
 
 
