@@ -1057,7 +1057,7 @@ static oob_status run_ranks(oob_dp_plan *pl, const double *d_fwd, const double *
         if (pl->timing && (!pipe_on || l == 2)) cudaEventRecord(pl->ev[pl->ev_used], stream);
         for (int i = 0; i < nr && ctas > 0; ++i) {
             RankRun &R = rr[i];
-            WaveW w;
+            WaveW w{};
             w.l = l;
             w.nranges = G.L - l + 1;
             w.cpr = wh.cpr;
@@ -1216,14 +1216,14 @@ extern "C" int oob_dbg_flush_stats(int enable, unsigned long long *out4) {
 }
 
 // Diagnostic (not part of the C ABI header; -DOOB_TIMELINE builds only): read and reset the
-// per-wave timeline of k_wave_w (6 x u64 per wave, see g_tl).
+// per-wave timeline of k_wave_w (8 x u64 per wave, see g_tl).
 extern "C" int oob_dbg_timeline(unsigned long long *out, int nwaves) {
 #ifdef OOB_TIMELINE
     if (nwaves > 1024) return 1;
-    if (out && cudaMemcpyFromSymbol(out, oob::g_tl, sizeof(unsigned long long) * 6 * nwaves) != cudaSuccess) return 1;
-    static unsigned long long init[1024][6];
+    if (out && cudaMemcpyFromSymbol(out, oob::g_tl, sizeof(unsigned long long) * 8 * nwaves) != cudaSuccess) return 1;
+    static unsigned long long init[1024][8];
     for (int i = 0; i < 1024; ++i)
-        for (int j = 0; j < 6; ++j) init[i][j] = (j == 0 || j == 1 || j == 4) ? ~0ull : 0ull;
+        for (int j = 0; j < 8; ++j) init[i][j] = (j == 0 || j == 1 || j == 4) ? ~0ull : 0ull;
     return cudaMemcpyToSymbol(oob::g_tl, init, sizeof(init)) == cudaSuccess ? 0 : 1;
 #else
     (void)out; (void)nwaves;

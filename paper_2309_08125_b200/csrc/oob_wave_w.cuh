@@ -187,7 +187,7 @@ __device__ int g_flush_stats_on;
 // CTA done with its units, [3] last CTA done (finalize included), [4] first aux block start,
 // [5] last aux block end
 #ifdef OOB_TIMELINE
-__device__ unsigned long long g_tl[1024][6];
+__device__ unsigned long long g_tl[1024][8];
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -1161,6 +1161,7 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
             __syncthreads();
             fin_seed_one(g, w.fa, (int64_t)ab * NTW + threadIdx.x);
             pipe_signal(w.pp, L_of(g), 0, w.fa.lseed);
+            if (threadIdx.x == 0) OOB_TL_MAX(w.l, 6);
         } else {
             // in-node cells of wave l+1 read in-node cells of waves <= l
             if (threadIdx.x == 0) pipe_wait(w.pp, L_of(g), w.fa.ls - 1, 2);
@@ -1168,6 +1169,7 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
             if (w.fa.small_range) fin_small_range(g, w.fa, (int64_t)ab - w.fa.nbseed, smem);
             else fin_small_block(g, w.fa, (int64_t)ab - w.fa.nbseed);
             pipe_signal(w.pp, L_of(g), 1, w.fa.ls);
+            if (threadIdx.x == 0) OOB_TL_MAX(w.l, 7);
         }
         if (threadIdx.x == 0) OOB_TL_MAX(w.l, 5);
         return;

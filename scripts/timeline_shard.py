@@ -34,7 +34,7 @@ packed = torch.empty(info.packed_bytes, dtype=torch.uint8, device="cuda")
 f = lib.oob_dbg_timeline
 f.restype = ctypes.c_int
 f.argtypes = [ctypes.c_void_p, ctypes.c_int]
-buf = np.zeros((cfg.L + 1, 6), dtype=np.uint64)
+buf = np.zeros((cfg.L + 1, 8), dtype=np.uint64)
 for r in range(4):
     assert f(None, cfg.L + 1) == 0, "library built without OOB_TIMELINE"
     dist.barrier()
