@@ -100,3 +100,19 @@ def test_exact_window_by_recursion_total():
         a = exact_template(p.fwd_ms, p.bwd_ms, M, n)
         b = exact_template(p.fwd_ms, p.bwd_ms, M, n, ub=ub)
         assert a["total"] == b["total"] and a["stages"] == b["stages"]
+
+
+def test_exact_vs_brute_force_constant_ties():
+    """Constant profiles (every layer alike: massive ties among mappings): exact == brute
+    force bit for bit, and the returned mapping is one of brute force's argmins."""
+    rng = random.Random(9)
+    for i in range(30):
+        L = rng.randint(2, 7)
+        M = rng.randint(1, 3)
+        n = rng.randint(1, min(3, L))
+        p = random_profile(9900 + i, L, M, "constant")
+        best, arg = brute_force(p.fwd_ms, p.bwd_ms, M, n)
+        e = exact_template(p.fwd_ms, p.bwd_ms, M, n)
+        _valid(e["stages"], L, M, n)
+        assert e["total"] == best
+        assert tuple(e["stages"]) in [tuple(m) for m in arg]
