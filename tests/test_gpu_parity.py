@@ -483,9 +483,20 @@ def _comm_worker(rank, world, port, q):
         profs = config_profiles(cfg, "real", count=5)
         ts = pl.generate_templates([(p.fwd_ms, p.bwd_ms) for p in profs], nodes=cfg.N, gpus_per_node=cfg.M,
                                    f=cfg.f, n0=cfg.n0, device=rank, comm=comm)
+        heur = []
         for i, p in enumerate(profs):
             want, _ = coracle.template_set(p.fwd_ms, p.bwd_ms, cfg.M, cfg.n0, cfg.n_max)
+            heur.append(want)
             ok = ok and ts.templates(i) == want
+        # the same batch with the exact optimum (opts.exact): each rank's block, all-gathered
+        from oracle.exact import exact_template
+        ts = pl.generate_templates([(p.fwd_ms, p.bwd_ms) for p in profs], nodes=cfg.N, gpus_per_node=cfg.M,
+                                   f=cfg.f, n0=cfg.n0, device=rank, comm=comm, exact=True)
+        for i, p in enumerate(profs):
+            for t in ts.templates(i)[::6]:
+                e = exact_template(p.fwd_ms, p.bwd_ms, cfg.M, t["nodes"], ub=heur[i][t["nodes"] - cfg.n0]["total"])
+                ok = ok and (t["S"], t["total"], [s[:4] for s in t["stages"]]) == \
+                    (e["S"], e["total"], [tuple(s) for s in e["stages"]])
         q.put((rank, ok))
     finally:
         dist.destroy_process_group()
@@ -493,8 +504,8 @@ def _comm_worker(rank, world, port, q):
 
 def test_generate_templates_with_communicator_two_gpus(planner):
     """oob_generate_templates with opts.comm (the headline API's multi-GPU path): one
-    profile sharded per wavefront, and a batch split in blocks + NCCL all-gather; every
-    rank receives the oracle's whole template set (needs >= 2 GPUs)."""
+    profile sharded per wavefront, and a batch split in blocks + NCCL all-gather (also with
+    opts.exact); every rank receives the oracle's whole template set (needs >= 2 GPUs)."""
     import socket
     import torch
     import torch.multiprocessing as mp
