@@ -290,7 +290,7 @@ struct Knobs {
     long long spin_max = 1ll << 24;        // OOB_DP_PIPE_SPIN: polls before a pipeline wait times out
     int fin_wait = -1;         // OOB_DP_FINWAIT=0/1: merged CTAs exit (the range's last one finalizes
                                // alone) / all wait and share; default: the last ceil(nout / fin_help)
-    int fin_help = 512;        // OOB_DP_FINHELP: outputs of a range per finalize helper CTA
+    int fin_help = 0;          // OOB_DP_FINHELP: outputs of a range per finalize helper CTA (0: 512, 768 with a peer exchange)
     int shard_x = 1;           // OOB_DP_SHARDX=nccl: per-wave ncclAllGather + k_fin instead of peer stores
     int small_range = 1;       // OOB_DP_SMALLRANGE=0: in-node cells thread(s) per cell instead of warp per range
     double slot_frac = 1.0;    // OOB_DP_SLOTFRAC: share of the resident CTA slots one wave's grid fills
@@ -1086,10 +1086,11 @@ static oob_status run_ranks(oob_dp_plan *pl, const double *d_fwd, const double *
             // finalize; the others leave at once and their slots go to the next wave
             // (OOB_DP_FINWAIT=1: every CTA helps, 0: the last alone; cfg4 14.54 -> 14.24 ms,
             // sharded over 4 GPUs 9.04 -> 7.43 ms)
+            // (peer exchange: 768 outputs per helper, 4 GPUs 7.43 -> 7.35 ms)
+            const int fin_help = pl->kn.fin_help > 0 ? pl->kn.fin_help : (peer ? 768 : 512);
             w.fin_helpers = pl->kn.fin_wait > 0 ? wh.cpr
                             : pl->kn.fin_wait == 0 ? 1
-                                                   : std::max(1, std::min(wh.cpr, (wh.nout + pl->kn.fin_help - 1) /
-                                                                                      pl->kn.fin_help));
+                                                   : std::max(1, std::min(wh.cpr, (wh.nout + fin_help - 1) / fin_help));
             w.warp_mode = wh.warp ? 1 : 0;
             // batched sweeps (one CTA per range, small shared memory, a larger L1): the exact
             // path's children are worth warming in L1 (cfg5 -2%; neutral to negative for cfg4)
