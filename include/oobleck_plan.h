@@ -280,8 +280,10 @@ oob_status oob_dp_run_virtual(oob_dp_plan *plan, const double *d_fwd, const doub
  *                    for an unbounded search (every stage time; slower)
  *   d_workspace    : >= oob_exact_workspace_bytes (same shape, current device); its first 8
  *                    bytes receive the number of (profile, tau) tasks solved (uint64)
- *   d_packed_out   : packed templates in oob_dp_run's layout (status 0; 3 = no mapping); may
- *                    be d_packed_ub (each bound is read before any output is written)
+ *   d_packed_out   : packed templates in oob_dp_run's layout (status 0; 3 = no mapping; 4 =
+ *                    an internal list overflowed: every template of the run is marked and
+ *                    oob_template_set_from_packed fails with OOB_E_CUDA); may be d_packed_ub
+ *                    (each bound is read before any output is written)
  * Enqueued on `stream`, no synchronisation.  Errors: OOB_E_INVALID (shape: 1 <= n_lo <=
  * n_hi <= L <= 1023, M <= 64, n_hi * M <= ~21,000), OOB_E_NOMEM (workspace), OOB_E_CUDA. */
 oob_status oob_exact_workspace_bytes(int32_t L, int32_t M, int32_t n_lo, int32_t n_hi,
