@@ -303,3 +303,19 @@ def test_min_nodes_spec(planner):
     from paper_2309_08125_b200._lib import OobError
     with pytest.raises(OobError):
         p.min_nodes(4, 40 * GB, 0.8)
+
+
+def test_exact_entry_points_fail_cleanly_without_device(planner):
+    """oob_exact_run / oob_exact_workspace_bytes: NULL buffers are OOB_E_INVALID before any
+    CUDA call; without a device the size query reports OOB_E_CUDA (no crash, no fallback)."""
+    from paper_2309_08125_b200._lib import OOB_E_CUDA, OOB_E_INVALID, OobError
+    with pytest.raises(OobError) as e:
+        planner.exact_run(12, 4, 1, 4, 1, 0, 0, 0, 0, 0, 0)
+    assert e.value.status == OOB_E_INVALID
+    import torch
+    if torch.cuda.is_available():
+        assert planner.exact_workspace_bytes(12, 4, 1, 4, 1) > 0
+        return
+    with pytest.raises(OobError) as e:
+        planner.exact_workspace_bytes(12, 4, 1, 4, 1)
+    assert e.value.status == OOB_E_CUDA
