@@ -446,14 +446,15 @@ __device__ __forceinline__ unsigned pending_mask(const float (&mn)[TE], const fl
 // blocks of TE steps (no guards) and a guarded tail; the outputs whose bounds pass the
 // filter are collected per block (bit mask) and re-evaluated exactly.
 template <int TE, bool LT>
-__device__ __forceinline__ void run_rows(XRing &xr, int64_t sidx, const int32_t *wls, int r_lo, int r_hi,
-                                         const float (&TA)[TE], const float (&TB)[TE], const float (&TS)[TE],
-                                         const float (&TC)[TE], int64_t bidx, int ncell, int rowB, int e0,
-                                         int l1, int L, const int *outOff, int nout, unsigned acc_s,
-                                         unsigned filt_s, unsigned *gfr, uint4 *q4, unsigned *q1,
-                                         const Cell4 *CELL) {
+__device__ __forceinline__ int run_rows(XRing &xr, int64_t sidx, const int32_t *wls, int r_lo, int r_hi,
+                                        const float (&TA)[TE], const float (&TB)[TE], const float (&TS)[TE],
+                                        const float (&TC)[TE], int64_t bidx, int ncell, int rowB, int e0,
+                                        int l1, int L, const int *outOff, int nout, unsigned acc_s,
+                                        unsigned filt_s, unsigned *gfr, uint4 *q4, unsigned *q1,
+                                        const Cell4 *CELL, int qn) {
     static_assert(TE == 4, "the pending-output switch below covers TE = 4");
-    int qn = 0;                                           // queued outputs (warp-uniform)
+    // qn: outputs queued so far by this warp (warp-uniform); the queue carries over to the
+    // warp's next unit of the same range and is flushed when full or after the last unit
     const int S0 = rowB + e0;
     const float *filt = reinterpret_cast<const float *>(__cvta_shared_to_generic(filt_s));
     int rb = 0;                                           // chunk cell of the row's first cell
@@ -531,9 +532,9 @@ __device__ __forceinline__ void run_rows(XRing &xr, int64_t sidx, const int32_t 
         }
         rb += rl;
     }
-    if (qn) xq_flush<TE>(q4, q1, qn, CELL, acc_s, filt_s, gfr);
     asm volatile("cp.async.wait_group 0;" ::: "memory");   // no copy of this chunk outlives the unit
     __syncwarp();
+    return qn;
 }
 
 // One warp unit (inlined: an out-of-line unit measured 9% slower on cfg4, and capping the
@@ -543,10 +544,10 @@ __device__ __forceinline__ void run_rows(XRing &xr, int64_t sidx, const int32_t 
 // the filter entries of the outputs [olo, ohi) the unit can touch from the range's global
 // filter (minima the range's other CTAs found), then run the rows.
 template <int TE, bool LT>
-__device__ __forceinline__ void run_unit(const float4 *__restrict__ SH, const Cell4 *CELL, int64_t sidx, const int32_t *wls,
-                                      int r_lo, int r_hi, int64_t bidx, int ncell, int rowB, int e0, int l1, int L,
-                                      const int *outOff, int nout, unsigned acc_s, unsigned filt_s, unsigned *gfr,
-                                      unsigned char *wsm, int olo, int ohi) {
+__device__ __forceinline__ int run_unit(const float4 *__restrict__ SH, const Cell4 *CELL, int64_t sidx, const int32_t *wls,
+                                     int r_lo, int r_hi, int64_t bidx, int ncell, int rowB, int e0, int l1, int L,
+                                     const int *outOff, int nout, unsigned acc_s, unsigned filt_s, unsigned *gfr,
+                                     unsigned char *wsm, int olo, int ohi, int qn) {
     const int lane = threadIdx.x & 31;
     uint4 *q4 = reinterpret_cast<uint4 *>(wsm + XR_BYTES);         // this warp's candidate queue
     unsigned *q1 = reinterpret_cast<unsigned *>(q4 + XQ_CAP);
@@ -572,8 +573,18 @@ __device__ __forceinline__ void run_unit(const float4 *__restrict__ SH, const Ce
         for (int j = 0; j < 4; ++j)
             if (gv[j] < filt[i0 + 32 * j]) atomicMin(filt + i0 + 32 * j, gv[j]);
     }
-    run_rows<TE, LT>(xr, sidx, wls, r_lo, r_hi, TA, TB, TS, TC, bidx, ncell, rowB, e0, l1, L, outOff, nout, acc_s, filt_s,
-                     gfr, q4, q1, CELL);
+    return run_rows<TE, LT>(xr, sidx, wls, r_lo, r_hi, TA, TB, TS, TC, bidx, ncell, rowB, e0, l1, L, outOff, nout, acc_s,
+                            filt_s, gfr, q4, q1, CELL, qn);
+}
+
+// The warp's queued candidates after its last unit of a range.
+template <int TE>
+__device__ __forceinline__ void flush_rest(unsigned char *wsm, int qn, const Cell4 *CELL, unsigned acc_s, unsigned filt_s,
+                                           unsigned *gfr) {
+    if (qn) {
+        const uint4 *q4 = reinterpret_cast<const uint4 *>(wsm + XR_BYTES);
+        xq_flush<TE>(q4, reinterpret_cast<const unsigned *>(q4 + XQ_CAP), qn, CELL, acc_s, filt_s, gfr);
+    }
 }
 
 // Per-wave finalize + small cells.  Blocks [0, nbw): one thread per (profile, range, W-part
@@ -1093,7 +1104,7 @@ __device__ __forceinline__ void warp_ranges(const DevGeom &g, const WaveW &w, un
     const unsigned acc_s = (unsigned)__cvta_generic_to_shared(acc);
     const unsigned filt_s = (unsigned)__cvta_generic_to_shared(filt);
     unsigned char *wsm = reinterpret_cast<unsigned char *>(rings) + (size_t)wi * (XR_BYTES + XQ_BYTES);
-    int ei = 0;
+    int ei = 0, qn = 0;
     for (int un = 0; un < w.nunits; ++un) {
         while (upre[ei + 1] <= un) ++ei;
         const int4 en = sents[ei];
@@ -1118,12 +1129,13 @@ __device__ __forceinline__ void warp_ranges(const DevGeom &g, const WaveW &w, un
         const int64_t sidx = pc + sbase[ls] + (int64_t)us * scells[ls] + d_wofs(g, ls, r_lo);
         const int64_t bidx = pc + sbase[lb] + (int64_t)ub * scells[lb] + (has ? wb0 : d_wofs(g, lb, 1)) + e0;
         if (ltiled)
-            run_unit<TE, true>(g.SH, g.CELL, sidx, g.wofs + ls * (L + 2), r_lo, r_hi, bidx, ncell, rowB, e0, l1, L,
-                               outOff, nout, acc_s, filt_s, gfilt, wsm, 0, 0);
+            qn = run_unit<TE, true>(g.SH, g.CELL, sidx, g.wofs + ls * (L + 2), r_lo, r_hi, bidx, ncell, rowB, e0, l1, L,
+                                    outOff, nout, acc_s, filt_s, gfilt, wsm, 0, 0, qn);
         else
-            run_unit<TE, false>(g.SH, g.CELL, sidx, g.wofs + ls * (L + 2), r_lo, r_hi, bidx, ncell, rowB, e0, l1, L,
-                                outOff, nout, acc_s, filt_s, gfilt, wsm, 0, 0);
+            qn = run_unit<TE, false>(g.SH, g.CELL, sidx, g.wofs + ls * (L + 2), r_lo, r_hi, bidx, ncell, rowB, e0, l1, L,
+                                     outOff, nout, acc_s, filt_s, gfilt, wsm, 0, 0, qn);
     }
+    flush_rest<TE>(wsm, qn, g.CELL, acc_s, filt_s, gfilt);
     __syncwarp();
     if (tid % 32 == 0) OOB_TL_MAX(l, 2);
     fin_w_range<32>(g, w.fw, pr, lane, 0, 1, acc);
@@ -1258,6 +1270,8 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
     const unsigned acc_s = (unsigned)__cvta_generic_to_shared(acc);
     const unsigned filt_s = (unsigned)__cvta_generic_to_shared(filt);
     int *gctr = w.ctr + pr;
+    unsigned char *wsm = reinterpret_cast<unsigned char *>(rings) + (size_t)(tid >> 5) * (XR_BYTES + XQ_BYTES);
+    int qn = 0;                                                   // this warp's queued candidates
 
     for (;;) {
         int un = 0;
@@ -1303,7 +1317,6 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
         const int ncell = max(0, min(TE, lenB - e0));             // valid cells of the tile
         // the streamed chunk's first batches are in flight while the tile and the filter load
         const int64_t sidx = pc + sbase[ls] + (int64_t)us * scells[ls] + d_wofs(g, ls, r_lo);
-        unsigned char *wsm = reinterpret_cast<unsigned char *>(rings) + (size_t)(tid >> 5) * (XR_BYTES + XQ_BYTES);
         if (w.prefetch) {   // warm L1 with the binary64 cells the exact path may load
             const Cell4 *tp = g.CELL + pc + sbase[lb] + (int64_t)ub * scells[lb] + (has ? d_wofs(g, lb, rowB) : 0) + e0;
             asm volatile("prefetch.global.L1 [%0];" ::"l"(tp));
@@ -1321,12 +1334,13 @@ __global__ void __launch_bounds__(NTW, WAVE_CTAS_PER_SM) k_wave_w(DevGeom g, Wav
             ohi = outOff[min(rmax + r_hi, L + 1)];
         }
         if (ltiled)
-            run_unit<TE, true>(g.SH, g.CELL, sidx, g.wofs + ls * (L + 2), r_lo, r_hi, bidx, ncell, rowB, e0, l1, L,
-                               outOff, nout, acc_s, filt_s, gfilt, wsm, olo, ohi);
+            qn = run_unit<TE, true>(g.SH, g.CELL, sidx, g.wofs + ls * (L + 2), r_lo, r_hi, bidx, ncell, rowB, e0, l1, L,
+                                    outOff, nout, acc_s, filt_s, gfilt, wsm, olo, ohi, qn);
         else
-            run_unit<TE, false>(g.SH, g.CELL, sidx, g.wofs + ls * (L + 2), r_lo, r_hi, bidx, ncell, rowB, e0, l1, L,
-                                outOff, nout, acc_s, filt_s, gfilt, wsm, olo, ohi);
+            qn = run_unit<TE, false>(g.SH, g.CELL, sidx, g.wofs + ls * (L + 2), r_lo, r_hi, bidx, ncell, rowB, e0, l1, L,
+                                     outOff, nout, acc_s, filt_s, gfilt, wsm, olo, ohi, qn);
     }
+    flush_rest<TE>(wsm, qn, g.CELL, acc_s, filt_s, gfilt);
     __syncthreads();
     if (tid == 0) OOB_TL_MAX(l, 2);
     // merge into the range's global accumulator (L2-coherent loads; a stale value is an
