@@ -395,19 +395,21 @@ __device__ __noinline__ int xq_push(unsigned mask, int base, unsigned bidx, int 
         const unsigned bal = __ballot_sync(0xFFFFFFFFu, h);
         if (!bal) break;
         const int n = __popc(bal);
-        if (count + n > XQ_CAP) {
+        if (h) {
+            const int slot = count + __popc(bal & lane_lt);
+            if (slot < XQ_CAP) {           // lanes past a full queue keep their bit for the next round
+                const int Ep = base + __ffs(mask) - 1;
+                mask &= mask - 1;
+                q4[slot] = make_uint4(bidx, srow, kb,
+                                      (unsigned)(idx0 + Ep) | ((unsigned)ncell << 16) | (LT ? 1u << 19 : 0u));
+                q1[slot] = (LT ? (unsigned)rs : (unsigned)S0) | ((unsigned)Ep << 10) | ((unsigned)rl << 21);
+            }
+        }
+        count = min(count + n, XQ_CAP);
+        if (count == XQ_CAP) {              // flush full queues only
             xq_flush<TE>(q4, q1, count, CELL, acc_s, filt_s, gfr);
             count = 0;
         }
-        if (h) {
-            const int Ep = base + __ffs(mask) - 1;
-            mask &= mask - 1;
-            const int slot = count + __popc(bal & lane_lt);
-            q4[slot] = make_uint4(bidx, srow, kb,
-                                  (unsigned)(idx0 + Ep) | ((unsigned)ncell << 16) | (LT ? 1u << 19 : 0u));
-            q1[slot] = (LT ? (unsigned)rs : (unsigned)S0) | ((unsigned)Ep << 10) | ((unsigned)rl << 21);
-        }
-        count += n;
     }
     return count;
 }
