@@ -518,7 +518,8 @@ def main():
                                          "total": e2e_s * 1e3 + inst_ms + inst_all_ms + reconf_ms},
                 "exact_optimum": exact,
                 "gpu_launches": int(info.kernel_launches) * args.steps,
-                "clocks": clocks, "step_ms": {"min": min(step_ms), "max": max(step_ms)}}
+                "clocks": clocks, "step_ms": {"min": min(step_ms), "max": max(step_ms), "median": statistics.median(step_ms),
+                            "all": [round(x, 4) for x in step_ms]}}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
