@@ -339,6 +339,10 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        if world > 1:
+            # device-side start line: every rank's stream leaves this all-reduce together, so
+            # the first timed step does not absorb the ranks' host skew after the barrier
+            dist.all_reduce(torch.zeros(1, device=dev))
         for i in range(args.steps):
             flush.fill_(i & 0xFF)                  # L2 flush between timed steps
             evs[i][0].record(stream)
