@@ -295,7 +295,7 @@ struct Knobs {
     int small_range = 1;       // OOB_DP_SMALLRANGE=0: in-node cells thread(s) per cell instead of warp per range
     double slot_frac = 1.0;    // OOB_DP_SLOTFRAC: share of the resident CTA slots one wave's grid fills
     int slot_frac_lmax = 1 << 30;   // OOB_DP_SLOTFRAC_LMAX: ... for waves l <= this only
-    int warp_units = 96;       // OOB_DP_WARPMAX: batched waves with <= this many units per range run one
+    int warp_units = 64;       // OOB_DP_WARPMAX: batched waves with <= this many units per range run one
                                // warp per (profile, range) (0: never)
     int debug = 0;             // OOB_DP_DEBUG: per-wave plan on stderr
 };
