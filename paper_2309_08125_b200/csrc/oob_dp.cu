@@ -281,7 +281,7 @@ struct Knobs {
     double seed_spo = 0.0;     // OOB_DP_SEEDSPO: seed waves with >= this many splits per W output
     int seed_min_l = SEED_MIN_L;   // OOB_DP_SEEDMINL: first seeded wavefront
     int small_pairs = 1;       // OOB_DP_SMALLPAIRS: layer splits per thread of an in-node cell
-    int chunk_max = 0;         // OOB_DP_CHMAX: streamed cells per unit (upper bound; 0: 320, 192 / 96 sharded over 2 / >= 4)
+    int chunk_max = 0;         // OOB_DP_CHMAX: streamed cells per unit (upper bound; 0: 320, 192 / 96 sharded over 2-3 / >= 4)
     int units_per_cta = 0;     // OOB_DP_UPC: minimum queue units per CTA (chunk size)
     int units_per_warp = 4;    // OOB_DP_UPW: chunks shrink until every warp slot has this many units
     int refresh = 1;           // OOB_DP_REFRESH=0: no per-unit filter refresh
@@ -546,7 +546,7 @@ static bool plan_pipe_on(const oob_dp_plan *pl) {
 
 // Wave sizing (chunks, CTAs per range, seeds), workspace layout and the geometry blob, for
 // `world` ranks sharing every wave's units: 320-cell chunks on one GPU (cfg4 13.96 -> 13.84 ms
-// with the carried-over candidate queue), 192 on 2 ranks, 96 from 4 (each rank's share of a
+// with the carried-over candidate queue), 192 on 2-3 ranks, 96 from 4 (each rank's share of a
 // range still has enough units; 4 GPUs 7.35 -> 7.20 ms).  Host only; run by
 // oob_dp_plan_create and again by oob_dp_set_comm / oob_dp_set_virtual_shards.
 static void size_plan(oob_dp_plan *pl, int world) {
@@ -554,7 +554,7 @@ static void size_plan(oob_dp_plan *pl, int world) {
     const int L = g.L, M = g.M, num_profiles = pl->P, SMS = pl->num_sms;
     pl->kernel = pl->kn.kernel;
     pl->max_smem = 0;
-    const int chmax = pl->kn.chunk_max > 0 ? pl->kn.chunk_max : (world >= 4 ? 96 : world == 2 ? 192 : 320);
+    const int chmax = pl->kn.chunk_max > 0 ? pl->kn.chunk_max : (world >= 4 ? 96 : world >= 2 ? 192 : 320);
     pl->chunk_eff = chmax;
     pl->waves.assign(L + 1, WaveHost());
     size_t items_total = 0, gacc_max = 0, ctr_total = 0;

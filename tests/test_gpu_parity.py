@@ -292,7 +292,7 @@ def _virtual_run(planner, cfg, profs, world):
     assert info.world == world and info.pipelined == 0 and (world == 1 or info.exchange == 3)
     import os
     if "OOB_DP_CHMAX" not in os.environ:        # waves re-sized for the ranks' unit shares
-        assert info.chunk_max == (320 if world == 1 else 192 if world == 2 else 96)
+        assert info.chunk_max == (320 if world == 1 else 192 if world <= 3 else 96)
     fwd = torch.tensor(np.stack([p.fwd_ms for p in profs]), dtype=torch.float64, device="cuda")
     bwd = torch.tensor(np.stack([p.bwd_ms for p in profs]), dtype=torch.float64, device="cuda")
     ws = [torch.empty(info.workspace_bytes, dtype=torch.uint8, device="cuda") for _ in range(world)]
