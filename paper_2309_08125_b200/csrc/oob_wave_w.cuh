@@ -100,7 +100,7 @@ struct WaveW {
     Pipe pp;                   // wavefront pipeline (pp.on = 0: plain kernel boundaries)
     int refresh;               // 1: each unit refreshes its filter entries from the range's global filter
     int fin_spin;              // polls a merged CTA waits for its range's others (0: exit; the last finalizes alone)
-    int fin_helpers;           // peer exchange: the range's last fin_helpers merged CTAs wait and share the finalize
+    int fin_helpers;           // the range's last fin_helpers merged CTAs wait (for the others / the ranks) and share the finalize
     int warp_mode;             // 1: one WARP per (profile, range) (batched sweeps' short waves: the
                                // per-range work is a few units, a CTA per range idles on its prologue,
                                // barrier and finalize); no pipeline, cpr = 1, no merge
@@ -185,7 +185,7 @@ __device__ int g_flush_stats_on;
 // diagnostic timeline (compiled in with -DOOB_TIMELINE, scripts/timeline.py): per wave the
 // global-timer ns of [0] first main-CTA start, [1] first CTA past its prologue waits, [2] last
 // CTA done with its units, [3] last CTA done (finalize included), [4] first aux block start,
-// [5] last aux block end
+// [5] last aux block end, [6] last seed block end, [7] last in-node block end
 #ifdef OOB_TIMELINE
 __device__ unsigned long long g_tl[1024][8];
 __device__ __forceinline__ unsigned long long gtime() {
