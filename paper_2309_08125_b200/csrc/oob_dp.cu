@@ -285,6 +285,8 @@ struct Knobs {
     int units_per_cta = 0;     // OOB_DP_UPC: minimum queue units per CTA (chunk size)
     int units_per_warp = 4;    // OOB_DP_UPW: chunks shrink until every warp slot has this many units
     int refresh = 1;           // OOB_DP_REFRESH=0: no per-unit filter refresh
+    int refresh_lmin = 64;     // OOB_DP_REFRESHL: refresh only from this wavefront on (shorter waves:
+                               // small units, the refresh costs more than it filters; cfg4 13.84 -> 13.76 ms)
     double shard_min = -1.0;   // OOB_DP_SHARDMIN: waves with fewer splits run redundantly (default:
                                // 5e6 with the peer exchange, 2e7 with per-wave ncclAllGather)
     long long spin_max = 1ll << 24;        // OOB_DP_PIPE_SPIN: polls before a pipeline wait times out
@@ -314,6 +316,7 @@ Knobs read_knobs() {
     if (const char *v = env("OOB_DP_UPC")) k.units_per_cta = std::max(0, std::atoi(v));
     if (const char *v = env("OOB_DP_UPW")) k.units_per_warp = std::max(1, std::atoi(v));
     if (const char *v = env("OOB_DP_REFRESH")) k.refresh = std::atoi(v) != 0;
+    if (const char *v = env("OOB_DP_REFRESHL")) k.refresh_lmin = std::max(0, std::atoi(v));
     if (const char *v = env("OOB_DP_SHARDMIN")) k.shard_min = std::atof(v);
     if (const char *v = env("OOB_DP_PIPE_SPIN")) k.spin_max = std::max(0ll, std::atoll(v));
     if (const char *v = env("OOB_DP_FINWAIT")) k.fin_wait = std::atoi(v) != 0 ? 1 : 0;
@@ -1109,7 +1112,7 @@ static oob_status run_ranks(oob_dp_plan *pl, const double *d_fwd, const double *
             w.world = shard ? pl->world : 1;
             int64_t aux = 0;
             w.nbmain = (int)ctas;
-            w.refresh = pl->kn.refresh && wh.cpr > 1;   // one CTA per range: its own filter is current
+            w.refresh = pl->kn.refresh && wh.cpr > 1 && l >= pl->kn.refresh_lmin;   // one CTA per range: its own filter is current
             w.fin_spin = pl->kn.fin_wait != 0 ? (1 << 22) : 0;
             // only the range's last merged CTAs (~512 outputs each) wait — for the range's other
             // CTAs, and with a peer exchange for the other ranks' partials — and share the
