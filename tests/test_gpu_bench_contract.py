@@ -48,3 +48,28 @@ def test_reference_arm_line():
     d = _run(["--impl", "reference", "--steps", "1", "--warmup", "0", "--workload", "cfg2"])
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+def test_bench_torchrun_two_gpus():
+    """Under torchrun (N = 2, one rank per GPU) rank 0 prints one line for the whole job:
+    n_gpus 2, weak scaling (each rank plans its own profile), value summed over the ranks
+    (needs >= 2 GPUs)."""
+    import socket
+    import torch
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--steps", "3", "--warmup", "3", "--workload", "cfg3"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["config"]["workload"] == "cfg3"
+    cells = d["config"]["cells_per_step"]
+    assert abs(d["value"] - cells / (d["ms_per_step"] / 1e3)) < 1e-6 * d["value"]
+    assert d["clocks"]["reasons"] == [] or isinstance(d["clocks"]["reasons"], list)
